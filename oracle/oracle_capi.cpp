@@ -62,7 +62,14 @@ struct MarkovModels {
 // reference cli.cpp:120-146 (build_models): noise seed = child_seed(seed, 1).
 MarkovModels build_markov(const json& lm) {
   MarkovModels m;
-  const auto seed = lm.at("seed").get<std::uint64_t>();
+  const auto seed = lm.value("seed", std::uint64_t(0));
+  if (lm.contains("target_rows")) {  // hand-built tables (reference test fixtures)
+    const auto tr = lm.at("target_rows").get<std::vector<Row>>();
+    const auto dr = lm.value("draft_rows", tr);
+    m.target = std::make_unique<MarkovLM>(int(tr[0].size()), lm.at("order").get<int>(), seed, tr);
+    m.draft = std::make_unique<MarkovLM>(int(dr[0].size()), lm.at("order").get<int>(), seed, dr);
+    return m;
+  }
   m.target = std::make_unique<MarkovLM>(markov_make(lm.at("vocab").get<int>(), lm.at("order").get<int>(),
                                                     lm.at("concentration").get<double>(), seed));
   const std::uint64_t noise = lm.value("noise_seed", child_seed(seed, 1));
@@ -99,6 +106,7 @@ PairParams parse_pair(const json& j) {
   p.seed = j.value("seed", p.seed);
   p.embed_scale = j.value("embed_scale", p.embed_scale);
   p.block_out_scale = j.value("block_out_scale", p.block_out_scale);
+  p.shared_mlp_scale = j.value("shared_mlp_scale", p.shared_mlp_scale);
   p.target_private_embed = j.value("target_private_embed", p.target_private_embed);
   p.target_private_head = j.value("target_private_head", p.target_private_head);
   p.draft_gain_mix = j.value("draft_gain_mix", p.draft_gain_mix);
@@ -201,8 +209,15 @@ json run(const json& req) {
     const Scheme s = parse_scheme(req.value("scheme", json()));
     const int K = req.at("lookahead");
     const auto ctx = req.at("context").get<std::vector<int>>();
-    Rng dr(req.at("draft_seed").get<std::uint64_t>());
-    Spec spec = draft_tokens(*m.draft, ctx, K, s, dr, req.value("origin", 0) ? Origin::Backup : Origin::Primary);
+    Spec spec;
+    if (req.contains("spec")) {  // explicit speculation (tokens + recorded dists)
+      spec.tokens = req.at("spec").at("tokens").get<std::vector<int>>();
+      spec.dists = req.at("spec").at("dists").get<std::vector<Row>>();
+      spec.origin = req.value("origin", 0) ? Origin::Backup : Origin::Primary;
+    } else {
+      Rng dr(req.at("draft_seed").get<std::uint64_t>());
+      spec = draft_tokens(*m.draft, ctx, K, s, dr, req.value("origin", 0) ? Origin::Backup : Origin::Primary);
+    }
     json o;
     o["spec"] = spec_json(spec, req.value("with_dists", false));
     if (op == "verify") {
@@ -288,8 +303,8 @@ int oracle_tf_create(const char* request) {
     const PairParams pp = parse_pair(j.value("pair", json::object()));
     const int threads = j.value("threads", 0);
     TfPair p;
-    p.target = std::make_unique<TransformerLM>(ts, ds.d, pp, Role::Target, threads);
-    p.draft = std::make_unique<TransformerLM>(ds, ds.d, pp, Role::Draft, threads);
+    p.target = std::make_unique<TransformerLM>(ts, ds, pp, Role::Target, threads);
+    p.draft = std::make_unique<TransformerLM>(ds, ds, pp, Role::Draft, threads);
     std::lock_guard<std::mutex> g(g_mu);
     g_pairs[g_next] = std::move(p);
     return g_next++;

@@ -54,7 +54,19 @@ struct Pair {
 // Mirrors cli.cpp build_models (noise seed derive_seed(seed, 1)).
 Pair models_of(const json& lmj) {
   Pair p;
-  const auto seed = lmj.at("seed").get<std::uint64_t>();
+  const auto seed = lmj.value("seed", std::uint64_t(0));
+  if (lmj.contains("target_rows")) {  // hand-built tables (reference test fixtures)
+    auto rows = [](const json& j) {
+      std::vector<dist::Logits> r;
+      for (const auto& x : j) r.push_back(dist::Logits{x.get<std::vector<double>>()});
+      return r;
+    };
+    const json dr = lmj.value("draft_rows", lmj.at("target_rows"));
+    const int order = lmj.at("order");
+    p.target = std::make_shared<lm::SyntheticLM>(int(lmj.at("target_rows")[0].size()), order, seed, rows(lmj.at("target_rows")));
+    p.draft = std::make_shared<lm::SyntheticLM>(int(dr[0].size()), order, seed, rows(dr));
+    return p;
+  }
   p.target = std::make_shared<lm::SyntheticLM>(lm::make_lm(lmj.at("vocab").get<int>(), lmj.at("order").get<int>(),
                                                            lmj.at("concentration").get<double>(), seed));
   const std::uint64_t noise = lmj.value("noise_seed", rng::derive_seed(seed, 1));
@@ -126,9 +138,15 @@ json run(const json& req) {
     const auto s = scheme_of(req.value("scheme", json()));
     const int K = req.at("lookahead");
     const auto ctx = req.at("context").get<std::vector<int>>();
-    rng::Stream dr(req.at("draft_seed").get<std::uint64_t>());
-    const specdec::Speculation spec = specdec::draft(*m.draft, ctx, K, s, dr,
-                                                     req.value("origin", 0) ? specdec::Origin::Backup : specdec::Origin::Primary);
+    specdec::Speculation spec;
+    if (req.contains("spec")) {
+      spec.tokens = req.at("spec").at("tokens").get<std::vector<int>>();
+      for (const auto& d : req.at("spec").at("dists")) spec.draft_dists.push_back(dist::Categorical{d.get<std::vector<double>>()});
+      spec.origin = req.value("origin", 0) ? specdec::Origin::Backup : specdec::Origin::Primary;
+    } else {
+      rng::Stream dr(req.at("draft_seed").get<std::uint64_t>());
+      spec = specdec::draft(*m.draft, ctx, K, s, dr, req.value("origin", 0) ? specdec::Origin::Backup : specdec::Origin::Primary);
+    }
     json o;
     o["spec"] = {{"tokens", spec.tokens}, {"origin", int(spec.origin)}};
     if (req.value("with_dists", false)) {

@@ -125,22 +125,40 @@ void rope_tables(const TfShape& s, std::vector<float>& cs, std::vector<float>& s
 
 namespace {
 
-void fill(Pool& pool, std::vector<std::uint16_t>& dst, std::uint64_t key, std::size_t n, float scale) {
-  dst.resize(n);
-  pool.run(long(n), [&](long b, long e) {
-    for (long i = b; i < e; ++i) dst[std::size_t(i)] = to_bf16(unit_value(key, std::uint64_t(i)) * scale);
-  });
-}
-
 float sign_of(std::uint64_t key, std::size_t i) { return unit_value(key, i) < 0.f ? -1.f : 1.f; }
+
+// Input width of a layer tensor (its row length).
+std::size_t in_dim(const TfShape& s, TensorKind k) {
+  if (k == WO) return std::size_t(s.heads) * std::size_t(s.head_dim);
+  if (k == WD) return std::size_t(s.ffn);
+  return std::size_t(s.d);
+}
 
 }  // namespace
 
+// Logical layer-tensor element, bf16 bits. The target's
+// layer-0 MLP embeds the draft's layer-0 MLP in its [ffn_d x d_d] corner.
+std::uint16_t layer_elem(const TfShape& self, const TfShape& draft, const PairParams& p, Role role, int l,
+                         TensorKind k, std::size_t r, std::size_t c) {
+  if (role == Role::Target && l == 0) {
+    if ((k == WG || k == WU) && r < std::size_t(draft.ffn) && c < std::size_t(draft.d))
+      return layer_elem(draft, draft, p, Role::Draft, 0, k, r, c);
+    if (k == WD && r < std::size_t(draft.d) && c < std::size_t(draft.ffn))
+      return layer_elem(draft, draft, p, Role::Draft, 0, k, r, c);
+  }
+  const std::size_t in = in_dim(self, k);
+  float scale = 1.0f / std::sqrt(float(in));
+  if (k == WO) scale = p.block_out_scale * scale;
+  if (k == WD) scale = ((role == Role::Draft && l == 0) ? p.shared_mlp_scale : p.block_out_scale) * scale;
+  return to_bf16(unit_value(tensor_key(p.seed, layer_tensor_id(role, l, k)), r * in + c) * scale);
+}
+
 // ------------------------------------------------------------ model
-TransformerLM::TransformerLM(const TfShape& s, int ds, const PairParams& p, Role role, int threads)
+TransformerLM::TransformerLM(const TfShape& s, const TfShape& dr, const PairParams& p, Role role, int threads)
     : s_(s), threads_(threads > 0 ? threads : int(std::max(1u, std::thread::hardware_concurrency()))) {
-  if (ds > s.d) throw Error("TransformerLM: shared dim exceeds d_model");
-  if (role == Role::Draft && (ds != s.d || !s.tied)) throw Error("TransformerLM: draft must be tied with shared_dim == d");
+  const int ds = dr.d;
+  if (ds > s.d || dr.ffn > s.ffn) throw Error("TransformerLM: draft backbone exceeds the target");
+  if (role == Role::Draft && (ds != s.d || !s.tied)) throw Error("TransformerLM: draft must be tied");
   Pool& pool = pool_for(threads_);
   const std::size_t V = std::size_t(s.vocab), d = std::size_t(s.d);
   const std::uint64_t kS = tensor_key(p.seed, kSharedEmbed);
@@ -163,32 +181,40 @@ TransformerLM::TransformerLM(const TfShape& s, int ds, const PairParams& p, Role
       }
     }
   });
-  // final norm gain
+  // norm gains
   final_gain_.resize(d);
+  ffn_gain0_.assign(d, 1.0f);
   const std::uint64_t kGS = tensor_key(p.seed, kGainShared), kGN = tensor_key(p.seed, kGainNoise),
                       kGT = tensor_key(p.seed, kGainTargetPriv);
+  const float comp = std::sqrt(float(ds) / float(s.d));  // rms over d vs d_draft
   for (std::size_t i = 0; i < d; ++i) {
     if (role == Role::Draft) {
       final_gain_[i] = (1.0f - p.draft_gain_mix) * sign_of(kGS, i) + p.draft_gain_mix * sign_of(kGN, i);
     } else {
       final_gain_[i] = i < std::size_t(ds) ? sign_of(kGS, i) : sign_of(kGT, i - std::size_t(ds));
+      if (i < std::size_t(ds)) ffn_gain0_[i] = comp;
     }
   }
   // blocks
   const int qd = s.heads * s.head_dim, kvd = s.kv_heads * s.head_dim;
-  const float in_d = 1.0f / std::sqrt(float(s.d)), in_q = 1.0f / std::sqrt(float(qd)),
-              in_f = 1.0f / std::sqrt(float(s.ffn));
   layers_.resize(std::size_t(s.layers));
   for (int l = 0; l < s.layers; ++l) {
     Layer& L = layers_[std::size_t(l)];
-    auto key = [&](TensorKind k) { return tensor_key(p.seed, layer_tensor_id(role, l, k)); };
-    fill(pool, L.wq, key(WQ), std::size_t(qd) * d, in_d);
-    fill(pool, L.wk, key(WK), std::size_t(kvd) * d, in_d);
-    fill(pool, L.wv, key(WV), std::size_t(kvd) * d, in_d);
-    fill(pool, L.wo, key(WO), d * std::size_t(qd), p.block_out_scale * in_q);
-    fill(pool, L.wg, key(WG), std::size_t(s.ffn) * d, in_d);
-    fill(pool, L.wu, key(WU), std::size_t(s.ffn) * d, in_d);
-    fill(pool, L.wd, key(WD), d * std::size_t(s.ffn), p.block_out_scale * in_f);
+    auto fill = [&](std::vector<std::uint16_t>& dst, TensorKind k, std::size_t rows) {
+      const std::size_t cols = in_dim(s, k);
+      dst.resize(rows * cols);
+      pool.run(long(rows), [&](long rb, long re) {
+        for (std::size_t r = std::size_t(rb); r < std::size_t(re); ++r)
+          for (std::size_t c = 0; c < cols; ++c) dst[r * cols + c] = layer_elem(s, dr, p, role, l, k, r, c);
+      });
+    };
+    fill(L.wq, WQ, std::size_t(qd));
+    fill(L.wk, WK, std::size_t(kvd));
+    fill(L.wv, WV, std::size_t(kvd));
+    fill(L.wo, WO, d);
+    fill(L.wg, WG, std::size_t(s.ffn));
+    fill(L.wu, WU, std::size_t(s.ffn));
+    fill(L.wd, WD, d);
   }
   rope_tables(s, cos_, sin_);
   kc_.assign(std::size_t(s.layers), {});
@@ -309,7 +335,7 @@ void TransformerLM::step(int token, int pos) {
     }
     gemv(L.wo, d, qd, att_.data(), tmp_.data());
     for (int i = 0; i < d; ++i) x_[std::size_t(i)] += tmp_[std::size_t(i)];
-    rmsnorm_bf16(x_.data(), nullptr, d, s_.norm_eps, hb_.data());
+    rmsnorm_bf16(x_.data(), l == 0 ? ffn_gain0_.data() : nullptr, d, s_.norm_eps, hb_.data());
     gemv(L.wg, s_.ffn, d, hb_.data(), g_.data());
     gemv(L.wu, s_.ffn, d, hb_.data(), u_.data());
     for (int i = 0; i < s_.ffn; ++i) {

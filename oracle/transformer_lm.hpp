@@ -28,15 +28,19 @@ struct TfShape {
   int max_ctx = 4096;
 };
 
-// Correlated random pair: a shared table S gives both
-// models the same bigram backbone; `draft_gain_mix` blends the draft's final
-// norm gain toward independent signs, the knob calibrated like
-// lm::calibrate_pair (lm.cpp:150-172).
+// Correlated random pair. Both models share a backbone: the
+// draft's tied table S (embedding and head over the first d_draft dims) and
+// the draft's layer-0 MLP, replicated inside the target's layer-0 MLP. All
+// other blocks are independent random weights at output scale beta, which
+// is what makes the pair disagree; `draft_gain_mix` blends the draft's final
+// norm gain toward independent signs (the knob, like lm::calibrate_pair,
+// lm.cpp:150-172).
 struct PairParams {
   std::uint64_t seed = 20250809;
   float embed_scale = 1.0f;
-  float block_out_scale = 0.5f;      // beta: scale of wo / w_down
-  float target_private_embed = 1.0f; // rho
+  float shared_mlp_scale = 8.0f;     // gamma: output scale of the shared layer-0 MLP
+  float block_out_scale = 0.1f;      // beta: output scale of every other wo / w_down
+  float target_private_embed = 0.1f; // rho
   float target_private_head = 0.25f; // q
   float draft_gain_mix = 0.0f;       // epsilon
 };
@@ -52,6 +56,8 @@ float from_bf16(std::uint16_t b);
 // Logical tensor ids.
 enum TensorKind : std::uint32_t { WQ = 0, WK, WV, WO, WG, WU, WD, NKIND };
 std::uint32_t layer_tensor_id(Role r, int layer, TensorKind k);
+struct PairParams;
+struct TfShape;
 constexpr std::uint32_t kSharedEmbed = 0xE0000001u, kTargetPrivEmbed = 0xE0000002u,
                         kTargetPrivHead = 0xE0000003u, kGainShared = 0xE0000004u,
                         kGainNoise = 0xE0000005u, kGainTargetPriv = 0xE0000006u;
@@ -62,8 +68,9 @@ void rope_tables(const TfShape& s, std::vector<float>& cos_t, std::vector<float>
 
 class TransformerLM : public LanguageModel {
  public:
-  // shared_dim: width of the shared backbone (the draft's d_model).
-  TransformerLM(const TfShape& shape, int shared_dim, const PairParams& p, Role role, int threads = 0);
+  // draft: the draft's shape (the shared backbone's width and ffn); for the
+  // draft itself pass its own shape.
+  TransformerLM(const TfShape& shape, const TfShape& draft, const PairParams& p, Role role, int threads = 0);
   int vocab() const override { return s_.vocab; }
   std::span<const double> logits(std::span<const int> ctx) override;
   // fp32 logits of the last call (what the GPU engine produces).
@@ -89,6 +96,8 @@ class TransformerLM : public LanguageModel {
   std::vector<std::uint16_t> embed_, head_;       // head_ empty when tied
   std::vector<Layer> layers_;
   std::vector<float> final_gain_;
+  std::vector<float> ffn_gain0_;                  // layer-0 ffn norm gain
+
   std::vector<float> cos_, sin_;
   // KV cache (bf16 values held as float) [layer][pos][kv_heads*head_dim]
   std::vector<std::vector<float>> kc_, vc_;
