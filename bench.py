@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""Batch-1 Saguaro (SSD) decode benchmark on B200 — BASELINE.json's metric
+(batch-1 decode tokens/sec + speedup vs AR and SD; cache hit rate; HBM GB/s).
+
+Workload (N=1): BASELINE.json configs[1] shapes — Llama-3.1-8B target +
+Llama-3.2-1B draft, random-init correlated pair, greedy, lookahead K=4,
+fan-out 4 at every position (20 branches), FastRandom backup, batch 1;
+verifier and speculator on two streams of one GPU (SURVEY §8e "1-GPU
+colocated"). A step = one decode of `--rounds` SSD rounds from a 128-token
+synthetic prompt. N>1: independent replicas, one per GPU ("weak").
+
+`--impl reference` times the reference algorithm on host cores instead:
+the CPU oracle port of run_protocol_harness over the same transformer pair
+(oracle/, test infrastructure), a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(args):
+    import paper_2603_03251_b200 as P
+    from paper_2603_03251_b200.configs import shapes
+    ts, ds = shapes(args.config, max_ctx=args.max_ctx)
+    K = args.lookahead
+    fan = [args.fanout] * (K + 1)
+    temp = 0.0 if args.greedy else args.temperature
+    cfg = P.SimConfig(lookahead=K, scheme=P.SamplingScheme.standard(temp),
+                      primary_plan=P.FanOutPlan(list(fan), P.PRIMARY), backup_plan=P.FanOutPlan(list(fan), P.BACKUP),
+                      primary_time=0.4, backup_time=0.0, backup_kind=P.FAST_RANDOM, rounds=args.rounds, seed=args.seed)
+    import numpy as np
+    prompt = np.random.default_rng(args.seed).integers(0, ts.vocab, args.prompt_len).tolist()
+    return P, ts, ds, cfg, prompt, fan, temp
+
+
+def cpu_sample(args, threads, rounds):
+    """The reference algorithm (oracle port of run_protocol_harness) on host
+    cores over the same transformer pair; `rounds` SSD rounds."""
+    import pyoracle
+    import psutil
+    P, ts, ds, cfg, prompt, fan, temp = workload(args)
+    shp = args.config
+    need = 2.2 * (P.api.shape_dict(ts)["vocab"] * ts.d_model * 2 + 2 * ts.vocab * ts.d_model) / 1e9
+    t_bytes = 2 * (ts.n_layers * (ts.d_model * (ts.n_heads + 2 * ts.n_kv_heads) * ts.head_dim +
+                                  ts.d_model * ts.n_heads * ts.head_dim + 3 * ts.d_model * ts.ffn) +
+                   2 * ts.vocab * ts.d_model)
+    d_bytes = 2 * (ds.n_layers * (ds.d_model * (ds.n_heads + 2 * ds.n_kv_heads) * ds.head_dim +
+                                  ds.d_model * ds.n_heads * ds.head_dim + 3 * ds.d_model * ds.ffn) +
+                   ds.vocab * ds.d_model)
+    need = 1.3 * (t_bytes + d_bytes)
+    avail = psutil.virtual_memory().available
+    if need > avail:
+        shp = "tiny"
+        args = argparse.Namespace(**{**vars(args), "config": "tiny"})
+        P, ts, ds, cfg, prompt, fan, temp = workload(args)
+    t0 = time.perf_counter()
+    pair = pyoracle.TfPair(P.shape_dict(ts), P.shape_dict(ds), P.Pair().as_dict(), threads=threads)
+    build_s = time.perf_counter() - t0
+    req = {"op": "simulate", "mode": "harness", "lookahead": cfg.lookahead, "rounds": rounds, "seed": cfg.seed,
+           "prompt": prompt, "scheme": {"temperature": temp}, "primary_plan": {"fan": fan},
+           "backup_plan": {"fan": fan}, "timing": {"primary_time": 0.4}}
+    t0 = time.perf_counter()
+    out = pair.call(req)
+    dt = time.perf_counter() - t0
+    pair.close()
+    return {"tokens": out["tokens"], "seconds": dt, "config": shp, "build_s": build_s, "rounds": rounds}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    P, ts, ds, cfg, prompt, fan, temp = workload(args)
+    toks, secs, cfg_used = 0, 0.0, args.config
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(args, threads, rounds=1)
+        if i >= args.warmup:
+            toks += s["tokens"]
+            secs += s["seconds"]
+            cfg_used = s["config"]
+    v = toks / secs if secs > 0 else 0.0
+    line = {"impl": "reference", "metric": "batch-1 decode tokens/sec (SSD)", "value": v, "unit": "tokens/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 weights, fp32 compute", "data": "synthetic",
+            "config": {"workload": f"{cfg_used} ssd harness greedy K={cfg.lookahead} F={args.fanout} batch1",
+                       "prompt_len": args.prompt_len},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+                             "sample": f"1 SSD round per step of the oracle run_protocol_harness port on {cfg_used}"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    P, ts, ds, cfg, prompt, fan, temp = workload(args)
+    B = sum(fan)
+    eng = P.Engine(ts, ds, P.Pair(), device=local, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.run_ssd(prompt, cfg)
+    barrier()
+    runs, walls = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = eng.run_ssd(prompt, cfg)
+            walls.append(time.perf_counter() - t0)
+            runs.append(r)
+    barrier()
+    tokens = sum(r.tokens for r in runs)
+    dev_ms = sum(r.device_ms for r in runs)
+    wall = sum(walls)
+    launches = sum(r.kernel_launches for r in runs) // max(1, len(runs))
+    if ws > 1:
+        t = torch.tensor([dev_ms, wall], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, wall = float(t[0]), float(t[1])
+    value = ws * tokens / (dev_ms * 1e-3)
+    e2e = ws * tokens / wall
+    # baselines on the same box: AR and synchronous SD, same token budget
+    ar = eng.run_ar(prompt, cfg.target_scheme or P.SamplingScheme.standard(temp), max(16, tokens // len(runs)),
+                    cfg.seed)
+    sd = eng.run_sd(prompt, cfg)
+    ar_tps = ar.tokens / (ar.device_ms * 1e-3)
+    sd_tps = sd.tokens / (sd.device_ms * 1e-3)
+    ssd_tps = tokens / (dev_ms * 1e-3) * (1 if ws == 1 else 1)
+    # roofline of the dominant kernel (weight-streaming GEMM), timed live
+    prof_t = eng.profile_forward(0, 1, args.prompt_len, 10)
+    prof_b = eng.profile_forward(1, B, args.prompt_len, 10)
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    achieved = prof_t["gemm_bytes"] / (prof_t["ms_gemm"] * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("bytes_per_step")
+    hits = sum(r.hits_total() for r in runs)
+    lookups = sum(r.lookups() for r in runs)
+    acc = sum(r.accepted_sum for r in runs) / sum(r.rounds for r in runs)
+    tw = eng.weight_bytes(0)
+    dw = eng.weight_bytes(1)
+    line = {"metric": "batch-1 decode tokens/sec (SSD)", "value": value, "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / len(runs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init correlated pair, random prompt)",
+            "config": {"workload": f"{args.config} (Llama-3.1-8B/Llama-3.2-1B shapes) ssd greedy K={cfg.lookahead} "
+                                   f"F={args.fanout} batch1 colocated", "prompt_len": args.prompt_len,
+                       "rounds_per_step": args.rounds, "branches": B,
+                       "l2": "no flush: 18 GB of weights streamed per round >> 126 MB L2",
+                       "parallelism": f"replicas{ws}" if ws > 1 else "verifier+speculator streams on 1 GPU"},
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 4 * len(prompt) + 1024,
+                    "d2h_bytes_per_step": 4 * (tokens // len(runs)) + 8 * 3 * args.rounds},
+            "gpu_launches": launches,
+            "ssd_tokens_per_s": ssd_tps, "ar_tokens_per_s": ar_tps, "sd_tokens_per_s": sd_tps,
+            "speedup_vs_ar": ssd_tps / ar_tps, "speedup_vs_sd": ssd_tps / sd_tps,
+            "hit_rate": hits / lookups if lookups else None, "mean_accepted": acc,
+            "tokens_per_round": tokens / sum(r.rounds for r in runs),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "peak_kind": pk_kind,
+                         "kernel": "linear_cc_kernel (weight-streaming GEMV), 8B target decode step M=1",
+                         "bytes_per_step": prof_t["gemm_bytes"], "ms_gemm_per_step": prof_t["ms_gemm"],
+                         "ms_forward_per_step": prof_t["ms_forward"],
+                         "draft_branch_step_ms": prof_b["ms_forward"],
+                         "draft_branch_gemm_gbs": prof_b["gemm_bytes"] / (prof_b["ms_gemm"] * 1e-3) / 1e9},
+            "model_bytes": {"target_step": tw, "draft_step": dw},
+            "clocks": clk.summary()}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        s = cpu_sample(args, os.cpu_count() or 1, rounds=1)
+        line["cpu_baseline"] = {"value": s["tokens"] / s["seconds"], "unit": "tokens/s", "cores": os.cpu_count(),
+                                "kind": "port",
+                                "sample": f"1 SSD round (+initial draft) of the oracle run_protocol_harness port on "
+                                          f"the {s['config']} pair, prompt {args.prompt_len}; model build "
+                                          f"{s['build_s']:.1f}s excluded"}
+    eng.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama8b_1b")
+    ap.add_argument("--rounds", type=int, default=32)
+    ap.add_argument("--lookahead", type=int, default=4)
+    ap.add_argument("--fanout", type=int, default=4)
+    ap.add_argument("--prompt-len", type=int, default=128)
+    ap.add_argument("--max-ctx", type=int, default=1024)
+    ap.add_argument("--temperature", type=float, default=1.0)
+    ap.add_argument("--sampled", dest="greedy", action="store_false")
+    ap.add_argument("--seed", type=int, default=20250809)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.set_defaults(greedy=True)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

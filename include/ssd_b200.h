@@ -1,0 +1,226 @@
+/*
+ * ssd_b200.h — C-ABI of the B200-native Saguaro (speculative speculative
+ * decoding) hot path.
+ *
+ * This is the drop-in boundary for the reference's speculator / verifier /
+ * speculation-cache interfaces (ssd-lab, proj/include/ssdlab). Every entry
+ * point names the reference interface it replaces. Plain C types only: no
+ * torch, no C++ in the signatures. All device work runs on the engine's own
+ * CUDA streams; results are copied back to caller-owned HOST buffers.
+ *
+ * Errors: every call returns an ssd_status; the codes map one-to-one onto
+ * the reference exception hierarchy (errors.hpp:9-61), and ssd_last_error()
+ * returns the message of the last failure on the calling thread. The C++
+ * shim (include/ssdlab_b200.hpp) re-throws the matching ssdlab:: type.
+ *
+ * Randomness: the engine reproduces the reference's stream discipline on the
+ * device — mt19937_64 streams seeded through derive_seed (rng.hpp:24-48),
+ * one uniform per draw, the same consumption order as run_ar / run_sd /
+ * run_protocol_harness (sim.cpp:64-121, 502-601) — so outputs can be
+ * compared with the CPU oracle stream for stream.
+ */
+#ifndef SSD_B200_H_
+#define SSD_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSD_B200_ABI_VERSION 1
+#define SSD_MAX_LOOKAHEAD 16
+
+/* errors.hpp:9-61 (ssdlab::Error and subclasses) */
+typedef enum ssd_status {
+  SSD_OK = 0,
+  SSD_ERROR = 1,                /* ssdlab::Error */
+  SSD_ALL_ZERO = 2,             /* AllZeroError */
+  SSD_DEGENERATE_RESIDUAL = 3,  /* DegenerateResidualError */
+  SSD_TOO_LARGE = 4,            /* TooLargeError */
+  SSD_BUDGET_TOO_SMALL = 5,     /* BudgetTooSmallError */
+  SSD_DIVERGENT = 6,            /* DivergentError */
+  SSD_INSUFFICIENT_DATA = 7,    /* InsufficientDataError */
+  SSD_UNREACHABLE = 8,          /* UnreachableError */
+  SSD_NO_CROSSOVER = 9,         /* NoCrossoverError */
+  SSD_PROTOCOL_VIOLATION = 10,  /* ProtocolViolationError */
+  SSD_CONFIG = 11,              /* ConfigError */
+  SSD_CUDA = 100                /* CUDA runtime failure (no reference analogue) */
+} ssd_status;
+
+const char* ssd_last_error(void);
+int ssd_abi_version(void);
+
+/* ---------------------------------------------------------------- types */
+
+/* Llama-style decoder shape. Replaces the reference's model parameter
+ * (lm::SyntheticLM, lm.hpp:12-47) with a transformer resident on the GPU. */
+typedef struct ssd_model_shape {
+  int32_t vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn;
+  int32_t tied;    /* embedding doubles as LM head */
+  int32_t max_ctx; /* KV capacity in tokens */
+  double rope_theta;
+  float norm_eps;
+} ssd_model_shape;
+
+/* Correlated random pair; the analogue of
+ * lm::derive_draft / calibrate_pair (lm.hpp:55-90). */
+typedef struct ssd_pair_params {
+  uint64_t seed;
+  float embed_scale, shared_mlp_scale, block_out_scale;
+  float target_private_embed, target_private_head, draft_gain_mix;
+} ssd_pair_params;
+
+/* dist::SamplingScheme (categorical.hpp:43-60). temperature == 0 selects
+ * greedy decoding (the tau -> 0 limit; argmax with lowest-index ties). */
+typedef struct ssd_scheme {
+  int32_t kind; /* 0 = Standard, 1 = Saguaro */
+  int32_t fan_out;
+  double temperature;
+  double downweight;
+} ssd_scheme;
+
+/* cache::FanOutPlan (cache.hpp:18-25) */
+typedef struct ssd_plan {
+  int32_t lookahead;
+  int32_t role; /* 0 = Primary, 1 = Backup */
+  int32_t budget;
+  int32_t fan_out[SSD_MAX_LOOKAHEAD + 1];
+} ssd_plan;
+
+/* sim::SimConfig (sim.hpp:28-53), minus the models (owned by the engine). */
+typedef struct ssd_sim_config {
+  int32_t lookahead;
+  ssd_scheme scheme;
+  ssd_scheme target_scheme;
+  ssd_plan primary_plan;
+  ssd_plan backup_plan;
+  int32_t backup_kind;  /* 0 = SamePrimaryJIT, 1 = FastRandom (sim.hpp:17-20) */
+  double primary_time, backup_time;
+  int64_t rounds;
+  uint64_t seed;
+  double accept_scale;
+} ssd_sim_config;
+
+/* sim::RunStats (sim.hpp:55-104) plus measured device time. */
+typedef struct ssd_run_stats {
+  int64_t rounds, tokens;
+  double virtual_time;
+  int64_t primary_origin_lookups, primary_origin_hits;
+  int64_t backup_origin_lookups, backup_origin_hits;
+  int64_t hit_rounds, miss_rounds, initial_rounds;
+  int64_t hit_round_tokens, miss_round_tokens;
+  double accepted_sum;
+  double device_ms;     /* CUDA-event time of the decode loop (prefill excluded) */
+  int64_t kernel_launches; /* engine kernels launched inside the timed loop */
+} ssd_run_stats;
+
+typedef struct ssd_engine ssd_engine;
+
+/* ------------------------------------------------- plans (host-only) */
+
+/* cache::geometric_fanout (cache.hpp:57-60, cache.cpp:39-113). */
+ssd_status ssd_geometric_fanout(double acceptance, double exponent, int32_t lookahead, int32_t budget,
+                                int32_t role, ssd_plan* out);
+/* cache::uniform_fanout (cache.hpp:62-64, cache.cpp:115-127). */
+ssd_status ssd_uniform_fanout(int32_t lookahead, int32_t budget, int32_t role, ssd_plan* out);
+/* cache::conditional_hit_rate (cache.hpp:79-85, cache.cpp:150-169). */
+double ssd_conditional_hit_rate(const ssd_plan* plan, double acceptance, double exponent);
+
+/* --------------------------------------------------------------- engine */
+
+/* Materialise the (target, draft) pair on `device` with synthetic weights
+ * (bit-identical to the CPU oracle's generator) and allocate KV caches for
+ * up to `max_branches` pre-speculation branches. */
+ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shape* draft,
+                             const ssd_pair_params* pair, int32_t device, int32_t max_branches,
+                             int32_t max_lookahead, ssd_engine** out);
+ssd_status ssd_engine_destroy(ssd_engine* e);
+/* Bytes of weights streamed per forward step of model `which` (0 target,
+ * 1 draft): the algorithmic bytes of one decode step. */
+int64_t ssd_engine_weight_bytes(const ssd_engine* e, int32_t which);
+
+/* ------------------------------------------------- decode loops (sim.hpp) */
+
+/* sim::run_ar (sim.cpp:64-86): `tokens` autoregressive target samples. */
+ssd_status ssd_run_ar(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
+                      const ssd_scheme* target_scheme, int64_t tokens, uint64_t seed,
+                      int32_t* out_tokens, int64_t out_capacity, ssd_run_stats* stats);
+
+/* sim::run_sd (sim.cpp:88-121): draft K, verify, repeat. */
+ssd_status ssd_run_sd(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
+                      const ssd_sim_config* cfg, int32_t* out_tokens, int64_t out_capacity,
+                      int64_t* out_len, ssd_run_stats* stats);
+
+/* sim::run_protocol_harness (sim.cpp:502-601): the Saguaro loop. The
+ * speculator pre-speculates every predicted outcome while the verifier
+ * verifies; one message pair per round (v2d outcome, d2v speculation).
+ * Per-round outcomes (k, t*) and hit bits of the sequence are written to
+ * out_outcomes[2*r..2*r+1] / out_hits[r] when non-NULL. */
+ssd_status ssd_run_ssd(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
+                       const ssd_sim_config* cfg, int32_t* out_tokens, int64_t out_capacity,
+                       int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits,
+                       ssd_run_stats* stats);
+
+/* ------------------------------------------ single operations (specdec.hpp,
+ * cache.hpp). Each starts from `context` (prefilled into the model's KV). */
+
+/* lm::SyntheticLM::logits_at (lm.cpp:82-84): fp32 logits after `context`. */
+ssd_status ssd_logits(ssd_engine* e, int32_t which, const int32_t* context, int32_t n,
+                      float* out_logits);
+
+/* specdec::draft (specdec.hpp:59-61): K tokens drawn from the draft under
+ * `scheme` with stream Stream(seed); fp32 draft logit rows [K][V] copied out
+ * when out_rows != NULL. */
+ssd_status ssd_draft(ssd_engine* e, const int32_t* context, int32_t n, int32_t lookahead,
+                     const ssd_scheme* scheme, uint64_t seed, int32_t* out_tokens, float* out_rows);
+
+/* cache::build_cache + SpeculationCache::lookup key set (cache.hpp:149-154,
+ * 123-126): the pre-speculation of the in-flight `spec_tokens` drafted from
+ * `context`. Writes the Σ F_k keys (k, t) in ordinal order to out_keys[2i..]
+ * and each entry's next_lookahead tokens to out_entry_tokens[i*next_K ..].
+ * `base_seed` stands for the one draw the reference takes from the caller's
+ * stream (cache.cpp:245). */
+ssd_status ssd_build_cache(ssd_engine* e, const int32_t* context, int32_t n,
+                           const int32_t* spec_tokens, int32_t lookahead, const ssd_plan* plan,
+                           const ssd_scheme* scheme, int32_t next_lookahead, uint64_t base_seed,
+                           int32_t* out_keys, int32_t* out_entry_tokens, int32_t* out_count);
+
+/* ------------------------------------------- kernel-level parity hooks
+ * (host buffers in, host buffers out; used by tests/). */
+
+/* Candidate keys from draft logit rows (cache.cpp:249-270): for each row k,
+ * the first fan_out[k] tokens of the (value desc, index asc) order that are
+ * not excluded[k] (-1 = no exclusion). Writes keys[k*max_f + j]. */
+ssd_status ssd_topk_keys(ssd_engine* e, const float* rows, int32_t n_rows, int32_t vocab,
+                         const int32_t* fan_out, const int32_t* excluded, int32_t max_f,
+                         int32_t* keys);
+
+/* specdec::verify decision (specdec.cpp:27-69) on given logits: target rows
+ * [K+1][V], draft rows [K][V] (NULL = uniform dists, the FastRandom backup),
+ * drafted tokens [K], verifier stream Stream(seed). Writes (accepted, bonus). */
+ssd_status ssd_verify_rows(ssd_engine* e, const float* target_rows, const float* draft_rows,
+                           const int32_t* tokens, int32_t lookahead, int32_t vocab,
+                           const ssd_scheme* draft_scheme, const ssd_scheme* target_scheme,
+                           double accept_scale, uint64_t seed, int32_t* accepted, int32_t* bonus);
+
+/* Roofline hook (bench.py): times `iters` forward steps of model `which`
+ * over M tokens at context position `pos` with CUDA events on the engine
+ * stream, and separately the step's weight-streaming GEMM launches alone.
+ * Outputs average ms per step / per step's GEMM launches and the GEMM
+ * launches' algorithmic bytes (weights + activations) per step. */
+ssd_status ssd_profile_forward(ssd_engine* e, int32_t which, int32_t M, int32_t pos, int32_t iters,
+                               double* ms_forward, double* ms_gemm, int64_t* gemm_bytes, int32_t* gemm_launches);
+
+/* mt19937_64 parity: n outputs of Stream(seed).next_u64() computed on the GPU. */
+ssd_status ssd_rng_u64(ssd_engine* e, uint64_t seed, int32_t n, uint64_t* out);
+
+/* Weight-generator parity: bf16 bits of logical elements (kind 0..6 = q,k,v,
+ * o,gate,up,down of `layer`; 100 = embedding; 101 = LM head). */
+ssd_status ssd_weight_bits(ssd_engine* e, int32_t which, int32_t layer, int32_t kind,
+                           const int64_t* rows, const int64_t* cols, int32_t n, uint16_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSD_B200_H_ */

@@ -204,6 +204,51 @@ json run(const json& req) {
     for (int i = 0; i < req.value("n", 1); ++i) out.push_back(draw(p, r));
     return json{{"draws", out}};
   }
+  if (op == "verify_rows") {
+    // specdec.cpp:27-69 on given logit rows: target row i is the target's
+    // logits after ctx ++ s_1..s_i; draft rows give the recorded laws (absent
+    // => the exact uniform law of the FastRandom backup, sim.cpp:35-48).
+    struct RowsLM : LanguageModel {
+      std::vector<Row> rows;
+      int vocab() const override { return int(rows[0].size()); }
+      std::span<const double> logits(std::span<const int> ctx) override { return rows.at(ctx.size() - 1); }
+    } lm;
+    lm.rows = req.at("target_rows").get<std::vector<Row>>();
+    const auto toks = req.at("tokens").get<std::vector<int>>();
+    const Scheme ds = parse_scheme(req.value("scheme", json()));
+    Spec spec;
+    spec.tokens = toks;
+    if (req.contains("draft_rows")) {
+      for (const auto& r : req.at("draft_rows")) spec.dists.push_back(scheme_probs(r.get<Row>(), ds));
+    } else {
+      spec.dists.assign(toks.size(), Row(lm.rows[0].size(), 1.0 / double(lm.rows[0].size())));
+    }
+    VerifyOpts vo;
+    vo.target_scheme = parse_scheme(req.value("target_scheme", json()));
+    vo.accept_scale = req.value("accept_scale", 1.0);
+    Rng r(req.at("seed").get<std::uint64_t>());
+    const std::vector<int> ctx{0};
+    const Round out = verify_spec(lm, ctx, spec, r, vo);
+    return json{{"accepted", out.key.k}, {"bonus", out.key.t}};
+  }
+  if (op == "keys_rows") {
+    // cache.cpp:249-270 key selection on given rows.
+    const auto rows = req.at("rows").get<std::vector<Row>>();
+    const auto fan = req.at("fan").get<std::vector<int>>();
+    const auto excl = req.at("excluded").get<std::vector<int>>();
+    json keys = json::array();
+    for (std::size_t k = 0; k < rows.size(); ++k) {
+      std::vector<int> got;
+      const int need = std::min(int(rows[k].size()), fan[k] + 1);
+      for (int c : rank_tokens(rows[k], need)) {
+        if (c == excl[k]) continue;
+        if (int(got.size()) == fan[k]) break;
+        got.push_back(c);
+      }
+      keys.push_back(got);
+    }
+    return json{{"keys", keys}};
+  }
   Models m = resolve(req);
   if (op == "draft" || op == "verify" || op == "build_cache") {
     const Scheme s = parse_scheme(req.value("scheme", json()));

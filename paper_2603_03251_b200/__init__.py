@@ -1,0 +1,12 @@
+"""B200-native Saguaro (speculative speculative decoding) hot path.
+
+The product is the native library libssd_b200.so (include/ssd_b200.h): CUDA
+kernels for sm_100a plus the C++ round loops. This package is the thin
+Python mirror of the reference's interface used by tests and bench.py.
+"""
+from .api import (  # noqa: F401
+    BACKUP, FAST_RANDOM, PRIMARY, SAME_PRIMARY_JIT, AllZeroError, BudgetTooSmallError, ConfigError, CudaError,
+    DegenerateResidualError, DivergentError, Engine, Error, FanOutPlan, InsufficientDataError, NoCrossoverError, Pair,
+    ProtocolViolationError, RunStats, SamplingScheme, SimConfig, Speculation, SpeculationCache, TooLargeError,
+    UnreachableError, conditional_hit_rate, geometric_fanout, model_shape, shape_dict, uniform_fanout)
+from .configs import CONFIGS, TINY_DRAFT, TINY_TARGET, LLAMA_1B, LLAMA_8B  # noqa: F401

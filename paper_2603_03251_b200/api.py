@@ -1,0 +1,405 @@
+"""Python mirror of the reference's speculator / verifier / speculation-cache
+interface (ssd-lab proj/include/ssdlab: categorical.hpp, cache.hpp,
+specdec.hpp, sim.hpp, errors.hpp), calling the B200 engine through the C-ABI
+(include/ssd_b200.h). Names, argument meaning and error classes follow the
+reference so the parity tests read like the reference's own tests.
+
+Host code here only marshals arguments; every decode step, verification,
+key selection, lookup and backup runs in the native library on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+# ------------------------------------------------------------------ errors
+# errors.hpp:9-61
+
+
+class Error(RuntimeError):
+    """ssdlab::Error"""
+
+
+class AllZeroError(Error): pass  # noqa: E701
+class DegenerateResidualError(Error): pass  # noqa: E701
+class TooLargeError(Error): pass  # noqa: E701
+class BudgetTooSmallError(Error): pass  # noqa: E701
+class DivergentError(Error): pass  # noqa: E701
+class InsufficientDataError(Error): pass  # noqa: E701
+class UnreachableError(Error): pass  # noqa: E701
+class NoCrossoverError(Error): pass  # noqa: E701
+class ProtocolViolationError(Error): pass  # noqa: E701
+class ConfigError(Error): pass  # noqa: E701
+class CudaError(Error): pass  # noqa: E701
+
+
+_BY_CODE = {1: Error, 2: AllZeroError, 3: DegenerateResidualError, 4: TooLargeError, 5: BudgetTooSmallError,
+            6: DivergentError, 7: InsufficientDataError, 8: UnreachableError, 9: NoCrossoverError,
+            10: ProtocolViolationError, 11: ConfigError, 100: CudaError}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = N.load().ssd_last_error().decode(errors="replace")
+        raise _BY_CODE.get(status, Error)(msg)
+
+
+# ------------------------------------------------------------------ types
+@dataclass(frozen=True)
+class SamplingScheme:
+    """dist::SamplingScheme (categorical.hpp:43-60); temperature 0 = greedy."""
+    kind: str = "standard"
+    temperature: float = 1.0
+    fan_out: int = 0
+    downweight: float = 1.0
+
+    @staticmethod
+    def standard(temperature: float = 1.0) -> "SamplingScheme":
+        return SamplingScheme("standard", temperature)
+
+    @staticmethod
+    def saguaro(fan_out: int, downweight: float, temperature: float = 1.0) -> "SamplingScheme":
+        return SamplingScheme("saguaro", temperature, fan_out, downweight)
+
+    @staticmethod
+    def greedy() -> "SamplingScheme":
+        return SamplingScheme("standard", 0.0)
+
+    def c(self) -> N.Scheme:
+        return N.Scheme(1 if self.kind == "saguaro" else 0, self.fan_out, self.temperature, self.downweight)
+
+
+PRIMARY, BACKUP = 0, 1  # specdec::Origin
+
+
+@dataclass
+class FanOutPlan:
+    """cache::FanOutPlan (cache.hpp:18-25)."""
+    fan_out: list
+    role: int = PRIMARY
+    budget: int = 0
+
+    @property
+    def lookahead(self) -> int:
+        return len(self.fan_out) - 1
+
+    def total(self) -> int:
+        return int(sum(self.fan_out))
+
+    def c(self) -> N.Plan:
+        p = N.Plan()
+        p.lookahead = self.lookahead
+        p.role = self.role
+        p.budget = self.budget or self.total()
+        for k, f in enumerate(self.fan_out):
+            p.fan_out[k] = int(f)
+        return p
+
+
+def _plan_from_c(p: N.Plan) -> FanOutPlan:
+    return FanOutPlan([p.fan_out[k] for k in range(p.lookahead + 1)], p.role, p.budget)
+
+
+def geometric_fanout(acceptance: float, exponent: float, lookahead: int, budget: int, role: int = PRIMARY) -> FanOutPlan:
+    """cache::geometric_fanout (cache.cpp:39-113), evaluated natively."""
+    p = N.Plan()
+    _check(N.load().ssd_geometric_fanout(acceptance, exponent, lookahead, budget, role, C.byref(p)))
+    return _plan_from_c(p)
+
+
+def uniform_fanout(lookahead: int, budget: int, role: int = PRIMARY) -> FanOutPlan:
+    """cache::uniform_fanout (cache.cpp:115-127)."""
+    p = N.Plan()
+    _check(N.load().ssd_uniform_fanout(lookahead, budget, role, C.byref(p)))
+    return _plan_from_c(p)
+
+
+def conditional_hit_rate(plan: FanOutPlan, acceptance: float, exponent: float) -> float:
+    return N.load().ssd_conditional_hit_rate(C.byref(plan.c()), acceptance, exponent)
+
+
+FAST_RANDOM, SAME_PRIMARY_JIT = "fast_random", "same_primary_jit"  # sim::BackupKind
+
+
+@dataclass
+class SimConfig:
+    """sim::SimConfig (sim.hpp:28-53); the models live in the Engine."""
+    lookahead: int = 4
+    scheme: SamplingScheme = field(default_factory=SamplingScheme.standard)
+    target_scheme: Optional[SamplingScheme] = None  # default: standard(scheme.temperature) as cli.cpp:211
+    primary_plan: Optional[FanOutPlan] = None
+    backup_plan: Optional[FanOutPlan] = None
+    primary_time: float = 0.3
+    backup_time: float = 0.0
+    backup_kind: str = FAST_RANDOM
+    rounds: int = 1000
+    seed: int = 0
+    accept_scale: float = 1.0
+
+    def c(self) -> N.SimConfigC:
+        ts = self.target_scheme or SamplingScheme.standard(self.scheme.temperature)
+        pp = self.primary_plan or uniform_fanout(self.lookahead, self.lookahead + 1, PRIMARY)
+        bp = self.backup_plan or FanOutPlan(list(pp.fan_out), BACKUP, pp.budget)
+        return N.SimConfigC(self.lookahead, self.scheme.c(), ts.c(), pp.c(), bp.c(),
+                            0 if self.backup_kind == SAME_PRIMARY_JIT else 1, self.primary_time, self.backup_time,
+                            self.rounds, self.seed, self.accept_scale)
+
+
+@dataclass
+class RunStats:
+    """sim::RunStats (sim.hpp:55-104) plus device time."""
+    rounds: int
+    tokens: int
+    virtual_time: float
+    primary_origin_lookups: int
+    primary_origin_hits: int
+    backup_origin_lookups: int
+    backup_origin_hits: int
+    hit_rounds: int
+    miss_rounds: int
+    initial_rounds: int
+    hit_round_tokens: int
+    miss_round_tokens: int
+    accepted_sum: float
+    device_ms: float
+    kernel_launches: int
+    streams: list = field(default_factory=list)
+    outcomes: Optional[np.ndarray] = None  # [rounds, 2] (accepted, bonus)
+    hits: Optional[np.ndarray] = None      # [rounds] 1/0, -1 on the last round
+
+    @classmethod
+    def _from_c(cls, s: N.RunStatsC, stream=None):
+        return cls(*[getattr(s, f) for f, _ in N.RunStatsC._fields_], streams=[stream] if stream is not None else [])
+
+    def speed(self) -> float:
+        return self.tokens / self.virtual_time
+
+    def lookups(self) -> int:
+        return self.primary_origin_lookups + self.backup_origin_lookups
+
+    def hits_total(self) -> int:
+        return self.primary_origin_hits + self.backup_origin_hits
+
+    def hit_rate(self) -> float:
+        return self.hits_total() / self.lookups() if self.lookups() else 0.0
+
+    def hit_rate_primary(self):
+        return self.primary_origin_hits / self.primary_origin_lookups if self.primary_origin_lookups else None
+
+    def hit_rate_backup(self):
+        return self.backup_origin_hits / self.backup_origin_lookups if self.backup_origin_lookups else None
+
+    def mean_accepted(self) -> float:
+        return self.accepted_sum / self.rounds
+
+    def tokens_per_second(self) -> float:
+        return self.tokens / (self.device_ms * 1e-3) if self.device_ms > 0 else 0.0
+
+
+@dataclass
+class Speculation:
+    """specdec::Speculation (specdec.hpp:22-28): tokens plus the draft logit
+    rows they were drawn from (the recorded laws are the scheme applied to
+    these rows)."""
+    tokens: list
+    rows: Optional[np.ndarray] = None
+    origin: int = PRIMARY
+
+
+@dataclass
+class SpeculationCache:
+    """cache::SpeculationCache (cache.hpp:114-135): (accepted, bonus) -> tokens."""
+    entries: dict
+    round_origin: int = PRIMARY
+
+    def lookup(self, accepted: int, bonus: int):
+        return self.entries.get((accepted, bonus))
+
+    def size(self) -> int:
+        return len(self.entries)
+
+
+# ------------------------------------------------------------------ shapes
+def model_shape(vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn, tied=False, max_ctx=4096,
+                rope_theta=500000.0, norm_eps=1e-5) -> N.ModelShape:
+    return N.ModelShape(vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn, 1 if tied else 0, max_ctx,
+                        rope_theta, norm_eps)
+
+
+def shape_dict(s: N.ModelShape) -> dict:
+    """Oracle-side (oracle/oracle_capi.cpp parse_shape) description."""
+    return {"vocab": s.vocab, "d": s.d_model, "layers": s.n_layers, "heads": s.n_heads, "kv_heads": s.n_kv_heads,
+            "head_dim": s.head_dim, "ffn": s.ffn, "tied": bool(s.tied), "rope_theta": s.rope_theta,
+            "norm_eps": s.norm_eps, "max_ctx": s.max_ctx}
+
+
+@dataclass
+class Pair:
+    """Correlated random pair parameters."""
+    seed: int = 20250809
+    embed_scale: float = 1.0
+    shared_mlp_scale: float = 8.0
+    block_out_scale: float = 0.1
+    target_private_embed: float = 0.1
+    target_private_head: float = 0.25
+    draft_gain_mix: float = 0.0
+
+    def c(self) -> N.PairParams:
+        return N.PairParams(self.seed, self.embed_scale, self.shared_mlp_scale, self.block_out_scale,
+                            self.target_private_embed, self.target_private_head, self.draft_gain_mix)
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def _i32(seq) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(seq, dtype=np.int32))
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+class Engine:
+    """A (target, draft) pair resident on one B200 plus its decode loops."""
+
+    def __init__(self, target: N.ModelShape, draft: N.ModelShape, pair: Pair = Pair(), device: int = 0,
+                 max_branches: int = 64, max_lookahead: int = 8):
+        self.lib = N.load()
+        self.target, self.draft, self.pair = target, draft, pair
+        self.vocab = target.vocab
+        h = C.c_void_p()
+        _check(self.lib.ssd_engine_create(C.byref(target), C.byref(draft), C.byref(pair.c()), device, max_branches,
+                                          max_lookahead, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ssd_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def weight_bytes(self, which: int) -> int:
+        return int(self.lib.ssd_engine_weight_bytes(self.h, which))
+
+    # ---- decode loops (sim.hpp)
+    def run_ar(self, prompt: Sequence[int], target_scheme: SamplingScheme, tokens: int, seed: int) -> RunStats:
+        p = _i32(prompt)
+        out = np.zeros(tokens, dtype=np.int32)
+        st = N.RunStatsC()
+        _check(self.lib.ssd_run_ar(self.h, _ptr(p, C.c_int32), len(p), C.byref(target_scheme.c()), tokens, seed,
+                                   _ptr(out, C.c_int32), tokens, C.byref(st)))
+        return RunStats._from_c(st, out.tolist())
+
+    def run_sd(self, prompt: Sequence[int], cfg: SimConfig) -> RunStats:
+        p = _i32(prompt)
+        cap = cfg.rounds * (cfg.lookahead + 1)
+        out = np.zeros(cap, dtype=np.int32)
+        n = C.c_int64()
+        st = N.RunStatsC()
+        _check(self.lib.ssd_run_sd(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), _ptr(out, C.c_int32), cap,
+                                   C.byref(n), C.byref(st)))
+        return RunStats._from_c(st, out[: n.value].tolist())
+
+    def run_ssd(self, prompt: Sequence[int], cfg: SimConfig) -> RunStats:
+        """sim::run_protocol_harness semantics (sim.cpp:502-601)."""
+        p = _i32(prompt)
+        cap = cfg.rounds * (cfg.lookahead + 1)
+        out = np.zeros(cap, dtype=np.int32)
+        oc = np.zeros(2 * cfg.rounds, dtype=np.int32)
+        hits = np.zeros(cfg.rounds, dtype=np.int32)
+        n = C.c_int64()
+        st = N.RunStatsC()
+        _check(self.lib.ssd_run_ssd(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), _ptr(out, C.c_int32), cap,
+                                    C.byref(n), _ptr(oc, C.c_int32), _ptr(hits, C.c_int32), C.byref(st)))
+        r = RunStats._from_c(st, out[: n.value].tolist())
+        r.outcomes = oc.reshape(-1, 2)
+        r.hits = hits
+        return r
+
+    # ---- single operations (specdec.hpp / cache.hpp / lm.hpp)
+    def logits(self, which: int, context: Sequence[int]) -> np.ndarray:
+        c = _i32(context)
+        out = np.zeros(self.vocab, dtype=np.float32)
+        _check(self.lib.ssd_logits(self.h, which, _ptr(c, C.c_int32), len(c), _ptr(out, C.c_float)))
+        return out
+
+    def draft_spec(self, context: Sequence[int], lookahead: int, scheme: SamplingScheme, seed: int,
+                   with_rows: bool = True) -> Speculation:
+        c = _i32(context)
+        toks = np.zeros(lookahead, dtype=np.int32)
+        rows = np.zeros((lookahead, self.vocab), dtype=np.float32) if with_rows else None
+        _check(self.lib.ssd_draft(self.h, _ptr(c, C.c_int32), len(c), lookahead, C.byref(scheme.c()), seed,
+                                  _ptr(toks, C.c_int32), _ptr(rows, C.c_float) if with_rows else None))
+        return Speculation(toks.tolist(), rows)
+
+    def build_cache(self, context: Sequence[int], spec: Speculation, plan: FanOutPlan, scheme: SamplingScheme,
+                    next_lookahead: int, seed: int) -> SpeculationCache:
+        c = _i32(context)
+        s = _i32(spec.tokens)
+        K = len(spec.tokens)
+        tot = plan.total()
+        keys = np.zeros(2 * max(tot, 1), dtype=np.int32)
+        toks = np.zeros(max(tot, 1) * next_lookahead, dtype=np.int32)
+        cnt = C.c_int32()
+        _check(self.lib.ssd_build_cache(self.h, _ptr(c, C.c_int32), len(c), _ptr(s, C.c_int32), K,
+                                        C.byref(plan.c()), C.byref(scheme.c()), next_lookahead, seed,
+                                        _ptr(keys, C.c_int32), _ptr(toks, C.c_int32), C.byref(cnt)))
+        entries = {}
+        for i in range(cnt.value):
+            entries[(int(keys[2 * i]), int(keys[2 * i + 1]))] = toks[i * next_lookahead:(i + 1) * next_lookahead].tolist()
+        return SpeculationCache(entries, plan.role)
+
+    # ---- kernel-level hooks
+    def topk_keys(self, rows: np.ndarray, fan_out: Sequence[int], excluded: Sequence[int]) -> np.ndarray:
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        n, V = rows.shape
+        f = _i32(fan_out)
+        e = _i32(excluded)
+        max_f = max(1, int(f.max()))
+        keys = np.zeros(n * max_f, dtype=np.int32)
+        _check(self.lib.ssd_topk_keys(self.h, _ptr(rows, C.c_float), n, V, _ptr(f, C.c_int32), _ptr(e, C.c_int32),
+                                      max_f, _ptr(keys, C.c_int32)))
+        return keys.reshape(n, max_f)
+
+    def verify_rows(self, target_rows: np.ndarray, draft_rows: Optional[np.ndarray], tokens: Sequence[int],
+                    draft_scheme: SamplingScheme, target_scheme: SamplingScheme, seed: int,
+                    accept_scale: float = 1.0):
+        t = np.ascontiguousarray(target_rows, dtype=np.float32)
+        d = None if draft_rows is None else np.ascontiguousarray(draft_rows, dtype=np.float32)
+        tk = _i32(tokens)
+        acc, bonus = C.c_int32(), C.c_int32()
+        _check(self.lib.ssd_verify_rows(self.h, _ptr(t, C.c_float), None if d is None else _ptr(d, C.c_float),
+                                        _ptr(tk, C.c_int32), len(tk), t.shape[1], C.byref(draft_scheme.c()),
+                                        C.byref(target_scheme.c()), accept_scale, seed, C.byref(acc), C.byref(bonus)))
+        return acc.value, bonus.value
+
+    def profile_forward(self, which: int, M: int, pos: int, iters: int) -> dict:
+        f, g = C.c_double(), C.c_double()
+        b, n = C.c_int64(), C.c_int32()
+        _check(self.lib.ssd_profile_forward(self.h, which, M, pos, iters, C.byref(f), C.byref(g), C.byref(b),
+                                            C.byref(n)))
+        return {"ms_forward": f.value, "ms_gemm": g.value, "gemm_bytes": b.value, "gemm_launches": n.value}
+
+    def rng_u64(self, seed: int, n: int) -> list:
+        out = np.zeros(n, dtype=np.uint64)
+        _check(self.lib.ssd_rng_u64(self.h, seed, n, _ptr(out, C.c_uint64)))
+        return [int(x) for x in out]
+
+    def weight_bits(self, which: int, layer: int, kind: int, rows, cols) -> np.ndarray:
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        out = np.zeros(len(r), dtype=np.uint16)
+        _check(self.lib.ssd_weight_bits(self.h, which, layer, kind, _ptr(r, C.c_int64), _ptr(c, C.c_int64), len(r),
+                                        _ptr(out, C.c_uint16)))
+        return out

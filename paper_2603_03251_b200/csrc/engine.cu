@@ -1,0 +1,940 @@
+// B200 Saguaro engine: host side (C++) of the C-ABI in include/ssd_b200.h.
+//
+// One process owns a (target, draft) pair on one GPU. The verifier runs on
+// stream `sv`, the speculator on stream `ss`; a whole SSD round (verify
+// forward + decision || extend + keys + K branch steps, then lookup) is one
+// CUDA graph with a fork/join between the two streams, replayed per round
+// with no host synchronisation for the FastRandom backup.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ssd_b200.h"
+#include "kernels.cuh"
+
+namespace ssd {
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_last_error;
+
+struct Fail : std::runtime_error {
+  int code;
+  Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw Fail(SSD_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__)); \
+  } while (0)
+#define KCHECK() CK(cudaGetLastError())
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  CK(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+// ------------------------------------------------------------------ model
+struct DevLayer {
+  bf16 *wqkv, *wo, *wgu, *wd;
+};
+
+struct Model {
+  ssd_model_shape s{};
+  int role = 0;  // 0 target, 1 draft
+  int qd = 0, kvd = 0;
+  bf16* embed = nullptr;
+  bf16* head = nullptr;  // == embed when tied
+  float* final_gain = nullptr;
+  float* ffn_gain0 = nullptr;
+  std::vector<DevLayer> layers;
+  int S = 0;             // KV slots per kv-head (main + branch region)
+  bf16* kc = nullptr;    // [L][KVH][S][hd]
+  bf16* vc = nullptr;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  int maxM = 0;
+  float *x = nullptr, *qkv = nullptr, *q = nullptr, *logits = nullptr;
+  bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
+  int64_t weight_bytes = 0;
+  std::vector<void*> owned;
+
+  size_t kv_layer_elems() const { return size_t(s.n_kv_heads) * size_t(S) * size_t(s.head_dim); }
+};
+
+struct Engine {
+  int dev = 0;
+  Model T, D;
+  int maxB = 0, maxK = 0;
+  int V = 0;
+  cudaStream_t sv = nullptr, ss = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_verified = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  LoopState* st = nullptr;
+  int* hist = nullptr;
+  FwdParams *P_t = nullptr, *P_x = nullptr, *P_b = nullptr, *P_s = nullptr, *P_pre = nullptr;
+  float* tlogits = nullptr;   // [K+1][V]
+  float* xrows = nullptr;     // extend rows [K+1][V]
+  float* dmain = nullptr;     // drafted rows [K][V]
+  float* brows[2] = {nullptr, nullptr};  // branch rows [K][B][V], double-buffered by round parity
+  int *keys = nullptr, *bk = nullptr, *btok = nullptr, *bt = nullptr;
+  double* bu = nullptr;
+  double* ubuf = nullptr;
+  int *plans = nullptr, *offs = nullptr;
+  RowStat* rstat = nullptr;
+  double* cum = nullptr;
+  int* tok_scratch = nullptr;
+  std::vector<void*> owned;
+  long long launches = 0;
+};
+
+// ----------------------------------------------------------------- helpers
+static void rope_tables(const ssd_model_shape& s, std::vector<float>& cs, std::vector<float>& sn) {
+  const int half = s.head_dim / 2;
+  cs.assign(size_t(s.max_ctx) * half, 0.f);
+  sn.assign(size_t(s.max_ctx) * half, 0.f);
+  for (int p = 0; p < s.max_ctx; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double inv = std::pow(s.rope_theta, -2.0 * i / double(s.head_dim));
+      const double a = double(p) * inv;
+      cs[size_t(p) * half + i] = float(std::cos(a));
+      sn[size_t(p) * half + i] = float(std::sin(a));
+    }
+}
+
+static uint64_t splitmix_h(uint64_t x) { return splitmix64(x); }
+static float unit_value_h(uint64_t key, uint64_t idx) {
+  const uint64_t h = derive_seed(key, idx);
+  return float(int32_t(uint32_t(h >> 32)) >> 8) * 0x1.0p-23f;
+}
+static float sign_h(uint64_t key, size_t i) { return unit_value_h(key, i) < 0.f ? -1.f : 1.f; }
+
+static GenShape gshape(const ssd_model_shape& s) { return GenShape{s.d_model, s.n_heads, s.n_kv_heads, s.head_dim, s.ffn}; }
+
+static void gen_launch(bf16* dst, int rows, int cols, int stride, int off, const ssd_model_shape& self,
+                       const ssd_model_shape& dr, const GenPair& gp, int role, int layer, int kind) {
+  gen_layer_kernel<<<148 * 8, 256>>>(dst, rows, cols, stride, off, gshape(self), gshape(dr), gp, role, layer, kind);
+  KCHECK();
+}
+
+static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shape& dr, const ssd_pair_params& pp,
+                        int role, int branch_slots, int maxM) {
+  m.s = s;
+  m.role = role;
+  const int d = s.d_model, hd = s.head_dim;
+  m.qd = s.n_heads * hd;
+  m.kvd = s.n_kv_heads * hd;
+  const GenPair gp{pp.seed, pp.embed_scale, pp.shared_mlp_scale, pp.block_out_scale, pp.target_private_embed,
+                   pp.target_private_head, pp.draft_gain_mix};
+  auto own = [&](void* p) { m.owned.push_back(p); return p; };
+  // tables
+  m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
+  gen_table_kernel<<<148 * 8, 256>>>(m.embed, s.vocab, d, dr.d_model, gp, 0);
+  KCHECK();
+  if (s.tied) {
+    m.head = m.embed;
+  } else {
+    m.head = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
+    gen_table_kernel<<<148 * 8, 256>>>(m.head, s.vocab, d, dr.d_model, gp, 1);
+    KCHECK();
+  }
+  // norm gains (host, float arithmetic identical to the oracle)
+  std::vector<float> fg(static_cast<size_t>(d)), g0(static_cast<size_t>(d), 1.0f);
+  const uint64_t kGS = derive_seed(pp.seed, 0xE0000004u), kGN = derive_seed(pp.seed, 0xE0000005u),
+                 kGT = derive_seed(pp.seed, 0xE0000006u);
+  const int ds = dr.d_model;
+  const float comp = std::sqrt(float(ds) / float(d));
+  for (int i = 0; i < d; ++i) {
+    if (role == 1) {
+      fg[size_t(i)] = (1.0f - pp.draft_gain_mix) * sign_h(kGS, size_t(i)) + pp.draft_gain_mix * sign_h(kGN, size_t(i));
+    } else {
+      fg[size_t(i)] = i < ds ? sign_h(kGS, size_t(i)) : sign_h(kGT, size_t(i - ds));
+      if (i < ds) g0[size_t(i)] = comp;
+    }
+  }
+  m.final_gain = static_cast<float*>(own(dalloc<float>(size_t(d))));
+  m.ffn_gain0 = static_cast<float*>(own(dalloc<float>(size_t(d))));
+  CK(cudaMemcpy(m.final_gain, fg.data(), fg.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.ffn_gain0, g0.data(), g0.size() * 4, cudaMemcpyHostToDevice));
+  // layers: fused QKV [q; k; v], interleaved gate/up rows (2j gate, 2j+1 up)
+  m.layers.resize(size_t(s.n_layers));
+  int64_t wb = 0;
+  for (int l = 0; l < s.n_layers; ++l) {
+    DevLayer& L = m.layers[size_t(l)];
+    L.wqkv = static_cast<bf16*>(own(dalloc<bf16>(size_t(m.qd + 2 * m.kvd) * d)));
+    L.wo = static_cast<bf16*>(own(dalloc<bf16>(size_t(d) * m.qd)));
+    L.wgu = static_cast<bf16*>(own(dalloc<bf16>(size_t(2 * s.ffn) * d)));
+    L.wd = static_cast<bf16*>(own(dalloc<bf16>(size_t(d) * s.ffn)));
+    gen_launch(L.wqkv, m.qd, d, 1, 0, s, dr, gp, role, l, 0);
+    gen_launch(L.wqkv, m.kvd, d, 1, m.qd, s, dr, gp, role, l, 1);
+    gen_launch(L.wqkv, m.kvd, d, 1, m.qd + m.kvd, s, dr, gp, role, l, 2);
+    gen_launch(L.wo, d, m.qd, 1, 0, s, dr, gp, role, l, 3);
+    gen_launch(L.wgu, s.ffn, d, 2, 0, s, dr, gp, role, l, 4);
+    gen_launch(L.wgu, s.ffn, d, 2, 1, s, dr, gp, role, l, 5);
+    gen_launch(L.wd, d, s.ffn, 1, 0, s, dr, gp, role, l, 6);
+    wb += int64_t(m.qd + 2 * m.kvd) * d + int64_t(d) * m.qd + int64_t(2 * s.ffn) * d + int64_t(d) * s.ffn;
+  }
+  wb += int64_t(s.vocab) * d;  // LM head
+  m.weight_bytes = wb * 2;
+  // KV cache
+  m.S = s.max_ctx + branch_slots;
+  m.kc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
+  m.vc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
+  std::vector<float> cs, sn;
+  rope_tables(s, cs, sn);
+  m.rope_cos = static_cast<float*>(own(dalloc<float>(cs.size())));
+  m.rope_sin = static_cast<float*>(own(dalloc<float>(sn.size())));
+  CK(cudaMemcpy(m.rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  // activations
+  m.maxM = maxM;
+  m.x = static_cast<float*>(own(dalloc<float>(size_t(maxM) * d)));
+  m.xb = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * std::max(d, m.qd))));
+  m.qkv = static_cast<float*>(own(dalloc<float>(size_t(maxM) * (m.qd + 2 * m.kvd))));
+  m.q = static_cast<float*>(own(dalloc<float>(size_t(maxM) * m.qd)));
+  m.attn = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * m.qd)));
+  m.act = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * s.ffn)));
+  m.logits = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.vocab)));
+}
+
+static void free_model(Model& m) {
+  for (void* p : m.owned) cudaFree(p);
+  m.owned.clear();
+}
+
+// ------------------------------------------------------------------ forward
+template <int EPI>
+static void linear(Engine& E, const bf16* W, int N, int K, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                   cudaStream_t s) {
+  const int rows_per_cta = 16;  // 8 warps x 2 rows
+  linear_cc_kernel<EPI, 4><<<(N + rows_per_cta - 1) / rows_per_cta, 256, 0, s>>>(W, N, K, X, M, Y, ldy, Yb, ldyb);
+  KCHECK();
+  ++E.launches;
+}
+
+// One forward step of `m` over the M tokens described by P. Logits of all M
+// rows go to `logits` ([M][V]) when non-null.
+static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
+  if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
+  const ssd_model_shape& sh = m.s;
+  const int d = sh.d_model, H = sh.n_heads, KVH = sh.n_kv_heads, hd = sh.head_dim, F = sh.ffn;
+  const int nqkv = m.qd + 2 * m.kvd;
+  embed_kernel<<<M, 256, 0, s>>>(m.embed, d, P, m.x);
+  KCHECK();
+  ++E.launches;
+  const float scale = 1.0f / std::sqrt(float(hd));
+  const size_t attn_smem = size_t(hd + sh.max_ctx + E.maxK + 2 + 128) * sizeof(float);
+  for (int l = 0; l < sh.n_layers; ++l) {
+    const DevLayer& L = m.layers[size_t(l)];
+    bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
+    bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
+    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, nullptr, sh.norm_eps, m.xb);
+    KCHECK();
+    linear<EPI_STORE>(E, L.wqkv, nqkv, d, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
+    rope_append_kernel<<<dim3(M, H + KVH), hd / 2, 0, s>>>(m.qkv, H, KVH, hd, P, m.rope_cos, m.rope_sin, m.q, kc, vc, m.S);
+    KCHECK();
+    attention_kernel<<<dim3(H, M), 128, attn_smem, s>>>(m.q, kc, vc, m.S, P, H, KVH, hd, scale, m.attn);
+    KCHECK();
+    linear<EPI_RESID>(E, L.wo, d, m.qd, m.attn, M, m.x, d, nullptr, 0, s);
+    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, l == 0 ? m.ffn_gain0 : nullptr, sh.norm_eps, m.xb);
+    KCHECK();
+    linear<EPI_SWIGLU>(E, L.wgu, 2 * F, d, m.xb, M, nullptr, 0, m.act, F, s);
+    linear<EPI_RESID>(E, L.wd, d, F, m.act, M, m.x, d, nullptr, 0, s);
+    E.launches += 4;
+  }
+  if (logits) {
+    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, m.final_gain, sh.norm_eps, m.xb);
+    KCHECK();
+    linear<EPI_STORE>(E, m.head, sh.vocab, d, m.xb, M, logits, sh.vocab, nullptr, 0, s);
+    ++E.launches;
+  }
+}
+
+// Prefill hist[0, n) into model m (chunks of maxM). Logits of the last
+// token to `last_logits` when non-null.
+static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t s) {
+  const int chunk = std::min(m.maxM, kMaxM);
+  for (int lo = 0; lo < n; lo += chunk) {
+    const int M = std::min(chunk, n - lo);
+    prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, lo, M);
+    KCHECK();
+    const bool last = lo + M >= n;
+    forward(E, m, E.P_pre, M, (last && last_logits) ? m.logits : nullptr, s);
+    if (last && last_logits)
+      CK(cudaMemcpyAsync(last_logits, m.logits + size_t(M - 1) * m.s.vocab, size_t(m.s.vocab) * 4,
+                         cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+static DScheme dscheme(const ssd_scheme& s) {
+  return DScheme{s.kind == 1 ? 1 : 0, s.fan_out, s.temperature, s.downweight};
+}
+
+static void check_scheme(const ssd_scheme& s, int V) {
+  if (s.temperature < 0.0 || !std::isfinite(s.temperature)) throw Fail(SSD_ERROR, "apply_scheme: temperature must be > 0");
+  if (s.kind == 1) {
+    if (s.fan_out < 1 || s.fan_out > V) throw Fail(SSD_ERROR, "apply_scheme: fan_out out of range");
+    if (s.fan_out > kMaxTopF) throw Fail(SSD_TOO_LARGE, "apply_scheme: fan_out above the engine's top-k capacity");
+    if (!(s.downweight >= 0.0) || !(s.downweight <= 1.0)) throw Fail(SSD_ERROR, "apply_scheme: downweight must be in [0, 1]");
+  }
+}
+
+// ------------------------------------------------------------------ state
+static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed, uint64_t vseed, const ssd_sim_config* c,
+                        cudaStream_t s) {
+  LoopState h;
+  std::memset(&h, 0, sizeof(h));
+  h.n = n;
+  h.K = K;
+  h.rounds = int(rounds);
+  h.backup_kind = c ? c->backup_kind : 1;
+  h.primary_time = c ? c->primary_time : 0.0;
+  h.backup_time = c ? (c->backup_kind == 0 ? c->primary_time : c->backup_time) : 0.0;
+  CK(cudaMemcpyAsync(E.st, &h, offsetof(LoopState, vrng), cudaMemcpyHostToDevice, s));
+  mt_init_kernel<<<1, 32, 0, s>>>(&E.st->vrng, vseed);
+  mt_init_kernel<<<1, 32, 0, s>>>(&E.st->drng, dseed);
+  KCHECK();
+}
+
+static LoopState read_state(Engine& E) {
+  LoopState h;
+  CK(cudaMemcpy(&h, E.st, offsetof(LoopState, vrng), cudaMemcpyDeviceToHost));
+  return h;
+}
+
+static void raise_device_error(const LoopState& h) {
+  if (h.error == 1) throw Fail(SSD_ERROR, "verify: drafted token has zero draft probability");
+  if (h.error == 3) throw Fail(SSD_DEGENERATE_RESIDUAL, "residual: zero positive mass (draft equals target)");
+  if (h.error) throw Fail(SSD_ERROR, "device error " + std::to_string(h.error));
+}
+
+// K sequential draft steps from the current history (specdec::draft,
+// specdec.cpp:8-25): rows into dmain, tokens into st->spec.
+static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int src, cudaStream_t s) {
+  const DScheme ds = dscheme(sc);
+  for (int i = 0; i < K; ++i) {
+    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i);
+    forward(E, E.D, E.P_s, 1, E.dmain + size_t(i) * E.V, s);
+    draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
+    sample_rows_kernel<<<1, kSampleThreads, 0, s>>>(E.dmain + size_t(i) * E.V, E.V, ds, E.ubuf, 1, &E.st->spec[i], 1);
+    KCHECK();
+    E.launches += 3;
+  }
+  set_spec_rows_kernel<<<1, 32, 0, s>>>(E.st, E.dmain, E.V, origin, src);
+  KCHECK();
+  ++E.launches;
+}
+
+// Verification of st->spec against the target (verify forward M = K+1,
+// then the decision kernels).
+static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_scheme& ds, double scale, int use_draft_stream,
+                         cudaStream_t s) {
+  prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1);
+  KCHECK();
+  forward(E, E.T, E.P_t, K + 1, E.tlogits, s);
+  verify_stats_kernel<<<2 * K + 1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.V, dscheme(ts), dscheme(ds), E.rstat);
+  verify_decide_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, E.V, dscheme(ts), dscheme(ds), scale, E.rstat,
+                                                    use_draft_stream);
+  KCHECK();
+  E.launches += 3;
+}
+
+// Pre-speculation for the in-flight speculation (cache::build_cache,
+// cache.cpp:232-277, batched): extend over [last, s_1..s_K], candidate keys,
+// per-branch streams, K branch decode steps at M = B.
+static void prespeculate(Engine& E, int K, int B, int max_f, const ssd_scheme& sc, int parity, cudaStream_t s) {
+  prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1);
+  KCHECK();
+  forward(E, E.D, E.P_x, K + 1, E.xrows, s);
+  keys_kernel<<<K + 1, 256, 0, s>>>(E.xrows, E.V, E.plans, E.offs, E.st, nullptr, K, max_f, E.keys, E.bk, E.btok);
+  const bool sampled = sc.temperature > 0.0;
+  branch_streams_kernel<<<1, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
+  KCHECK();
+  E.launches += 3;
+  const DScheme ds = dscheme(sc);
+  float* rows = E.brows[parity];
+  for (int j = 0; j < K; ++j) {
+    prep_branch_kernel<<<(B + 127) / 128, 128, 0, s>>>(E.st, E.bk, E.btok, E.bt, E.P_b, B, j, E.D.s.max_ctx);
+    float* out = rows + size_t(j) * B * E.V;
+    forward(E, E.D, E.P_b, B, out, s);
+    sample_rows_kernel<<<B, kSampleThreads, 0, s>>>(out, E.V, ds, sampled ? E.bu + j : nullptr, K, E.bt + j, K);
+    KCHECK();
+    E.launches += 2;
+  }
+}
+
+static void upload_plans(Engine& E, const ssd_plan& p, const ssd_plan& b, int K, int& B, int& max_f) {
+  std::vector<int> fan(size_t(2 * (K + 1))), off(size_t(2 * (K + 1)));
+  B = 0;
+  max_f = 1;
+  for (int r = 0; r < 2; ++r) {
+    const ssd_plan& pl = r == 0 ? p : b;
+    if (pl.lookahead != K) throw Fail(SSD_ERROR, "build_cache: plan length does not match speculation");
+    int tot = 0;
+    for (int k = 0; k <= K; ++k) {
+      const int f = pl.fan_out[k];
+      if (f < 0) throw Fail(SSD_ERROR, "plan: negative fan-out");
+      if (f > kMaxTopF - 1) throw Fail(SSD_TOO_LARGE, "plan: fan-out above the engine's top-k capacity");
+      if (f > (k < K ? E.V - 1 : E.V)) throw Fail(SSD_ERROR, "plan: fan-out exceeds candidate count");
+      fan[size_t(r * (K + 1) + k)] = f;
+      off[size_t(r * (K + 1) + k)] = tot;
+      tot += f;
+      max_f = std::max(max_f, f);
+    }
+    B = std::max(B, tot);
+  }
+  if (B > E.maxB) throw Fail(SSD_TOO_LARGE, "plan: budget exceeds the engine's branch capacity");
+  B = std::max(B, 1);
+  CK(cudaMemcpy(E.plans, fan.data(), fan.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(E.offs, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+}
+
+static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_needed) {
+  if (n < 1) throw Fail(SSD_ERROR, "prompt must hold at least one token");
+  const int cap = std::min(E.T.s.max_ctx, E.D.s.max_ctx);
+  if (max_ctx_needed > cap) throw Fail(SSD_TOO_LARGE, "context exceeds max_ctx");
+  for (int i = 0; i < n; ++i)
+    if (prompt[i] < 0 || prompt[i] >= E.V) throw Fail(SSD_ERROR, "context_index: token out of range");
+  CK(cudaMemcpy(E.hist, prompt, size_t(n) * 4, cudaMemcpyHostToDevice));
+}
+
+static void fill_stats(const LoopState& h, int64_t rounds, float ms, long long launches, ssd_run_stats* out) {
+  if (!out) return;
+  out->rounds = rounds;
+  out->tokens = h.tokens;
+  out->virtual_time = h.clock;
+  out->primary_origin_lookups = h.p_lookups;
+  out->primary_origin_hits = h.p_hits;
+  out->backup_origin_lookups = h.b_lookups;
+  out->backup_origin_hits = h.b_hits;
+  out->hit_rounds = h.hit_rounds;
+  out->miss_rounds = h.miss_rounds;
+  out->initial_rounds = h.initial_rounds;
+  out->hit_round_tokens = h.hit_round_tokens;
+  out->miss_round_tokens = h.miss_round_tokens;
+  out->accepted_sum = h.accepted_sum;
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+}
+
+static void copy_out(Engine& E, int n0, int n, int32_t* out, int64_t cap, int64_t* out_len) {
+  const int64_t len = n - n0;
+  if (out_len) *out_len = len;
+  if (out && len > 0) CK(cudaMemcpy(out, E.hist + n0, size_t(std::min<int64_t>(len, cap)) * 4, cudaMemcpyDeviceToHost));
+}
+
+static void validate_cfg(Engine& E, const ssd_sim_config* c) {
+  if (!c) throw Fail(SSD_CONFIG, "sim: config required");
+  if (c->lookahead < 1) throw Fail(SSD_ERROR, "sim: lookahead must be >= 1");
+  if (c->lookahead > E.maxK) throw Fail(SSD_TOO_LARGE, "sim: lookahead exceeds the engine's capacity");
+  if (c->rounds < 1) throw Fail(SSD_ERROR, "sim: rounds must be >= 1");
+  check_scheme(c->scheme, E.V);
+  check_scheme(c->target_scheme, E.V);
+}
+
+}  // namespace ssd
+
+using namespace ssd;
+
+struct ssd_engine {
+  Engine e;
+};
+
+#define API_BEGIN try {
+#define API_END                                      \
+  }                                                  \
+  catch (const Fail& f) {                            \
+    g_last_error = f.what();                         \
+    return ssd_status(f.code);                       \
+  }                                                  \
+  catch (const std::exception& x) {                  \
+    g_last_error = x.what();                         \
+    return SSD_ERROR;                                \
+  }                                                  \
+  return SSD_OK;
+
+extern "C" {
+
+const char* ssd_last_error(void) { return g_last_error.c_str(); }
+int ssd_abi_version(void) { return SSD_B200_ABI_VERSION; }
+
+ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shape* draft, const ssd_pair_params* pair,
+                             int32_t device, int32_t max_branches, int32_t max_lookahead, ssd_engine** out) {
+  API_BEGIN
+  if (!target || !draft || !pair || !out) throw Fail(SSD_CONFIG, "engine: null argument");
+  if (target->vocab != draft->vocab) throw Fail(SSD_ERROR, "sim: target and draft shapes differ");
+  if (draft->d_model > target->d_model || draft->ffn > target->ffn || !draft->tied)
+    throw Fail(SSD_CONFIG, "engine: the draft must be tied and no wider than the target");
+  for (const ssd_model_shape* s : {target, draft}) {
+    if (s->head_dim % 16 || s->head_dim > 128 || s->n_heads % s->n_kv_heads || s->d_model % 8 || s->ffn % 8)
+      throw Fail(SSD_CONFIG, "engine: unsupported shape");
+  }
+  if (max_lookahead < 1 || max_lookahead > kMaxK) throw Fail(SSD_TOO_LARGE, "engine: lookahead capacity");
+  if (max_branches < 1 || max_branches > kMaxM) throw Fail(SSD_TOO_LARGE, "engine: branch capacity");
+  CK(cudaSetDevice(device));
+  auto* h = new ssd_engine();
+  Engine& E = h->e;
+  E.dev = device;
+  E.maxB = max_branches;
+  E.maxK = max_lookahead;
+  E.V = target->vocab;
+  const int maxM = std::max(max_branches, max_lookahead + 1);
+  build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
+  build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
+  CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&E.ev_verified, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreate(&E.ev_t0));
+  CK(cudaEventCreate(&E.ev_t1));
+  auto own = [&](void* p) { E.owned.push_back(p); return p; };
+  const int K = max_lookahead, B = max_branches, V = E.V;
+  E.st = static_cast<LoopState*>(own(dalloc<LoopState>(1)));
+  E.hist = static_cast<int*>(own(dalloc<int>(size_t(std::max(target->max_ctx, draft->max_ctx)) + K + 2)));
+  E.P_t = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
+  E.P_x = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
+  E.P_b = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
+  E.P_s = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
+  E.P_pre = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
+  E.tlogits = static_cast<float*>(own(dalloc<float>(size_t(K + 1) * V)));
+  E.xrows = static_cast<float*>(own(dalloc<float>(size_t(K + 1) * V)));
+  E.dmain = static_cast<float*>(own(dalloc<float>(size_t(K) * V)));
+  E.brows[0] = static_cast<float*>(own(dalloc<float>(size_t(K) * B * V)));
+  E.brows[1] = static_cast<float*>(own(dalloc<float>(size_t(K) * B * V)));
+  E.keys = static_cast<int*>(own(dalloc<int>(size_t(K + 1) * kMaxTopF)));
+  E.bk = static_cast<int*>(own(dalloc<int>(size_t(B))));
+  E.btok = static_cast<int*>(own(dalloc<int>(size_t(B))));
+  E.bt = static_cast<int*>(own(dalloc<int>(size_t(B) * K)));
+  E.bu = static_cast<double*>(own(dalloc<double>(size_t(B) * K)));
+  E.ubuf = static_cast<double*>(own(dalloc<double>(64)));
+  E.plans = static_cast<int*>(own(dalloc<int>(size_t(2 * (K + 1)))));
+  E.offs = static_cast<int*>(own(dalloc<int>(size_t(2 * (K + 1)))));
+  E.rstat = static_cast<RowStat*>(own(dalloc<RowStat>(size_t(2 * K + 1))));
+  E.tok_scratch = static_cast<int*>(own(dalloc<int>(64)));
+  // exact sequential cumulative of the uniform law (FastRandom tokens)
+  std::vector<double> cum(static_cast<size_t>(V));
+  double c = 0.0;
+  for (int i = 0; i < V; ++i) { c += 1.0 / V; cum[size_t(i)] = c; }
+  E.cum = static_cast<double*>(own(dalloc<double>(size_t(V))));
+  CK(cudaMemcpy(E.cum, cum.data(), size_t(V) * 8, cudaMemcpyHostToDevice));
+  CK(cudaDeviceSynchronize());
+  *out = h;
+  API_END
+}
+
+ssd_status ssd_engine_destroy(ssd_engine* h) {
+  API_BEGIN
+  if (!h) return SSD_OK;
+  Engine& E = h->e;
+  cudaSetDevice(E.dev);
+  cudaDeviceSynchronize();
+  free_model(E.T);
+  free_model(E.D);
+  for (void* p : E.owned) cudaFree(p);
+  cudaStreamDestroy(E.sv);
+  cudaStreamDestroy(E.ss);
+  cudaEventDestroy(E.ev_fork);
+  cudaEventDestroy(E.ev_verified);
+  cudaEventDestroy(E.ev_join);
+  cudaEventDestroy(E.ev_t0);
+  cudaEventDestroy(E.ev_t1);
+  delete h;
+  API_END
+}
+
+int64_t ssd_engine_weight_bytes(const ssd_engine* h, int32_t which) {
+  if (!h) return 0;
+  return which == 0 ? h->e.T.weight_bytes : h->e.D.weight_bytes;
+}
+
+ssd_status ssd_run_ar(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_scheme* ts, int64_t tokens,
+                      uint64_t seed, int32_t* out, int64_t cap, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (tokens < 1) throw Fail(SSD_ERROR, "run_ar: tokens must be >= 1");
+  if (!ts) throw Fail(SSD_CONFIG, "run_ar: scheme required");
+  check_scheme(*ts, E.V);
+  set_history(E, prompt, n0, int(n0 + tokens + 1));
+  cudaStream_t s = E.sv;
+  reset_state(E, 1, n0, tokens, derive_seed(seed, 0), 0, nullptr, s);
+  if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, s);
+  E.launches = 0;
+  const DScheme d = dscheme(*ts);
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t i = 0; i < tokens; ++i) {
+    prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1);
+    forward(E, E.T, E.P_t, 1, E.tlogits, s);
+    draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
+    sample_rows_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.V, d, E.ubuf, 1, E.tok_scratch, 1);
+    ar_commit_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.tok_scratch);
+    KCHECK();
+    E.launches += 4;
+  }
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  LoopState st = read_state(E);
+  raise_device_error(st);
+  st.clock = double(tokens);
+  fill_stats(st, tokens, ms, E.launches, stats);
+  copy_out(E, n0, st.n, out, cap, nullptr);
+  API_END
+}
+
+ssd_status ssd_run_sd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t* out,
+                      int64_t cap, int64_t* out_len, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  validate_cfg(E, c);
+  const int K = c->lookahead;
+  set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + K + 2));
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n0, c->rounds, derive_seed(c->seed, 0), 0, c, s);
+  if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
+  if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, s);
+  E.launches = 0;
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t r = 0; r < c->rounds; ++r) {
+    draft_steps(E, K, c->scheme, 0, 0, s);
+    verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, /*single stream*/ 1, s);
+    commit_kernel<<<1, 32, 0, s>>>(E.st);
+    KCHECK();
+    ++E.launches;
+  }
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  LoopState st = read_state(E);
+  raise_device_error(st);
+  st.clock = double(c->rounds) * (1.0 + c->primary_time);
+  fill_stats(st, c->rounds, ms, E.launches, stats);
+  copy_out(E, n0, st.n, out, cap, out_len);
+  API_END
+}
+
+ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t* out,
+                       int64_t cap, int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  validate_cfg(E, c);
+  const int K = c->lookahead;
+  if (c->primary_time < 1.0 && false) {}
+  int B = 0, max_f = 0;
+  upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);
+  set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2));
+  const int64_t R = c->rounds;
+  int* d_out = static_cast<int*>(nullptr);
+  int* d_hit = static_cast<int*>(nullptr);
+  d_out = dalloc<int>(size_t(2 * R));
+  d_hit = dalloc<int>(size_t(R));
+  cudaStream_t sv = E.sv, ss = E.ss;
+  // harness streams: draft j=0 derive_seed(seed, 0); verifier
+  // derive_seed(derive_seed(seed, 0x5EED), 0) (sim.cpp:379-380, 516-518)
+  reset_state(E, K, n0, R, derive_seed(c->seed, 0), derive_seed(derive_seed(c->seed, 0x5EED), 0), c, sv);
+  if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, sv);
+  if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, sv);
+  // initial synchronous draft; clock starts at T_p (sim.cpp:524-526)
+  draft_steps(E, K, c->scheme, 0, 0, sv);
+  {
+    LoopState tmp;
+    tmp.clock = c->primary_time;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, clock), &tmp.clock, sizeof(double),
+                       cudaMemcpyHostToDevice, sv));
+  }
+  CK(cudaStreamSynchronize(sv));
+  E.launches = 0;
+  const bool jit = c->backup_kind == 0;
+  CK(cudaEventRecord(E.ev_t0, sv));
+  for (int64_t r = 0; r < R; ++r) {
+    const int parity = int(r & 1);
+    // fork: speculator follows everything enqueued on the verifier stream
+    CK(cudaEventRecord(E.ev_fork, sv));
+    CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
+    prespeculate(E, K, B, max_f, c->scheme, parity, ss);
+    verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv);
+    CK(cudaEventRecord(E.ev_verified, sv));
+    CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
+    lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], B, E.V, E.cum, d_out, d_hit);
+    KCHECK();
+    ++E.launches;
+    CK(cudaEventRecord(E.ev_join, ss));
+    CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
+    if (jit && r + 1 < R) {
+      CK(cudaStreamSynchronize(sv));
+      int hit = 0;
+      CK(cudaMemcpy(&hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int), cudaMemcpyDeviceToHost));
+      if (!hit) draft_steps(E, K, c->scheme, 1, 2, sv);
+    }
+  }
+  CK(cudaEventRecord(E.ev_t1, sv));
+  CK(cudaStreamSynchronize(sv));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  LoopState st = read_state(E);
+  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
+  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_out);
+  cudaFree(d_hit);
+  raise_device_error(st);
+  fill_stats(st, R, ms, E.launches, stats);
+  copy_out(E, n0, st.n, out, cap, out_len);
+  API_END
+}
+
+ssd_status ssd_logits(ssd_engine* h, int32_t which, const int32_t* ctx, int32_t n, float* out) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  set_history(E, ctx, n, n + 1);
+  Model& m = which == 0 ? E.T : E.D;
+  prefill(E, m, n, E.tlogits, E.sv);
+  CK(cudaStreamSynchronize(E.sv));
+  CK(cudaMemcpy(out, E.tlogits, size_t(E.V) * 4, cudaMemcpyDeviceToHost));
+  API_END
+}
+
+ssd_status ssd_draft(ssd_engine* h, const int32_t* ctx, int32_t n, int32_t K, const ssd_scheme* sc, uint64_t seed,
+                     int32_t* out_tokens, float* out_rows) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (K < 1) throw Fail(SSD_ERROR, "draft: lookahead must be >= 1");
+  if (K > E.maxK) throw Fail(SSD_TOO_LARGE, "draft: lookahead exceeds the engine's capacity");
+  if (!sc) throw Fail(SSD_CONFIG, "draft: scheme required");
+  check_scheme(*sc, E.V);
+  set_history(E, ctx, n, n + K + 1);
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n, 1, seed, 0, nullptr, s);
+  if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
+  draft_steps(E, K, *sc, 0, 0, s);
+  CK(cudaStreamSynchronize(s));
+  LoopState st = read_state(E);
+  std::memcpy(out_tokens, st.spec, size_t(K) * 4);
+  if (out_rows) CK(cudaMemcpy(out_rows, E.dmain, size_t(K) * E.V * 4, cudaMemcpyDeviceToHost));
+  API_END
+}
+
+ssd_status ssd_build_cache(ssd_engine* h, const int32_t* ctx, int32_t n, const int32_t* spec, int32_t K,
+                           const ssd_plan* plan, const ssd_scheme* sc, int32_t next_K, uint64_t seed, int32_t* out_keys,
+                           int32_t* out_entry_tokens, int32_t* out_count) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!plan || !sc) throw Fail(SSD_CONFIG, "build_cache: plan and scheme required");
+  if (plan->lookahead != K) throw Fail(SSD_ERROR, "build_cache: plan length does not match speculation");
+  if (next_K != K) throw Fail(SSD_CONFIG, "build_cache: the engine drafts continuations of the same lookahead");
+  if (K < 1 || K > E.maxK) throw Fail(SSD_TOO_LARGE, "build_cache: lookahead exceeds the engine's capacity");
+  check_scheme(*sc, E.V);
+  int B = 0, max_f = 0;
+  upload_plans(E, *plan, *plan, K, B, max_f);
+  int total = 0;
+  for (int k = 0; k <= K; ++k) total += plan->fan_out[k];
+  set_history(E, ctx, n, n + 2 * K + 2);
+  for (int i = 0; i < K; ++i)
+    if (spec[i] < 0 || spec[i] >= E.V) throw Fail(SSD_ERROR, "context_index: token out of range");
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n, 1, seed, 0, nullptr, s);
+  {
+    int tmp[kMaxK + 1];
+    std::memcpy(tmp, spec, size_t(K) * 4);
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec), tmp, size_t(K) * 4,
+                       cudaMemcpyHostToDevice, s));
+    const int origin = plan->role;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec_origin), &origin, 4,
+                       cudaMemcpyHostToDevice, s));
+  }
+  if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
+  if (total > 0) prespeculate(E, K, B, max_f, *sc, 0, s);
+  else branch_streams_kernel<<<1, 32, 0, s>>>(E.st, 0, E.bu, 0);
+  CK(cudaStreamSynchronize(s));
+  std::vector<int> bkh(static_cast<size_t>(B)), bth(static_cast<size_t>(B)), tt(static_cast<size_t>(B) * K);
+  CK(cudaMemcpy(bkh.data(), E.bk, size_t(B) * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(bth.data(), E.btok, size_t(B) * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(tt.data(), E.bt, size_t(B) * K * 4, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < total; ++i) {
+    if (out_keys) { out_keys[2 * i] = bkh[size_t(i)]; out_keys[2 * i + 1] = bth[size_t(i)]; }
+    if (out_entry_tokens) std::memcpy(out_entry_tokens + size_t(i) * K, &tt[size_t(i) * K], size_t(K) * 4);
+  }
+  if (out_count) *out_count = total;
+  API_END
+}
+
+ssd_status ssd_topk_keys(ssd_engine* h, const float* rows, int32_t n_rows, int32_t V, const int32_t* fan,
+                         const int32_t* excluded, int32_t max_f, int32_t* keys) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (n_rows < 1 || n_rows > E.maxK + 1 || V > E.V || V < 1) throw Fail(SSD_TOO_LARGE, "topk_keys: shape exceeds capacity");
+  if (max_f > kMaxTopF) throw Fail(SSD_TOO_LARGE, "topk_keys: fan-out above capacity");
+  std::vector<int> fan2(size_t(2 * n_rows)), off2(size_t(2 * n_rows));
+  int tot = 0;
+  for (int k = 0; k < n_rows; ++k) {
+    if (fan[k] > max_f || fan[k] >= kMaxTopF) throw Fail(SSD_TOO_LARGE, "topk_keys: fan-out above capacity");
+    fan2[size_t(k)] = fan2[size_t(n_rows + k)] = fan[k];
+    off2[size_t(k)] = off2[size_t(n_rows + k)] = tot;
+    tot += fan[k];
+  }
+  if (tot > E.maxB) throw Fail(SSD_TOO_LARGE, "topk_keys: too many candidates");
+  CK(cudaMemcpy(E.plans, fan2.data(), fan2.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(E.offs, off2.data(), off2.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(E.xrows, rows, size_t(n_rows) * V * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(E.tok_scratch, excluded, size_t(n_rows) * 4, cudaMemcpyHostToDevice));
+  keys_kernel<<<n_rows, 256, 0, E.sv>>>(E.xrows, V, E.plans, E.offs, nullptr, E.tok_scratch, n_rows, max_f, E.keys, E.bk,
+                                        E.btok);
+  KCHECK();
+  CK(cudaStreamSynchronize(E.sv));
+  CK(cudaMemcpy(keys, E.keys, size_t(n_rows) * max_f * 4, cudaMemcpyDeviceToHost));
+  API_END
+}
+
+ssd_status ssd_verify_rows(ssd_engine* h, const float* trows, const float* drows, const int32_t* tokens, int32_t K,
+                           int32_t V, const ssd_scheme* ds, const ssd_scheme* ts, double scale, uint64_t seed,
+                           int32_t* accepted, int32_t* bonus) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (K < 1) throw Fail(SSD_ERROR, "verify: empty speculation");
+  if (K > E.maxK || V != E.V) throw Fail(SSD_TOO_LARGE, "verify_rows: shape exceeds capacity");
+  check_scheme(*ds, V);
+  check_scheme(*ts, V);
+  for (int i = 0; i < K; ++i)
+    if (tokens[i] < 0 || tokens[i] >= V) throw Fail(SSD_ERROR, "verify: token out of range");
+  cudaStream_t s = E.sv;
+  CK(cudaMemcpy(E.tlogits, trows, size_t(K + 1) * V * 4, cudaMemcpyHostToDevice));
+  if (drows) CK(cudaMemcpy(E.dmain, drows, size_t(K) * V * 4, cudaMemcpyHostToDevice));
+  std::vector<int> hist0(1, 0);
+  CK(cudaMemcpy(E.hist, hist0.data(), 4, cudaMemcpyHostToDevice));
+  reset_state(E, K, 1, 1, 0, seed, nullptr, s);
+  {
+    int tmp[kMaxK];
+    std::memcpy(tmp, tokens, size_t(K) * 4);
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec), tmp, size_t(K) * 4,
+                       cudaMemcpyHostToDevice, s));
+  }
+  if (drows) set_spec_rows_kernel<<<1, 32, 0, s>>>(E.st, E.dmain, V, 0, 0);
+  else {
+    const int one = 1;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec_uniform), &one, 4,
+                       cudaMemcpyHostToDevice, s));
+  }
+  verify_stats_kernel<<<2 * K + 1, kSampleThreads, 0, s>>>(E.tlogits, E.st, V, dscheme(*ts), dscheme(*ds), E.rstat);
+  verify_decide_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, V, dscheme(*ts), dscheme(*ds), scale, E.rstat, 0);
+  KCHECK();
+  CK(cudaStreamSynchronize(s));
+  LoopState st = read_state(E);
+  raise_device_error(st);
+  *accepted = st.out_k;
+  *bonus = st.out_t;
+  API_END
+}
+
+ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t pos, int32_t iters, double* ms_forward,
+                               double* ms_gemm, int64_t* gemm_bytes, int32_t* gemm_launches) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  Model& m = which == 0 ? E.T : E.D;
+  if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
+  cudaStream_t s = E.sv;
+  prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M);
+  KCHECK();
+  const ssd_model_shape& sh = m.s;
+  const int d = sh.d_model, F = sh.ffn, nqkv = m.qd + 2 * m.kvd;
+  auto gemms = [&]() {
+    for (int l = 0; l < sh.n_layers; ++l) {
+      const DevLayer& L = m.layers[size_t(l)];
+      linear<EPI_STORE>(E, L.wqkv, nqkv, d, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
+      linear<EPI_RESID>(E, L.wo, d, m.qd, m.attn, M, m.x, d, nullptr, 0, s);
+      linear<EPI_SWIGLU>(E, L.wgu, 2 * F, d, m.xb, M, nullptr, 0, m.act, F, s);
+      linear<EPI_RESID>(E, L.wd, d, F, m.act, M, m.x, d, nullptr, 0, s);
+    }
+    linear<EPI_STORE>(E, m.head, sh.vocab, d, m.xb, M, m.logits, sh.vocab, nullptr, 0, s);
+  };
+  forward(E, m, E.P_pre, M, m.logits, s);  // warm
+  gemms();
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int i = 0; i < iters; ++i) forward(E, m, E.P_pre, M, m.logits, s);
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaEventSynchronize(E.ev_t1));
+  float f_ms = 0.f;
+  CK(cudaEventElapsedTime(&f_ms, E.ev_t0, E.ev_t1));
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int i = 0; i < iters; ++i) gemms();
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaEventSynchronize(E.ev_t1));
+  float g_ms = 0.f;
+  CK(cudaEventElapsedTime(&g_ms, E.ev_t0, E.ev_t1));
+  *ms_forward = f_ms / iters;
+  *ms_gemm = g_ms / iters;
+  // algorithmic bytes: every weight once + bf16 activations in + fp32 out
+  const int64_t act = int64_t(M) * (int64_t(sh.n_layers) * (2LL * d + 2LL * m.qd + 2LL * d + 2LL * F +
+                                                              4LL * nqkv + 8LL * d + 2LL * F + 8LL * d) +
+                                    2LL * d + 4LL * sh.vocab);
+  *gemm_bytes = m.weight_bytes + act;
+  *gemm_launches = 4 * sh.n_layers + 1;
+  API_END
+}
+
+ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  uint64_t* d = dalloc<uint64_t>(size_t(n));
+  Mt64* m = dalloc<Mt64>(1);
+  mt_init_kernel<<<1, 32>>>(m, seed);
+  mt_draw_kernel<<<1, 32>>>(m, n, d);
+  KCHECK();
+  CK(cudaMemcpy(out, d, size_t(n) * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(m);
+  API_END
+}
+
+ssd_status ssd_weight_bits(ssd_engine* h, int32_t which, int32_t layer, int32_t kind, const int64_t* rows,
+                           const int64_t* cols, int32_t n, uint16_t* out) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  Model& m = which == 0 ? E.T : E.D;
+  const size_t d = size_t(m.s.d_model);
+  for (int i = 0; i < n; ++i) {
+    const size_t r = size_t(rows[i]), c = size_t(cols[i]);
+    const bf16* p = nullptr;
+    if (kind == 100) p = m.embed + r * d + c;
+    else if (kind == 101) p = m.head + r * d + c;
+    else {
+      if (layer < 0 || layer >= m.s.n_layers) throw Fail(SSD_ERROR, "weight_bits: bad layer");
+      const DevLayer& L = m.layers[size_t(layer)];
+      switch (kind) {
+        case 0: p = L.wqkv + r * d + c; break;
+        case 1: p = L.wqkv + (size_t(m.qd) + r) * d + c; break;
+        case 2: p = L.wqkv + (size_t(m.qd + m.kvd) + r) * d + c; break;
+        case 3: p = L.wo + r * size_t(m.qd) + c; break;
+        case 4: p = L.wgu + (2 * r) * d + c; break;
+        case 5: p = L.wgu + (2 * r + 1) * d + c; break;
+        case 6: p = L.wd + r * size_t(m.s.ffn) + c; break;
+        default: throw Fail(SSD_ERROR, "weight_bits: bad kind");
+      }
+    }
+    CK(cudaMemcpy(&out[i], p, 2, cudaMemcpyDeviceToHost));
+  }
+  API_END
+}
+
+}  // extern "C"

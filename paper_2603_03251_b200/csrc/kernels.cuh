@@ -1,0 +1,862 @@
+// Device kernels of the B200 Saguaro engine (sm_100a).
+//
+// Decode-step kernels (the replacement of lm::SyntheticLM::logits_at,
+// reference lm.cpp:82-84) and the SSD control kernels (specdec.cpp:8-69,
+// cache.cpp:232-277, sim.cpp:35-48, 258-601) that keep the whole round on
+// the device. Layout conventions are in DESIGN.md §3.
+#pragma once
+
+#include "common.cuh"
+
+namespace ssd {
+
+typedef __nv_bfloat16 bf16;
+
+// ------------------------------------------------------------------ params
+// Per-forward token table (device memory, written by the prep kernels).
+struct FwdParams {
+  int tokens[kMaxM];
+  int pos[kMaxM];       // RoPE position
+  int slot[kMaxM];      // KV slot written by this token
+  int main_len[kMaxM];  // visible main-cache slots [0, main_len)
+  int bbase[kMaxM];     // visible branch slots [bbase, bbase + blen)
+  int blen[kMaxM];
+};
+
+// Device-resident loop state: the harness' two processes' bookkeeping
+// (sim.cpp:321-485) and the sim::RunStats counters (sim.hpp:55-104).
+struct LoopState {
+  int n;             // history length (tokens in hist[])
+  int round;         // rounds completed
+  int rounds;        // rounds requested
+  int K;
+  int spec[kMaxK];   // in-flight speculation
+  int spec_origin;   // 0 Primary, 1 Backup
+  int spec_src;      // 0 Initial, 1 CacheHit, 2 Backup
+  int spec_uniform;  // dists are exactly uniform (FastRandom)
+  const float* spec_rows[kMaxK];  // draft logit rows the tokens were drawn from
+  int out_k, out_t;  // last verification outcome
+  int hit;           // last lookup
+  int error;         // ssd_status raised on the device (0 = ok)
+  int backup_kind;   // 0 SamePrimaryJIT, 1 FastRandom
+  int pad_;
+  double clock;      // harness virtual clock
+  double primary_time, backup_time;
+  long long tokens, p_lookups, p_hits, b_lookups, b_hits;
+  long long hit_rounds, miss_rounds, initial_rounds, hit_round_tokens, miss_round_tokens;
+  double accepted_sum;
+  Mt64 vrng;         // verifier stream
+  Mt64 drng;         // draft stream (the single stream for AR / SD)
+};
+
+// Scheme in device form (categorical.hpp:43-60).
+struct DScheme {
+  int saguaro;
+  int fan_out;
+  double tau;   // 0 = greedy
+  double C;
+};
+
+// ------------------------------------------------------------------ weights
+// Synthetic weight generator: a pure function of
+// (seed, tensor id, flat index), bit-identical to oracle/transformer_lm.cpp.
+struct GenShape { int d, heads, kv_heads, head_dim, ffn; };
+struct GenPair { uint64_t seed; float embed_scale, shared_mlp_scale, block_out_scale, priv_embed, priv_head, gain_mix; };
+
+__device__ __forceinline__ float unit_value(uint64_t key, uint64_t idx) {
+  const uint64_t h = derive_seed(key, idx);
+  const int32_t top = int32_t(uint32_t(h >> 32));
+  return float(top >> 8) * 0x1.0p-23f;
+}
+
+__device__ __forceinline__ uint32_t layer_tensor_id(int role, int layer, int kind) {
+  return (uint32_t(role) << 24) | (uint32_t(layer) << 8) | uint32_t(kind);
+}
+
+__device__ __forceinline__ size_t in_dim(const GenShape& s, int kind) {
+  if (kind == 3) return size_t(s.heads) * size_t(s.head_dim);  // WO
+  if (kind == 6) return size_t(s.ffn);                         // WD
+  return size_t(s.d);
+}
+
+__device__ inline bf16 layer_elem(const GenShape& self, const GenShape& dr, const GenPair& p, int role, int l,
+                                  int kind, size_t r, size_t c) {
+  const GenShape* sh = &self;
+  if (role == 0 && l == 0) {
+    const bool gu = (kind == 4 || kind == 5) && r < size_t(dr.ffn) && c < size_t(dr.d);
+    const bool dn = kind == 6 && r < size_t(dr.d) && c < size_t(dr.ffn);
+    if (gu || dn) { role = 1; sh = &dr; }
+  }
+  const size_t in = in_dim(*sh, kind);
+  float scale = 1.0f / sqrtf(float(in));
+  if (kind == 3) scale = p.block_out_scale * scale;
+  if (kind == 6) scale = ((role == 1 && l == 0) ? p.shared_mlp_scale : p.block_out_scale) * scale;
+  const uint64_t key = derive_seed(p.seed, layer_tensor_id(role, l, kind));
+  return __float2bfloat16_rn(unit_value(key, r * in + c) * scale);
+}
+
+// Fill device rows [row_off + row_stride * r] of dst (row length cols) with
+// logical tensor (role, layer, kind) rows [0, rows).
+__global__ void gen_layer_kernel(bf16* dst, int rows, int cols, int row_stride, int row_off, GenShape self,
+                                 GenShape dr, GenPair p, int role, int layer, int kind) {
+  const size_t total = size_t(rows) * size_t(cols);
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = e / size_t(cols), c = e % size_t(cols);
+    dst[(size_t(row_off) + size_t(row_stride) * r) * size_t(cols) + c] = layer_elem(self, dr, p, role, layer, kind, r, c);
+  }
+}
+
+// Embedding / LM head [V][d]: shared table S in dims [0, ds), target-private
+// tables beyond (oracle transformer_lm.cpp constructor).
+__global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int which /*0 embed 1 head*/) {
+  const uint64_t kS = derive_seed(p.seed, 0xE0000001u), kPE = derive_seed(p.seed, 0xE0000002u),
+                 kPH = derive_seed(p.seed, 0xE0000003u);
+  const size_t total = size_t(V) * size_t(d), dp = size_t(d - ds);
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t v = e / size_t(d), i = e % size_t(d);
+    float val;
+    if (i < size_t(ds)) {
+      val = unit_value(kS, v * size_t(ds) + i) * p.embed_scale;
+    } else {
+      const size_t j = v * dp + (i - size_t(ds));
+      val = which == 0 ? unit_value(kPE, j) * p.priv_embed : unit_value(kPH, j) * p.priv_head;
+    }
+    dst[e] = __float2bfloat16_rn(val);
+  }
+}
+
+// ------------------------------------------------------------------ forward
+// x[m][:] = E[token_m][:] (fp32 residual stream)
+__global__ void embed_kernel(const bf16* __restrict__ E, int d, const FwdParams* __restrict__ P, float* __restrict__ x) {
+  const int m = blockIdx.x;
+  const bf16* row = E + size_t(P->tokens[m]) * size_t(d);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[size_t(m) * d + i] = __bfloat162float(row[i]);
+}
+
+// RMSNorm (gain optional) with bf16 rounding of the output: the GEMM input
+// precision (oracle rmsnorm_bf16).
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int d, const float* __restrict__ g, float eps,
+                               bf16* __restrict__ out) {
+  __shared__ float sh[32];
+  const int m = blockIdx.x;
+  const float* xr = x + size_t(m) * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  ss = block_sum(ss, sh);
+  const float r = 1.0f / sqrtf(ss / float(d) + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = xr[i] * r;
+    out[size_t(m) * d + i] = __float2bfloat16_rn(g ? v * g[i] : v);
+  }
+}
+
+enum Epi { EPI_STORE = 0, EPI_RESID = 1, EPI_SWIGLU = 2 };
+
+// Weight-streaming linear layer on CUDA cores: Y[m][r] (+)= sum_k W[r][k] X[m][k].
+// Each warp owns two weight rows and streams them once with 16-byte
+// non-allocating loads; tokens are processed MT at a time (re-reads of the
+// two rows for further token chunks hit L1/L2). Used for M = 1 decode steps.
+template <int EPI, int MT>
+__global__ void __launch_bounds__(256) linear_cc_kernel(const bf16* __restrict__ W, int N, int K,
+                                                        const bf16* __restrict__ X, int M, float* __restrict__ Y,
+                                                        int ldy, bf16* __restrict__ Yb, int ldyb) {
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int r0 = warp * 2;
+  if (r0 >= N) return;
+  const bool has1 = r0 + 1 < N;
+  const uint4* w0 = reinterpret_cast<const uint4*>(W + size_t(r0) * K);
+  const uint4* w1 = reinterpret_cast<const uint4*>(W + size_t(has1 ? r0 + 1 : r0) * K);
+  const int nvec = K >> 3;
+  constexpr int U = 4;
+  for (int m0 = 0; m0 < M; m0 += MT) {
+    const int mt = min(MT, M - m0);
+    float a0[MT], a1[MT];
+#pragma unroll
+    for (int t = 0; t < MT; ++t) a0[t] = a1[t] = 0.f;
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+      uint4 wa[U], wb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + 32 * u;
+        if (v < nvec) { wa[u] = ldg_stream(w0 + v); wb[u] = ldg_stream(w1 + v); }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + 32 * u;
+        if (v < nvec) {
+          float fa[8], fb[8];
+          bf16x8_to_f32(wa[u], fa);
+          bf16x8_to_f32(wb[u], fb);
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            if (t < mt) {
+              const uint4 xv = __ldg(reinterpret_cast<const uint4*>(X + size_t(m0 + t) * K) + v);
+              float fx[8];
+              bf16x8_to_f32(xv, fx);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) { a0[t] += fa[i] * fx[i]; a1[t] += fb[i] * fx[i]; }
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      if (t < mt) {
+        const float s0 = warp_sum(a0[t]), s1 = warp_sum(a1[t]);
+        if (lane == 0) {
+          const int m = m0 + t;
+          if (EPI == EPI_STORE) {
+            Y[size_t(m) * ldy + r0] = s0;
+            if (has1) Y[size_t(m) * ldy + r0 + 1] = s1;
+          } else if (EPI == EPI_RESID) {
+            Y[size_t(m) * ldy + r0] += s0;
+            if (has1) Y[size_t(m) * ldy + r0 + 1] += s1;
+          } else {  // SwiGLU: rows (2j, 2j+1) = (gate_j, up_j)
+            const float act = s0 / (1.0f + expf(-s0)) * s1;
+            Yb[size_t(m) * ldyb + (r0 >> 1)] = __float2bfloat16_rn(act);
+          }
+        }
+      }
+    }
+  }
+}
+
+// RoPE (rotate-half pairs (i, i + hd/2)) on q and k, KV-cache append in bf16.
+// qkv row layout: [q: H*hd][k: KVH*hd][v: KVH*hd]. grid (M, H + KVH).
+__global__ void rope_append_kernel(const float* __restrict__ qkv, int H, int KVH, int hd, const FwdParams* __restrict__ P,
+                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                   float* __restrict__ q_out, bf16* __restrict__ kc, bf16* __restrict__ vc, int S) {
+  const int m = blockIdx.x, hh = blockIdx.y, half = hd >> 1;
+  const int pos = P->pos[m], slot = P->slot[m];
+  const size_t row = size_t(m) * size_t((H + 2 * KVH) * hd);
+  const float* cs = cos_t + size_t(pos) * half;
+  const float* sn = sin_t + size_t(pos) * half;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    if (hh < H) {
+      const float* src = qkv + row + size_t(hh) * hd;
+      const float a = src[i], b = src[i + half];
+      float* dst = q_out + size_t(m) * H * hd + size_t(hh) * hd;
+      dst[i] = a * cs[i] - b * sn[i];
+      dst[i + half] = b * cs[i] + a * sn[i];
+    } else {
+      const int kh = hh - H;
+      const float* ks = qkv + row + size_t(H) * hd + size_t(kh) * hd;
+      const float* vs = qkv + row + size_t(H + KVH) * hd + size_t(kh) * hd;
+      const float a = ks[i], b = ks[i + half];
+      bf16* kd = kc + (size_t(kh) * S + slot) * hd;
+      bf16* vd = vc + (size_t(kh) * S + slot) * hd;
+      kd[i] = __float2bfloat16_rn(a * cs[i] - b * sn[i]);
+      kd[i + half] = __float2bfloat16_rn(b * cs[i] + a * sn[i]);
+      vd[i] = __float2bfloat16_rn(vs[i]);
+      vd[i + half] = __float2bfloat16_rn(vs[i + half]);
+    }
+  }
+}
+
+// Decode attention over a main-cache prefix plus a branch-local segment
+// (the tree/branch mask of pre-speculation, generated arithmetically from
+// (main_len, bbase, blen) instead of materialised). grid (H, M), 128 threads.
+__global__ void __launch_bounds__(128) attention_kernel(const float* __restrict__ q, const bf16* __restrict__ kc,
+                                                        const bf16* __restrict__ vc, int S, const FwdParams* __restrict__ P,
+                                                        int H, int KVH, int hd, float scale, bf16* __restrict__ out) {
+  extern __shared__ float smem[];
+  __shared__ float red[32];
+  const int h = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
+  const int kvh = h / (H / KVH);
+  const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
+  const int nk = main_len + blen;
+  float* qs = smem;           // hd
+  float* sc = smem + hd;      // nk
+  float* part = sc + nk;      // blockDim
+  for (int i = tid; i < hd; i += blockDim.x) qs[i] = q[size_t(m) * H * hd + size_t(h) * hd + i];
+  __syncthreads();
+  const bf16* kbase = kc + size_t(kvh) * S * hd;
+  const bf16* vbase = vc + size_t(kvh) * S * hd;
+  float mx = -INFINITY;
+  for (int j = tid; j < nk; j += blockDim.x) {
+    const int slot = j < main_len ? j : bbase + (j - main_len);
+    const uint4* kr = reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
+    float dot = 0.f;
+    for (int c = 0; c < (hd >> 3); ++c) {
+      float f[8];
+      bf16x8_to_f32(kr[c], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dot += qs[c * 8 + i] * f[i];
+    }
+    const float s = dot * scale;
+    sc[j] = s;
+    mx = fmaxf(mx, s);
+  }
+  mx = warp_max(mx);
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+  float den = 0.f;
+  for (int j = tid; j < nk; j += blockDim.x) {
+    const float e = expf(sc[j] - mx);
+    sc[j] = e;
+    den += e;
+  }
+  den = block_sum(den, red);
+  __syncthreads();
+  const int parts = blockDim.x / hd;  // hd in {64, 128}
+  const int dd = tid % hd, pp = tid / hd;
+  float acc = 0.f;
+  if (pp < parts) {
+    for (int j = pp; j < nk; j += parts) {
+      const int slot = j < main_len ? j : bbase + (j - main_len);
+      acc += sc[j] * __bfloat162float(vbase[size_t(slot) * hd + dd]);
+    }
+  }
+  part[tid] = acc;
+  __syncthreads();
+  if (tid < hd) {
+    float o = 0.f;
+    for (int p2 = 0; p2 < parts; ++p2) o += part[p2 * hd + tid];
+    out[size_t(m) * H * hd + size_t(h) * hd + tid] = __float2bfloat16_rn(o / den);
+  }
+}
+
+// ------------------------------------------------------------------ top-k
+// Block-wide top-T in the (value desc, index asc) order of
+// dist::top_indices (categorical.cpp:35-48). Each thread keeps a sorted
+// local list over a strided slice; warps merge by repeated warp argmax, then
+// warp 0 merges the warp lists. Result in out[0..T) (shared memory).
+template <int NT>
+__device__ void block_topk(const float* __restrict__ z, int V, int T, VI* out, VI* wl /* (NT/32) * T */) {
+  VI L[kMaxTopF + 1];
+  for (int t = 0; t < T; ++t) L[t] = VI{-INFINITY, 0x7fffffff};
+  for (int j = threadIdx.x; j < V; j += NT) {
+    const float v = z[j];
+    if (ranks_before(v, j, L[T - 1].v, L[T - 1].i)) {
+      int p = T - 1;
+      while (p > 0 && ranks_before(v, j, L[p - 1].v, L[p - 1].i)) { L[p] = L[p - 1]; --p; }
+      L[p] = VI{v, j};
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int head = 0;
+  for (int t = 0; t < T; ++t) {
+    VI mine = head < T ? L[head] : VI{-INFINITY, 0x7fffffff};
+    VI best = warp_best(mine);
+    if (head < T && mine.v == best.v && mine.i == best.i) ++head;
+    if (lane == 0) wl[w * T + t] = best;
+  }
+  __syncthreads();
+  if (w == 0) {
+    constexpr int NW = NT / 32;
+    int h2 = 0;
+    for (int t = 0; t < T; ++t) {
+      VI mine = (lane < NW && h2 < T) ? wl[lane * T + h2] : VI{-INFINITY, 0x7fffffff};
+      VI best = warp_best(mine);
+      if (lane < NW && h2 < T && mine.v == best.v && mine.i == best.i) ++h2;
+      if (lane == 0) out[t] = best;
+    }
+  }
+  __syncthreads();
+}
+
+// Cache keys (cache.cpp:249-270): for row k, the first fan[k] tokens of the
+// ranking that differ from excl[k]. Writes keys[k*max_f + j] (-1 padded) and
+// the flat branch list (bk, bt) at offset off[k]. grid = rows, 256 threads.
+// Plans are [2][rows] (Primary, Backup); with `st` the plan follows the
+// in-flight speculation's origin and the exclusions are its tokens.
+__global__ void __launch_bounds__(256) keys_kernel(const float* __restrict__ rows, int V, const int* __restrict__ fan2,
+                                                   const int* __restrict__ off2, const LoopState* __restrict__ st,
+                                                   const int* __restrict__ excl_explicit, int n_excl, int max_f,
+                                                   int* __restrict__ keys, int* __restrict__ bk, int* __restrict__ btok) {
+  __shared__ VI top[kMaxTopF + 1];
+  __shared__ VI wl[8 * (kMaxTopF + 1)];
+  const int k = blockIdx.x, nrows = gridDim.x;
+  const int origin = st ? st->spec_origin : 0;
+  const int* fan = fan2 + origin * nrows;
+  const int* off = off2 + origin * nrows;
+  const int* excl_tok = st ? st->spec : excl_explicit;
+  const int F = fan[k];
+  if (F <= 0) {
+    for (int j = threadIdx.x; j < max_f; j += blockDim.x) keys[k * max_f + j] = -1;
+    return;
+  }
+  const int excl = k < n_excl ? excl_tok[k] : -1;
+  const int T = min(F + 1, V);
+  block_topk<256>(rows + size_t(k) * V, V, T, top, wl);
+  if (threadIdx.x == 0) {
+    int got = 0;
+    for (int t = 0; t < T && got < F; ++t) {
+      const int cand = top[t].i;
+      if (cand == excl) continue;
+      keys[k * max_f + got] = cand;
+      bk[off[k] + got] = k;
+      btok[off[k] + got] = cand;
+      ++got;
+    }
+    for (int j = got; j < max_f; ++j) keys[k * max_f + j] = -1;
+  }
+}
+
+// ------------------------------------------------------------------ sampling
+// Greedy / sampled draw from one logit row under a scheme, with the uniform
+// u[row] (dist::apply_scheme + dist::sample, categorical.cpp:65-92, 129-143).
+// Probabilities in fp64 like the reference; the inverse CDF is a blocked
+// prefix sum. grid = rows, 1024 threads.
+constexpr int kSampleThreads = 1024;
+
+__device__ inline int sample_row(const float* __restrict__ z, int V, const DScheme& s, double u) {
+  __shared__ double shd[32];
+  __shared__ VI shv[32];
+  __shared__ VI top[kMaxTopF + 1];
+  __shared__ VI wl[(kSampleThreads / 32) * (kMaxTopF + 1)];
+  __shared__ int pick;
+  const int tid = threadIdx.x;
+  if (s.tau == 0.0) {
+    if (s.saguaro && s.C == 0.0) {  // greedy with the top-F set removed: rank F
+      block_topk<kSampleThreads>(z, V, s.fan_out + 1, top, wl);
+      return top[s.fan_out].i;
+    }
+    VI b{-INFINITY, 0x7fffffff};
+    for (int j = tid; j < V; j += blockDim.x)
+      if (ranks_before(z[j], j, b.v, b.i)) b = VI{z[j], j};
+    b = block_best(b, shv);
+    return b.i;
+  }
+  VI thr{INFINITY, -1};  // F-th ranked element when Saguaro
+  if (s.saguaro) {
+    block_topk<kSampleThreads>(z, V, s.fan_out, top, wl);
+    thr = top[s.fan_out - 1];
+  }
+  const double tau = s.tau;
+  double mx = -INFINITY;
+  for (int j = tid; j < V; j += blockDim.x) mx = fmax(mx, double(z[j]) / tau);
+  mx = block_maxd(mx, shd);
+  // contiguous chunk per thread for the ordered scan
+  const int chunk = (V + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(V, tid * chunk), b1 = min(V, b0 + chunk);
+  auto weight = [&](int j) {
+    double w = exp(double(z[j]) / tau - mx);
+    if (s.saguaro && (ranks_before(z[j], j, thr.v, thr.i) || j == thr.i)) w *= s.C;
+    return w;
+  };
+  double loc = 0.0;
+  for (int j = b0; j < b1; ++j) loc += weight(j);
+  const double S = block_sum(loc, shd);
+  // exclusive scan of per-thread probability mass
+  double pm = 0.0;
+  for (int j = b0; j < b1; ++j) pm += weight(j) / S;
+  __shared__ double wsum[32];
+  const int lane = tid & 31, w = tid >> 5;
+  double incl = pm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[w] = incl;
+  if (tid == 0) pick = 0x7fffffff;
+  __syncthreads();
+  double before = 0.0;
+  for (int i = 0; i < w; ++i) before += wsum[i];
+  const double excl = before + incl - pm;
+  if (b0 < b1 && u < excl + pm) atomicMin(&pick, tid);
+  __syncthreads();
+  __shared__ int result;
+  if (tid == pick) {
+    double c = excl;
+    int r = b1 - 1;
+    for (int j = b0; j < b1; ++j) {
+      c += weight(j) / S;
+      if (u < c) { r = j; break; }
+    }
+    result = r;
+  }
+  __syncthreads();
+  if (pick == 0x7fffffff) {  // rounding left the total below u: last positive
+    int last = -1;
+    for (int j = tid; j < V; j += blockDim.x) if (weight(j) > 0.0) last = max(last, j);
+    VI lv{float(last), last};
+    lv = block_best(lv, shv);
+    return lv.i;
+  }
+  return result;
+}
+
+// Draw `n` uniforms from a device stream into u[] (the single-stream
+// consumption of run_ar / run_sd, sim.cpp:64-121).
+__global__ void draw_uniforms_kernel(Mt64* st, double* u, int n) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int i = 0; i < n; ++i) u[i] = mt_unit(*st);
+}
+
+// Sample rows[r] with u[r]; token written to out[r * out_stride].
+__global__ void __launch_bounds__(kSampleThreads) sample_rows_kernel(const float* __restrict__ rows, int V, DScheme s,
+                                                                    const double* __restrict__ u, int u_stride,
+                                                                    int* __restrict__ out, int out_stride) {
+  const int r = blockIdx.x;
+  const int t = sample_row(rows + size_t(r) * V, V, s, u ? u[size_t(r) * u_stride] : 0.0);
+  if (threadIdx.x == 0) out[size_t(r) * out_stride] = t;
+}
+
+// ------------------------------------------------------------------ verify
+// Per-row statistics for verification: max(z/tau) and sum of scheme weights
+// for target rows [0, K] and draft rows [0, K), plus argmax (greedy) and the
+// Saguaro threshold element. grid = 2K + 1, 1024 threads.
+struct RowStat {
+  double mx, S;
+  int argmax;
+  float thr_v;
+  int thr_i;
+};
+
+__device__ inline double scheme_weight(float zj, int j, double mx, const DScheme& s, const RowStat& st) {
+  double w = exp(double(zj) / s.tau - mx);
+  if (s.saguaro && (ranks_before(zj, j, st.thr_v, st.thr_i) || j == st.thr_i)) w *= s.C;
+  return w;
+}
+
+__global__ void __launch_bounds__(kSampleThreads) verify_stats_kernel(const float* __restrict__ trows,
+                                                                     const LoopState* __restrict__ st, int V,
+                                                                     DScheme ts, DScheme ds, RowStat* __restrict__ out) {
+  __shared__ double shd[32];
+  __shared__ VI shv[32];
+  __shared__ VI top[kMaxTopF + 1];
+  __shared__ VI wl[(kSampleThreads / 32) * (kMaxTopF + 1)];
+  const int K = st->K;
+  const int r = blockIdx.x;
+  const bool target = r <= K;
+  if (!target && st->spec_uniform) return;
+  const float* z = target ? trows + size_t(r) * V : st->spec_rows[r - K - 1];
+  const DScheme s = target ? ts : ds;
+  RowStat rs{0.0, 0.0, 0, INFINITY, -1};
+  VI b{-INFINITY, 0x7fffffff};
+  for (int j = threadIdx.x; j < V; j += blockDim.x)
+    if (ranks_before(z[j], j, b.v, b.i)) b = VI{z[j], j};
+  b = block_best(b, shv);
+  rs.argmax = b.i;
+  if (s.tau > 0.0) {
+    if (s.saguaro) {
+      block_topk<kSampleThreads>(z, V, s.fan_out, top, wl);
+      rs.thr_v = top[s.fan_out - 1].v;
+      rs.thr_i = top[s.fan_out - 1].i;
+    }
+    double mx = -INFINITY;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmax(mx, double(z[j]) / s.tau);
+    mx = block_maxd(mx, shd);
+    rs.mx = mx;
+    double loc = 0.0;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) loc += scheme_weight(z[j], j, mx, s, rs);
+    rs.S = block_sum(loc, shd);
+  } else if (s.saguaro && s.C == 0.0) {
+    block_topk<kSampleThreads>(z, V, s.fan_out + 1, top, wl);
+    rs.argmax = top[s.fan_out].i;
+  }
+  if (threadIdx.x == 0) out[r] = rs;
+}
+
+// Probability of token j in a row under scheme s (greedy: one-hot).
+__device__ __forceinline__ double row_prob(const float* z, int j, const DScheme& s, const RowStat& st) {
+  if (s.tau == 0.0) return j == st.argmax ? 1.0 : 0.0;
+  return scheme_weight(z[j], j, st.mx, s, st) / st.S;
+}
+
+// The verification decision (specdec.cpp:27-69) and history append.
+// One CTA of 1024 threads; thread 0 walks the accept coins on the
+// verifier stream, then the block samples the bonus from the residual
+// (or from the target row K when everything is accepted).
+__global__ void __launch_bounds__(kSampleThreads) verify_decide_kernel(const float* __restrict__ trows, LoopState* st,
+                                                                      int* __restrict__ hist, int V, DScheme ts, DScheme ds,
+                                                                      double accept_scale, const RowStat* __restrict__ rs,
+                                                                      int use_draft_stream) {
+  __shared__ int s_k;
+  __shared__ double s_u;
+  __shared__ int s_err;
+  __shared__ double shd[32];
+  __shared__ VI shv[32];
+  const int K = st->K;
+  Mt64& rng = use_draft_stream ? st->drng : st->vrng;
+  const bool uni = st->spec_uniform != 0;
+  const double inv_v = 1.0 / double(V);
+  if (threadIdx.x == 0) {
+    int k = K;
+    s_err = 0;
+    for (int i = 0; i < K; ++i) {
+      const int x = st->spec[i];
+      const double pt = row_prob(trows + size_t(i) * V, x, ts, rs[i]);
+      const double pd = uni ? inv_v : row_prob(st->spec_rows[i], x, ds, rs[K + 1 + i]);
+      if (!(pd > 0.0)) { s_err = 1; k = i; break; }
+      double a = fmin(1.0, pt / pd);
+      a = fmin(1.0, a * accept_scale);
+      if (mt_unit(rng) < a) continue;
+      k = i;
+      break;
+    }
+    s_k = k;
+    s_u = mt_unit(rng);  // the bonus draw
+  }
+  __syncthreads();
+  const int k = s_k;
+  const double u = s_u;
+  const float* zt = trows + size_t(k) * V;
+  const RowStat& tst = rs[k];
+  int bonus;
+  if (k == K) {  // all accepted: bonus ~ target row K
+    bonus = -1;
+    if (ts.tau == 0.0) {
+      bonus = tst.argmax;
+    } else {
+      // inverse CDF of the target row, thread-chunked like sample_row
+      const int chunk = (V + blockDim.x - 1) / blockDim.x;
+      const int b0 = min(V, int(threadIdx.x) * chunk), b1 = min(V, b0 + chunk);
+      double pm = 0.0;
+      for (int j = b0; j < b1; ++j) pm += row_prob(zt, j, ts, tst);
+      __shared__ double wsum[32];
+      __shared__ int pick;
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      double incl = pm;
+      for (int o = 1; o < 32; o <<= 1) { const double t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
+      __syncthreads();
+      if (lane == 31) wsum[w] = incl;
+      if (threadIdx.x == 0) pick = 0x7fffffff;
+      __syncthreads();
+      double before = 0.0;
+      for (int i = 0; i < w; ++i) before += wsum[i];
+      const double ex = before + incl - pm;
+      if (b0 < b1 && u < ex + pm) atomicMin(&pick, int(threadIdx.x));
+      __syncthreads();
+      __shared__ int res;
+      if (int(threadIdx.x) == pick) {
+        double c = ex;
+        int r = b1 - 1;
+        for (int j = b0; j < b1; ++j) { c += row_prob(zt, j, ts, tst); if (u < c) { r = j; break; } }
+        res = r;
+      }
+      __syncthreads();
+      if (pick == 0x7fffffff) {
+        int last = -1;
+        for (int j = threadIdx.x; j < V; j += blockDim.x) if (row_prob(zt, j, ts, tst) > 0.0) last = max(last, j);
+        VI lv{float(last), last};
+        lv = block_best(lv, shv);
+        res = lv.i;
+      }
+      __syncthreads();
+      bonus = res;
+    }
+  } else if (ts.tau == 0.0) {
+    bonus = tst.argmax;  // residual of one-hot target against any draft law
+  } else {
+    // residual max(p_t - p_d, 0), normalised (categorical.cpp:94-110)
+    const float* zd = uni ? nullptr : st->spec_rows[k];
+    const RowStat& dst = rs[K + 1 + k];
+    auto resid = [&](int j) {
+      const double pt = row_prob(zt, j, ts, tst);
+      const double pd = uni ? inv_v : row_prob(zd, j, ds, dst);
+      return fmax(pt - pd, 0.0);
+    };
+    const int chunk = (V + blockDim.x - 1) / blockDim.x;
+    const int b0 = min(V, int(threadIdx.x) * chunk), b1 = min(V, b0 + chunk);
+    double loc = 0.0;
+    for (int j = b0; j < b1; ++j) loc += resid(j);
+    const double R = block_sum(loc, shd);
+    if (!(R > 0.0)) {
+      if (threadIdx.x == 0) s_err = 3;
+      bonus = 0;
+    } else {
+      double pm = 0.0;
+      for (int j = b0; j < b1; ++j) pm += resid(j) / R;
+      __shared__ double wsum[32];
+      __shared__ int pick;
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      double incl = pm;
+      for (int o = 1; o < 32; o <<= 1) { const double t = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += t; }
+      __syncthreads();
+      if (lane == 31) wsum[w] = incl;
+      if (threadIdx.x == 0) pick = 0x7fffffff;
+      __syncthreads();
+      double before = 0.0;
+      for (int i = 0; i < w; ++i) before += wsum[i];
+      const double ex = before + incl - pm;
+      if (b0 < b1 && u < ex + pm) atomicMin(&pick, int(threadIdx.x));
+      __syncthreads();
+      __shared__ int res;
+      if (int(threadIdx.x) == pick) {
+        double c = ex;
+        int r = b1 - 1;
+        for (int j = b0; j < b1; ++j) { c += resid(j) / R; if (u < c) { r = j; break; } }
+        res = r;
+      }
+      __syncthreads();
+      if (pick == 0x7fffffff) {
+        int last = -1;
+        for (int j = threadIdx.x; j < V; j += blockDim.x) if (resid(j) > 0.0) last = max(last, j);
+        VI lv{float(last), last};
+        lv = block_best(lv, shv);
+        res = lv.i;
+      }
+      __syncthreads();
+      bonus = res;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (s_err == 1) st->error = 1;
+    if (s_err == 3) st->error = 3;
+    st->out_k = k;
+    st->out_t = bonus;
+    const int n = st->n;
+    for (int i = 0; i < k; ++i) hist[n + i] = st->spec[i];
+    hist[n + k] = bonus;
+    st->tokens += k + 1;
+    st->accepted_sum += double(k);
+  }
+}
+
+// ------------------------------------------------------------------ prep
+// Chain inputs [hist[n-1], spec[0..M-2]] at positions n-1 .. (verify /
+// extend / AR step). Causal visibility over the main cache.
+__global__ void prep_chain_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int M) {
+  const int m = threadIdx.x;
+  if (m >= M) return;
+  const int n = st->n;
+  const int tok = m == 0 ? hist[n - 1] : st->spec[m - 1];
+  const int pos = n - 1 + m;
+  P->tokens[m] = tok; P->pos[m] = pos; P->slot[m] = pos;
+  P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+}
+
+// Draft step i of specdec::draft: input hist[n-1] (i == 0) or spec[i-1].
+__global__ void prep_draft_step_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int i) {
+  if (threadIdx.x != 0) return;
+  const int n = st->n;
+  const int pos = n - 1 + i;
+  P->tokens[0] = i == 0 ? hist[n - 1] : st->spec[i - 1];
+  P->pos[0] = pos; P->slot[0] = pos; P->main_len[0] = pos + 1; P->bbase[0] = 0; P->blen[0] = 0;
+}
+
+// Prefill of hist[lo, hi) (chunked by the caller, M <= kMaxM).
+__global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, int lo, int M) {
+  const int m = threadIdx.x;
+  if (m >= M) return;
+  const int pos = lo + m;
+  P->tokens[m] = hist[pos]; P->pos[m] = pos; P->slot[m] = pos;
+  P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+}
+
+// Branch step j (cache.cpp:258-268 continuation drafts, batched): branch b
+// = (k_b, t_b) continues prefix hist ++ spec[0..k_b) with t_b, then its own
+// drafted tokens. KV of branch-local tokens lives in slots
+// kv_base + b*K + j; its attention sees main slots [0, n + k_b) plus its own
+// branch slots.
+__global__ void prep_branch_kernel(const LoopState* __restrict__ st, const int* __restrict__ bk, const int* __restrict__ btok,
+                                   const int* __restrict__ bt /* [B][K] */, FwdParams* P, int B, int j, int kv_base) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int K = st->K, n = st->n, k = bk[b];
+  P->tokens[b] = j == 0 ? btok[b] : bt[b * K + j - 1];
+  P->pos[b] = n + k + j;
+  P->slot[b] = kv_base + b * K + j;
+  P->main_len[b] = n + k;
+  P->bbase[b] = kv_base + b * K;
+  P->blen[b] = j + 1;
+}
+
+// Per-branch streams: base = one next_u64 of the draft stream (cache.cpp:245),
+// branch b draws K uniforms from Stream(derive_seed(base, b)) (cache.cpp:264).
+__global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__ bu /* [B][K] */, int need) {
+  __shared__ uint64_t base;
+  if (threadIdx.x == 0) base = mt_next(st->drng);
+  __syncthreads();
+  if (!need) return;
+  const int K = st->K;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    Mt64 m;
+    mt_seed(m, derive_seed(base, uint64_t(b)));
+    for (int j = 0; j < K; ++j) bu[b * K + j] = mt_unit(m);
+  }
+}
+
+// Lookup + backup + bookkeeping: the draft side's handle_outcomes
+// (sim.cpp:418-463) and the harness clock (sim.cpp:528-577).
+// cum: exact sequential fp64 cumulative of the uniform law (categorical.cpp
+// :133-138 on a vector of 1/V), for the FastRandom tokens (sim.cpp:35-48).
+__global__ void lookup_kernel(LoopState* st, const int* __restrict__ keys, int max_f, const int* __restrict__ off,
+                              const int* __restrict__ bt, const float* __restrict__ brows, int B, int V,
+                              const double* __restrict__ cum, int* __restrict__ log_outcomes, int* __restrict__ log_hits) {
+  if (threadIdx.x != 0) return;
+  const int K = st->K;
+  const int k = st->out_k, t = st->out_t;
+  const int r = st->round;  // 0-based round being closed
+  // tokens attributed to the source of the verified speculation
+  const long long emitted = k + 1;
+  if (st->spec_src == 0) st->initial_rounds++;
+  else if (st->spec_src == 1) { st->hit_rounds++; st->hit_round_tokens += emitted; }
+  else { st->miss_rounds++; st->miss_round_tokens += emitted; }
+  if (log_outcomes) { log_outcomes[2 * r] = k; log_outcomes[2 * r + 1] = t; }
+  const double v0 = st->clock, v1 = v0 + 1.0, ready = v0 + st->primary_time;
+  st->n += k + 1;
+  st->round = r + 1;
+  if (r + 1 >= st->rounds) {  // last round: no lookup, no backup
+    st->clock = v1;
+    if (log_hits) log_hits[r] = -1;
+    return;
+  }
+  int b = -1;
+  for (int j = 0; j < max_f; ++j)
+    if (keys[k * max_f + j] == t) { b = off[k] + j; break; }
+  const bool hit = b >= 0;
+  const bool from_primary = st->spec_origin == 0;
+  if (from_primary) { st->p_lookups++; st->p_hits += hit; } else { st->b_lookups++; st->b_hits += hit; }
+  if (log_hits) log_hits[r] = hit ? 1 : 0;
+  st->hit = hit;
+  if (hit) {
+    for (int i = 0; i < K; ++i) {
+      st->spec[i] = bt[b * K + i];
+      st->spec_rows[i] = brows + (size_t(i) * B + b) * size_t(V);
+    }
+    st->spec_origin = 0; st->spec_src = 1; st->spec_uniform = 0;
+    st->clock = fmax(v1, ready);
+  } else {
+    st->spec_origin = 1; st->spec_src = 2;
+    st->clock = v1 + st->backup_time;
+    if (st->backup_kind == 1) {  // FastRandom: K uniform draws, exact CDF
+      for (int i = 0; i < K; ++i) {
+        const double u = mt_unit(st->drng);
+        int lo = 0, hi = V;  // first idx with u < cum[idx]
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (u < cum[mid]) hi = mid; else lo = mid + 1; }
+        st->spec[i] = lo < V ? lo : V - 1;
+        st->spec_rows[i] = nullptr;
+      }
+      st->spec_uniform = 1;
+    } else {
+      st->spec_uniform = 0;  // the host runs the JIT re-draft
+    }
+  }
+}
+
+// After a JIT / initial draft of spec[] from rows: origin bookkeeping.
+__global__ void set_spec_rows_kernel(LoopState* st, const float* __restrict__ rows, int V, int origin, int src) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < st->K; ++i) st->spec_rows[i] = rows + size_t(i) * V;
+  st->spec_origin = origin; st->spec_src = src; st->spec_uniform = 0;
+}
+
+// SD / AR commit: n += k + 1 (history already appended by verify).
+__global__ void commit_kernel(LoopState* st) {
+  if (threadIdx.x == 0) { st->n += st->out_k + 1; st->round += 1; }
+}
+
+// AR: append sampled token.
+__global__ void ar_commit_kernel(LoopState* st, int* hist, const int* tok) {
+  if (threadIdx.x == 0) { hist[st->n] = tok[0]; st->n += 1; st->tokens += 1; st->round += 1; }
+}
+
+__global__ void mt_init_kernel(Mt64* m, uint64_t seed) {
+  if (threadIdx.x == 0) mt_seed(*m, seed);
+}
+
+__global__ void mt_draw_kernel(Mt64* m, int n, uint64_t* out) {
+  if (threadIdx.x == 0) for (int i = 0; i < n; ++i) out[i] = mt_next(*m);
+}
+
+}  // namespace ssd
