@@ -69,6 +69,7 @@ typedef struct ssd_pair_params {
   uint64_t seed;
   float embed_scale, shared_mlp_scale, block_out_scale;
   float target_private_embed, target_private_head, draft_gain_mix;
+  float logit_scale; /* magnitude of the final RMSNorm gains */
 } ssd_pair_params;
 
 /* dist::SamplingScheme (categorical.hpp:43-60). temperature == 0 selects

@@ -110,6 +110,7 @@ PairParams parse_pair(const json& j) {
   p.target_private_embed = j.value("target_private_embed", p.target_private_embed);
   p.target_private_head = j.value("target_private_head", p.target_private_head);
   p.draft_gain_mix = j.value("draft_gain_mix", p.draft_gain_mix);
+  p.logit_scale = j.value("logit_scale", p.logit_scale);
   return p;
 }
 

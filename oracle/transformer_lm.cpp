@@ -189,9 +189,9 @@ TransformerLM::TransformerLM(const TfShape& s, const TfShape& dr, const PairPara
   const float comp = std::sqrt(float(ds) / float(s.d));  // rms over d vs d_draft
   for (std::size_t i = 0; i < d; ++i) {
     if (role == Role::Draft) {
-      final_gain_[i] = (1.0f - p.draft_gain_mix) * sign_of(kGS, i) + p.draft_gain_mix * sign_of(kGN, i);
+      final_gain_[i] = p.logit_scale * ((1.0f - p.draft_gain_mix) * sign_of(kGS, i) + p.draft_gain_mix * sign_of(kGN, i));
     } else {
-      final_gain_[i] = i < std::size_t(ds) ? sign_of(kGS, i) : sign_of(kGT, i - std::size_t(ds));
+      final_gain_[i] = p.logit_scale * (i < std::size_t(ds) ? sign_of(kGS, i) : sign_of(kGT, i - std::size_t(ds)));
       if (i < std::size_t(ds)) ffn_gain0_[i] = comp;
     }
   }

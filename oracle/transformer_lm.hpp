@@ -43,6 +43,7 @@ struct PairParams {
   float target_private_embed = 0.1f; // rho
   float target_private_head = 0.25f; // q
   float draft_gain_mix = 0.0f;       // epsilon
+  float logit_scale = 0.25f;         // magnitude of the final norm gains
 };
 
 enum class Role { Target = 0, Draft = 1 };

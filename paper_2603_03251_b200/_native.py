@@ -21,7 +21,7 @@ class ModelShape(C.Structure):
 class PairParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("embed_scale", C.c_float), ("shared_mlp_scale", C.c_float),
                 ("block_out_scale", C.c_float), ("target_private_embed", C.c_float),
-                ("target_private_head", C.c_float), ("draft_gain_mix", C.c_float)]
+                ("target_private_head", C.c_float), ("draft_gain_mix", C.c_float), ("logit_scale", C.c_float)]
 
 
 class Scheme(C.Structure):

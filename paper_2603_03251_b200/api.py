@@ -248,10 +248,12 @@ class Pair:
     target_private_embed: float = 0.1
     target_private_head: float = 0.25
     draft_gain_mix: float = 0.0
+    logit_scale: float = 0.25
 
     def c(self) -> N.PairParams:
         return N.PairParams(self.seed, self.embed_scale, self.shared_mlp_scale, self.block_out_scale,
-                            self.target_private_embed, self.target_private_head, self.draft_gain_mix)
+                            self.target_private_embed, self.target_private_head, self.draft_gain_mix,
+                            self.logit_scale)
 
     def as_dict(self) -> dict:
         return dict(self.__dict__)

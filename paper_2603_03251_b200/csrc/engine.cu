@@ -156,9 +156,10 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   const float comp = std::sqrt(float(ds) / float(d));
   for (int i = 0; i < d; ++i) {
     if (role == 1) {
-      fg[size_t(i)] = (1.0f - pp.draft_gain_mix) * sign_h(kGS, size_t(i)) + pp.draft_gain_mix * sign_h(kGN, size_t(i));
+      fg[size_t(i)] = pp.logit_scale * ((1.0f - pp.draft_gain_mix) * sign_h(kGS, size_t(i)) +
+                                        pp.draft_gain_mix * sign_h(kGN, size_t(i)));
     } else {
-      fg[size_t(i)] = i < ds ? sign_h(kGS, size_t(i)) : sign_h(kGT, size_t(i - ds));
+      fg[size_t(i)] = pp.logit_scale * (i < ds ? sign_h(kGS, size_t(i)) : sign_h(kGT, size_t(i - ds)));
       if (i < ds) g0[size_t(i)] = comp;
     }
   }
