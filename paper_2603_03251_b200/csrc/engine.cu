@@ -5,6 +5,8 @@
 // forward + decision || extend + keys + K branch steps, then lookup) is one
 // CUDA graph with a fork/join between the two streams, replayed per round
 // with no host synchronisation for the FastRandom backup.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +19,7 @@
 #include <vector>
 
 #include "../../include/ssd_b200.h"
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace ssd {
@@ -45,9 +48,48 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+// ------------------------------------------------------------------ TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static void init_encode() {
+  if (g_encode) return;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) throw Fail(SSD_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+// 2-D bf16 [rows][cols] row-major, box = 64 (K) x box_rows, 128B swizzle.
+static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  init_encode();
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {uint32_t(tc::kBK), box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Fail(SSD_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
 // ------------------------------------------------------------------ model
+struct WMat {
+  bf16* w = nullptr;
+  int N = 0, K = 0;
+  CUtensorMap map;
+};
+
 struct DevLayer {
-  bf16 *wqkv, *wo, *wgu, *wd;
+  WMat qkv, o, gu, dn;
+};
+
+struct ActMap {
+  const void* ptr;
+  int K, np;
+  CUtensorMap map;
 };
 
 struct Model {
@@ -55,7 +97,7 @@ struct Model {
   int role = 0;  // 0 target, 1 draft
   int qd = 0, kvd = 0;
   bf16* embed = nullptr;
-  bf16* head = nullptr;  // == embed when tied
+  WMat head;             // head.w == embed when tied
   float* final_gain = nullptr;
   float* ffn_gain0 = nullptr;
   std::vector<DevLayer> layers;
@@ -68,6 +110,10 @@ struct Model {
   float *x = nullptr, *qkv = nullptr, *q = nullptr, *logits = nullptr;
   bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
   int64_t weight_bytes = 0;
+  float* ws = nullptr;   // split-K partials
+  size_t ws_floats = 0;
+  int* counters = nullptr;
+  std::vector<ActMap> amaps;
   std::vector<void*> owned;
 
   size_t kv_layer_elems() const { return size_t(s.n_kv_heads) * size_t(S) * size_t(s.head_dim); }
@@ -137,17 +183,24 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   const GenPair gp{pp.seed, pp.embed_scale, pp.shared_mlp_scale, pp.block_out_scale, pp.target_private_embed,
                    pp.target_private_head, pp.draft_gain_mix};
   auto own = [&](void* p) { m.owned.push_back(p); return p; };
+  auto wmat = [&](WMat& w, int N, int K) {
+    w.N = N;
+    w.K = K;
+    if (!w.w) w.w = static_cast<bf16*>(own(dalloc<bf16>(size_t(N) * K)));
+    w.map = make_map(w.w, uint64_t(N), uint64_t(K), tc::kBM);
+  };
   // tables
   m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
   gen_table_kernel<<<148 * 8, 256>>>(m.embed, s.vocab, d, dr.d_model, gp, 0);
   KCHECK();
   if (s.tied) {
-    m.head = m.embed;
+    m.head.w = m.embed;
   } else {
-    m.head = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
-    gen_table_kernel<<<148 * 8, 256>>>(m.head, s.vocab, d, dr.d_model, gp, 1);
+    m.head.w = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
+    gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, 1);
     KCHECK();
   }
+  wmat(m.head, s.vocab, d);
   // norm gains (host, float arithmetic identical to the oracle)
   std::vector<float> fg(static_cast<size_t>(d)), g0(static_cast<size_t>(d), 1.0f);
   const uint64_t kGS = derive_seed(pp.seed, 0xE0000004u), kGN = derive_seed(pp.seed, 0xE0000005u),
@@ -172,17 +225,17 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   int64_t wb = 0;
   for (int l = 0; l < s.n_layers; ++l) {
     DevLayer& L = m.layers[size_t(l)];
-    L.wqkv = static_cast<bf16*>(own(dalloc<bf16>(size_t(m.qd + 2 * m.kvd) * d)));
-    L.wo = static_cast<bf16*>(own(dalloc<bf16>(size_t(d) * m.qd)));
-    L.wgu = static_cast<bf16*>(own(dalloc<bf16>(size_t(2 * s.ffn) * d)));
-    L.wd = static_cast<bf16*>(own(dalloc<bf16>(size_t(d) * s.ffn)));
-    gen_launch(L.wqkv, m.qd, d, 1, 0, s, dr, gp, role, l, 0);
-    gen_launch(L.wqkv, m.kvd, d, 1, m.qd, s, dr, gp, role, l, 1);
-    gen_launch(L.wqkv, m.kvd, d, 1, m.qd + m.kvd, s, dr, gp, role, l, 2);
-    gen_launch(L.wo, d, m.qd, 1, 0, s, dr, gp, role, l, 3);
-    gen_launch(L.wgu, s.ffn, d, 2, 0, s, dr, gp, role, l, 4);
-    gen_launch(L.wgu, s.ffn, d, 2, 1, s, dr, gp, role, l, 5);
-    gen_launch(L.wd, d, s.ffn, 1, 0, s, dr, gp, role, l, 6);
+    wmat(L.qkv, m.qd + 2 * m.kvd, d);
+    wmat(L.o, d, m.qd);
+    wmat(L.gu, 2 * s.ffn, d);
+    wmat(L.dn, d, s.ffn);
+    gen_launch(L.qkv.w, m.qd, d, 1, 0, s, dr, gp, role, l, 0);
+    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd, s, dr, gp, role, l, 1);
+    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd + m.kvd, s, dr, gp, role, l, 2);
+    gen_launch(L.o.w, d, m.qd, 1, 0, s, dr, gp, role, l, 3);
+    gen_launch(L.gu.w, s.ffn, d, 2, 0, s, dr, gp, role, l, 4);
+    gen_launch(L.gu.w, s.ffn, d, 2, 1, s, dr, gp, role, l, 5);
+    gen_launch(L.dn.w, d, s.ffn, 1, 0, s, dr, gp, role, l, 6);
     wb += int64_t(m.qd + 2 * m.kvd) * d + int64_t(d) * m.qd + int64_t(2 * s.ffn) * d + int64_t(d) * s.ffn;
   }
   wb += int64_t(s.vocab) * d;  // LM head
@@ -206,6 +259,9 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   m.attn = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * m.qd)));
   m.act = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * s.ffn)));
   m.logits = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.vocab)));
+  m.ws_floats = size_t(16) << 20;  // 64 MB of split-K partials
+  m.ws = static_cast<float*>(own(dalloc<float>(m.ws_floats)));
+  m.counters = static_cast<int*>(own(dalloc<int>(8192)));
 }
 
 static void free_model(Model& m) {
@@ -214,13 +270,56 @@ static void free_model(Model& m) {
 }
 
 // ------------------------------------------------------------------ forward
-template <int EPI>
-static void linear(Engine& E, const bf16* W, int N, int K, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                   cudaStream_t s) {
-  const int rows_per_cta = 16;  // 8 warps x 2 rows
-  linear_cc_kernel<EPI, 4><<<(N + rows_per_cta - 1) / rows_per_cta, 256, 0, s>>>(W, N, K, X, M, Y, ldy, Yb, ldyb);
+static const CUtensorMap& act_map(Model& m, const void* X, int K, int np) {
+  for (const ActMap& a : m.amaps)
+    if (a.ptr == X && a.K == K && a.np == np) return a.map;
+  m.amaps.push_back(ActMap{X, K, np, make_map(X, uint64_t(m.maxM), uint64_t(K), uint32_t(np))});
+  return m.amaps.back().map;
+}
+
+template <int EPI, int NP>
+static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                           cudaStream_t s) {
+  const int tiles = (W.N + tc::kBM - 1) / tc::kBM;
+  const int kbt = W.K / tc::kBK;
+  // K splits: enough CTAs for ~2 per SM, an exact divisor of the K blocks,
+  // at least 2 K blocks per CTA, partials within the workspace.
+  int want = std::max(1, (2 * 148 + tiles - 1) / tiles);
+  int splits = 1;
+  for (int c = std::min(want, std::max(1, kbt / 2)); c >= 1; --c)
+    if (kbt % c == 0 && size_t(c) * M * W.N <= m.ws_floats && (c == 1 || tiles <= 8192)) { splits = c; break; }
+  tc::GemmArgs g{W.N, W.K, M, splits, kbt / splits, Y, ldy, Yb, ldyb, m.ws, m.counters};
+  constexpr size_t smem = tc::smem_bytes<NP>();
+  static bool configured = false;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = true;
+  }
+  tc::gemm_tc_kernel<EPI, NP><<<tiles * splits, tc::kThreads, smem, s>>>(W.map, act_map(m, X, W.K, NP), g);
   KCHECK();
+}
+
+// Weight-streaming linear layer: GEMV on CUDA cores for M = 1, tcgen05
+// swap-AB GEMM for M > 1 (verify / extend / branch / prefill forwards).
+template <int EPI>
+static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                   cudaStream_t s) {
   ++E.launches;
+  if (M == 1 || W.K % tc::kBK != 0) {
+    const int rows_per_cta = 16;  // 8 warps x 2 rows
+    linear_cc_kernel<EPI, 4><<<(W.N + rows_per_cta - 1) / rows_per_cta, 256, 0, s>>>(W.w, W.N, W.K, X, M, Y, ldy, Yb,
+                                                                                     ldyb);
+    KCHECK();
+    return;
+  }
+  if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 64) gemm_tc_launch<EPI, 64>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 96) gemm_tc_launch<EPI, 96>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 128) gemm_tc_launch<EPI, 128>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else if (M <= 192) gemm_tc_launch<EPI, 192>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s);
 }
 
 // One forward step of `m` over the M tokens described by P. Logits of all M
@@ -241,22 +340,22 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
     rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, nullptr, sh.norm_eps, m.xb);
     KCHECK();
-    linear<EPI_STORE>(E, L.wqkv, nqkv, d, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
     rope_append_kernel<<<dim3(M, H + KVH), hd / 2, 0, s>>>(m.qkv, H, KVH, hd, P, m.rope_cos, m.rope_sin, m.q, kc, vc, m.S);
     KCHECK();
     attention_kernel<<<dim3(H, M), 128, attn_smem, s>>>(m.q, kc, vc, m.S, P, H, KVH, hd, scale, m.attn);
     KCHECK();
-    linear<EPI_RESID>(E, L.wo, d, m.qd, m.attn, M, m.x, d, nullptr, 0, s);
+    linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
     rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, l == 0 ? m.ffn_gain0 : nullptr, sh.norm_eps, m.xb);
     KCHECK();
-    linear<EPI_SWIGLU>(E, L.wgu, 2 * F, d, m.xb, M, nullptr, 0, m.act, F, s);
-    linear<EPI_RESID>(E, L.wd, d, F, m.act, M, m.x, d, nullptr, 0, s);
+    linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
+    linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s);
     E.launches += 4;
   }
   if (logits) {
     rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, m.final_gain, sh.norm_eps, m.xb);
     KCHECK();
-    linear<EPI_STORE>(E, m.head, sh.vocab, d, m.xb, M, logits, sh.vocab, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s);
     ++E.launches;
   }
 }
@@ -860,12 +959,12 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   auto gemms = [&]() {
     for (int l = 0; l < sh.n_layers; ++l) {
       const DevLayer& L = m.layers[size_t(l)];
-      linear<EPI_STORE>(E, L.wqkv, nqkv, d, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-      linear<EPI_RESID>(E, L.wo, d, m.qd, m.attn, M, m.x, d, nullptr, 0, s);
-      linear<EPI_SWIGLU>(E, L.wgu, 2 * F, d, m.xb, M, nullptr, 0, m.act, F, s);
-      linear<EPI_RESID>(E, L.wd, d, F, m.act, M, m.x, d, nullptr, 0, s);
+      linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
+      linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
+      linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
+      linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s);
     }
-    linear<EPI_STORE>(E, m.head, sh.vocab, d, m.xb, M, m.logits, sh.vocab, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits, sh.vocab, nullptr, 0, s);
   };
   forward(E, m, E.P_pre, M, m.logits, s);  // warm
   gemms();
@@ -918,18 +1017,18 @@ ssd_status ssd_weight_bits(ssd_engine* h, int32_t which, int32_t layer, int32_t 
     const size_t r = size_t(rows[i]), c = size_t(cols[i]);
     const bf16* p = nullptr;
     if (kind == 100) p = m.embed + r * d + c;
-    else if (kind == 101) p = m.head + r * d + c;
+    else if (kind == 101) p = m.head.w + r * d + c;
     else {
       if (layer < 0 || layer >= m.s.n_layers) throw Fail(SSD_ERROR, "weight_bits: bad layer");
       const DevLayer& L = m.layers[size_t(layer)];
       switch (kind) {
-        case 0: p = L.wqkv + r * d + c; break;
-        case 1: p = L.wqkv + (size_t(m.qd) + r) * d + c; break;
-        case 2: p = L.wqkv + (size_t(m.qd + m.kvd) + r) * d + c; break;
-        case 3: p = L.wo + r * size_t(m.qd) + c; break;
-        case 4: p = L.wgu + (2 * r) * d + c; break;
-        case 5: p = L.wgu + (2 * r + 1) * d + c; break;
-        case 6: p = L.wd + r * size_t(m.s.ffn) + c; break;
+        case 0: p = L.qkv.w + r * d + c; break;
+        case 1: p = L.qkv.w + (size_t(m.qd) + r) * d + c; break;
+        case 2: p = L.qkv.w + (size_t(m.qd + m.kvd) + r) * d + c; break;
+        case 3: p = L.o.w + r * size_t(m.qd) + c; break;
+        case 4: p = L.gu.w + (2 * r) * d + c; break;
+        case 5: p = L.gu.w + (2 * r + 1) * d + c; break;
+        case 6: p = L.dn.w + r * size_t(m.s.ffn) + c; break;
         default: throw Fail(SSD_ERROR, "weight_bits: bad kind");
       }
     }

@@ -161,13 +161,29 @@ def test_run_ar_greedy_matches_oracle(tiny):
     _assert_streams_match_or_near_tie(P, orc, prompt, g.streams[0], o["streams"][0])
 
 
+CDF_TOL = 5e-3  # CDF shift allowed by the |logit| < 1e-2 noise
+
+
 def test_run_ar_sampled_matches_oracle(tiny):
+    """Same mt19937_64 uniforms on both sides: the streams agree until a
+    uniform lands where logit noise can move the inverse-CDF boundary; such a
+    divergence must sit within CDF_TOL of the oracle's CDF."""
     P, eng, orc = tiny
     prompt = _prompt(16, seed=6)
     g = eng.run_ar(prompt, P.SamplingScheme.standard(1.0), 32, seed=10)
     o = orc.call({"op": "simulate", "mode": "ar", "lookahead": 1, "rounds": 32, "seed": 10, "prompt": prompt,
                   "scheme": {"temperature": 1.0}})
-    assert g.streams[0] == o["streams"][0]
+    gs, os_ = g.streams[0], o["streams"][0]
+    i = _first_divergence(gs, os_)
+    if i is None:
+        return
+    assert i >= 1, "sampled streams diverge at the first token"
+    z = orc.logits(0, list(prompt) + list(gs[:i])).astype(np.float64)
+    p = np.exp(z - z.max())
+    p /= p.sum()
+    cdf = np.concatenate([[0.0], np.cumsum(p)])
+    a, b = sorted((gs[i], os_[i]))
+    assert cdf[b] - cdf[a + 1] < CDF_TOL, (i, gs[i], os_[i], cdf[b] - cdf[a + 1])
 
 
 def _sim_req(prompt, mode, K, rounds, seed, temperature, fan, backup="fast_random"):
@@ -192,8 +208,46 @@ def test_run_sd_matches_oracle(tiny, temperature):
     if temperature == 0.0:
         _assert_streams_match_or_near_tie(P, orc, prompt, g.streams[0], o["streams"][0])
     else:
-        assert g.streams[0] == o["streams"][0]
-        assert g.accepted_sum == o["accepted_sum"]
+        # same uniforms, but logit noise can move a sampling boundary at any
+        # draw: exactness is asserted at kernel level on identical rows
+        # (test_verify_decision_matches_oracle), loop statistics below
+        assert len(g.streams[0]) == g.tokens and g.rounds == R
+        assert all(0 <= t < eng.vocab for t in g.streams[0])
+
+
+def _binom_close(k1, n1, k2, n2, z=4.0):
+    p = (k1 + k2) / (n1 + n2)
+    sd = np.sqrt(max(p * (1 - p), 1e-12) * (1 / n1 + 1 / n2))
+    return abs(k1 / n1 - k2 / n2) <= z * sd + 1e-9
+
+
+@pytest.mark.parametrize("mode", ["sd", "harness"])
+def test_sampled_acceptance_and_hit_rate_statistically_match(tiny, mode):
+    """tau = 1.0 (BASELINE configs[2] style): the per-position acceptance rate
+    and the cache hit rate of the GPU loop match the oracle's within 4 sigma
+    (binomial) over independent prompts."""
+    P, eng, orc = tiny
+    K, R, fan = 4, 40, [4] * 5
+    acc_g = acc_o = rounds = 0
+    hit_g = hit_o = look_g = look_o = 0
+    for rep in range(3):
+        prompt = _prompt(12, seed=100 + rep)
+        cfg = _cfg(P, K, R, 500 + rep, 1.0, fan)
+        req = _sim_req(prompt, mode, K, R, 500 + rep, 1.0, fan)
+        g = eng.run_sd(prompt, cfg) if mode == "sd" else eng.run_ssd(prompt, cfg)
+        o = orc.call(req)
+        acc_g += g.accepted_sum
+        acc_o += o["accepted_sum"]
+        rounds += R
+        if mode == "harness":
+            hit_g += g.hits_total()
+            look_g += g.lookups()
+            hit_o += o["p_hits"] + o["b_hits"]
+            look_o += o["p_lookups"] + o["b_lookups"]
+    # accepted tokens out of K proposals per round
+    assert _binom_close(acc_g, rounds * K, acc_o, rounds * K), (acc_g, acc_o, rounds)
+    if mode == "harness":
+        assert _binom_close(hit_g, look_g, hit_o, look_o), (hit_g, look_g, hit_o, look_o)
 
 
 @pytest.mark.parametrize("temperature,backup", [(0.0, "fast_random"), (1.0, "fast_random"), (0.0, "same_primary_jit")])
@@ -215,9 +269,10 @@ def test_run_ssd_matches_oracle_harness(tiny, temperature, backup):
                              ("miss_rounds", "miss_rounds"), ("accepted_sum", "accepted_sum")):
             assert getattr(g, key_g) == o[key_o], key_g
         assert abs(g.virtual_time - o["vtime"]) < 1e-9
-    else:
-        assert temperature == 0.0
+    elif temperature == 0.0:
         _assert_streams_match_or_near_tie(P, orc, prompt, gs, os_)
+    else:  # sampled: statistics checked in test_sampled_acceptance_and_hit_rate...
+        assert g.tokens == len(gs) and g.rounds == R
 
 
 def test_build_cache_keys_and_entries_match_oracle(tiny):
@@ -245,3 +300,18 @@ def test_errors_map_to_reference_classes(tiny):
         P.geometric_fanout(0.8, 1.0, 4, 3)
     with pytest.raises(P.TooLargeError):
         eng.run_ar([1] * 10, P.SamplingScheme.greedy(), 5000, 0)
+
+
+@pytest.mark.parametrize("M", [2, 5, 20, 33, 100])
+def test_tcgen05_forward_matches_gemv_path(tiny, M):
+    """The tcgen05 swap-AB GEMM path (M > 1 forwards) against the CUDA-core
+    GEMV path (M = 1): logits of the last prefill position of a context of
+    length M (one M-token forward) vs the oracle."""
+    P, eng, orc = tiny
+    ctx = _prompt(M, seed=200 + M)
+    g = eng.logits(0, ctx)
+    o = orc.logits(0, ctx)
+    assert np.max(np.abs(g - o)) < LOGIT_TOL, np.max(np.abs(g - o))
+    g1 = eng.logits(1, ctx)
+    o1 = orc.logits(1, ctx)
+    assert np.max(np.abs(g1 - o1)) < LOGIT_TOL
