@@ -76,11 +76,29 @@ static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint
 }
 
 // ------------------------------------------------------------------ model
+// Pre-tiled weight matrix (gemm_tc.cuh): rows padded to a multiple of 128.
 struct WMat {
   bf16* w = nullptr;
   int N = 0, K = 0;
-  CUtensorMap map;
 };
+
+// Launch with programmatic dependent launch (PDL): the kernel may start
+// while its predecessor drains; it calls griddepcontrol.wait before reading
+// the predecessor's output (weights are prefetched before that).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, args...));
+}
 
 struct DevLayer {
   WMat qkv, o, gu, dn;
@@ -97,7 +115,8 @@ struct Model {
   int role = 0;  // 0 target, 1 draft
   int qd = 0, kvd = 0;
   bf16* embed = nullptr;
-  WMat head;             // head.w == embed when tied
+  int embed_tiled = 0;   // embed aliases the pre-tiled head (tied)
+  WMat head;
   float* final_gain = nullptr;
   float* ffn_gain0 = nullptr;
   std::vector<DevLayer> layers;
@@ -183,24 +202,28 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   const GenPair gp{pp.seed, pp.embed_scale, pp.shared_mlp_scale, pp.block_out_scale, pp.target_private_embed,
                    pp.target_private_head, pp.draft_gain_mix};
   auto own = [&](void* p) { m.owned.push_back(p); return p; };
+  auto padded = [](int N) { return size_t((N + tc::kBM - 1) / tc::kBM) * tc::kBM; };
   auto wmat = [&](WMat& w, int N, int K) {
+    if (K % tc::kBK) throw Fail(SSD_CONFIG, "engine: every GEMM K must be a multiple of 64");
     w.N = N;
     w.K = K;
-    if (!w.w) w.w = static_cast<bf16*>(own(dalloc<bf16>(size_t(N) * K)));
-    w.map = make_map(w.w, uint64_t(N), uint64_t(K), tc::kBM);
+    if (!w.w) w.w = static_cast<bf16*>(own(dalloc<bf16>(padded(N) * K)));
   };
-  // tables
-  m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
-  gen_table_kernel<<<148 * 8, 256>>>(m.embed, s.vocab, d, dr.d_model, gp, 0);
+  // tables: the LM head is pre-tiled for the GEMM; a tied table is both
+  m.head.N = s.vocab;
+  m.head.K = d;
+  m.head.w = static_cast<bf16*>(own(dalloc<bf16>(padded(s.vocab) * d)));
+  gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, s.tied ? 0 : 1, 1);
   KCHECK();
   if (s.tied) {
-    m.head.w = m.embed;
+    m.embed = m.head.w;
+    m.embed_tiled = 1;
   } else {
-    m.head.w = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
-    gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, 1);
+    m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
+    gen_table_kernel<<<148 * 8, 256>>>(m.embed, s.vocab, d, dr.d_model, gp, 0, 0);
     KCHECK();
+    m.embed_tiled = 0;
   }
-  wmat(m.head, s.vocab, d);
   // norm gains (host, float arithmetic identical to the oracle)
   std::vector<float> fg(static_cast<size_t>(d)), g0(static_cast<size_t>(d), 1.0f);
   const uint64_t kGS = derive_seed(pp.seed, 0xE0000004u), kGN = derive_seed(pp.seed, 0xE0000005u),
@@ -264,6 +287,8 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   m.counters = static_cast<int*>(own(dalloc<int>(8192)));
 }
 
+static int E_num_sms = 148;
+
 static void free_model(Model& m) {
   for (void* p : m.owned) cudaFree(p);
   m.owned.clear();
@@ -280,38 +305,26 @@ static const CUtensorMap& act_map(Model& m, const void* X, int K, int np) {
 template <int EPI, int NP>
 static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                            cudaStream_t s) {
+  using C = tc::Cfg<NP>;
   const int tiles = (W.N + tc::kBM - 1) / tc::kBM;
-  const int kbt = W.K / tc::kBK;
-  // K splits: enough CTAs for ~2 per SM, an exact divisor of the K blocks,
-  // at least 2 K blocks per CTA, partials within the workspace.
-  int want = std::max(1, (2 * 148 + tiles - 1) / tiles);
-  int splits = 1;
-  for (int c = std::min(want, std::max(1, kbt / 2)); c >= 1; --c)
-    if (kbt % c == 0 && size_t(c) * M * W.N <= m.ws_floats && (c == 1 || tiles <= 8192)) { splits = c; break; }
-  tc::GemmArgs g{W.N, W.K, M, splits, kbt / splits, Y, ldy, Yb, ldyb, m.ws, m.counters};
-  constexpr size_t smem = tc::smem_bytes<NP>();
+  const int units = tiles * (W.K / tc::kBK);
+  const int grid = std::min(units, E_num_sms);
+  if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
+  tc::GemmArgs g{W.w, W.N, W.K / tc::kBK, M, Y, ldy, Yb, ldyb, m.ws, m.counters};
   static bool configured = false;
   if (!configured) {
-    CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
     configured = true;
   }
-  tc::gemm_tc_kernel<EPI, NP><<<tiles * splits, tc::kThreads, smem, s>>>(W.map, act_map(m, X, W.K, NP), g);
-  KCHECK();
+  launch_pdl(tc::gemm_tc_kernel<EPI, NP>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP), g);
 }
 
-// Weight-streaming linear layer: GEMV on CUDA cores for M = 1, tcgen05
-// swap-AB GEMM for M > 1 (verify / extend / branch / prefill forwards).
+// Weight-streaming linear layer: tcgen05 swap-AB stream-K GEMM for every M
+// (M = 1 decode steps pad the token operand to 16).
 template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                    cudaStream_t s) {
   ++E.launches;
-  if (M == 1 || W.K % tc::kBK != 0) {
-    const int rows_per_cta = 16;  // 8 warps x 2 rows
-    linear_cc_kernel<EPI, 4><<<(W.N + rows_per_cta - 1) / rows_per_cta, 256, 0, s>>>(W.w, W.N, W.K, X, M, Y, ldy, Yb,
-                                                                                     ldyb);
-    KCHECK();
-    return;
-  }
   if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s);
   else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s);
   else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s);
@@ -322,39 +335,42 @@ static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, flo
   else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s);
 }
 
+static size_t attn_smem_bytes(const Model& m, int maxK) {
+  const int G = m.s.n_heads / m.s.n_kv_heads;
+  const int nk = m.s.max_ctx + maxK + 2;
+  return size_t(G * m.s.head_dim + G * nk + 2 * kMaxGroup + kAttnThreads * G) * sizeof(float);
+}
+
 // One forward step of `m` over the M tokens described by P. Logits of all M
-// rows go to `logits` ([M][V]) when non-null.
+// rows go to `logits` ([M][V]) when non-null. Every kernel is launched with
+// PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, H = sh.n_heads, KVH = sh.n_kv_heads, hd = sh.head_dim, F = sh.ffn;
   const int nqkv = m.qd + 2 * m.kvd;
-  embed_kernel<<<M, 256, 0, s>>>(m.embed, d, P, m.x);
-  KCHECK();
+  launch_pdl(embed_kernel, dim3(M), dim3(256), 0, s, (const bf16*)m.embed, d, m.embed_tiled, P, m.x);
   ++E.launches;
   const float scale = 1.0f / std::sqrt(float(hd));
-  const size_t attn_smem = size_t(hd + sh.max_ctx + E.maxK + 2 + 128) * sizeof(float);
+  const size_t attn_smem = attn_smem_bytes(m, E.maxK);
   for (int l = 0; l < sh.n_layers; ++l) {
     const DevLayer& L = m.layers[size_t(l)];
     bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
-    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, nullptr, sh.norm_eps, m.xb);
-    KCHECK();
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)nullptr, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-    rope_append_kernel<<<dim3(M, H + KVH), hd / 2, 0, s>>>(m.qkv, H, KVH, hd, P, m.rope_cos, m.rope_sin, m.q, kc, vc, m.S);
-    KCHECK();
-    attention_kernel<<<dim3(H, M), 128, attn_smem, s>>>(m.q, kc, vc, m.S, P, H, KVH, hd, scale, m.attn);
-    KCHECK();
+    launch_pdl(attention_kernel, dim3(KVH, M), dim3(kAttnThreads), attn_smem, s, (const float*)m.qkv, P, M,
+               (const float*)m.rope_cos, (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn);
     linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
-    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, l == 0 ? m.ffn_gain0 : nullptr, sh.norm_eps, m.xb);
-    KCHECK();
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d,
+               (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
     linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
     linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s);
-    E.launches += 4;
+    E.launches += 3;
   }
   if (logits) {
-    rmsnorm_kernel<<<M, 256, 0, s>>>(m.x, d, m.final_gain, sh.norm_eps, m.xb);
-    KCHECK();
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)m.final_gain, sh.norm_eps,
+               m.xb);
     linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s);
     ++E.launches;
   }
@@ -588,9 +604,18 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   E.maxB = max_branches;
   E.maxK = max_lookahead;
   E.V = target->vocab;
+  {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    E_num_sms = sms;
+  }
   const int maxM = std::max(max_branches, max_lookahead + 1);
   build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
   build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
+  for (const ssd_model_shape* s : {target, draft})
+    if (s->n_heads / s->n_kv_heads > kMaxGroup) throw Fail(SSD_CONFIG, "engine: GQA group above 8");
+  CK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(std::max(attn_smem_bytes(E.T, max_lookahead), attn_smem_bytes(E.D, max_lookahead)))));
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
@@ -1016,19 +1041,20 @@ ssd_status ssd_weight_bits(ssd_engine* h, int32_t which, int32_t layer, int32_t 
   for (int i = 0; i < n; ++i) {
     const size_t r = size_t(rows[i]), c = size_t(cols[i]);
     const bf16* p = nullptr;
-    if (kind == 100) p = m.embed + r * d + c;
-    else if (kind == 101) p = m.head.w + r * d + c;
+    const size_t kd = d / 64, kq = size_t(m.qd) / 64, kf = size_t(m.s.ffn) / 64;
+    if (kind == 100) p = m.embed + (m.embed_tiled ? tiled_at(r, c, kd) : r * d + c);
+    else if (kind == 101) p = m.head.w + tiled_at(r, c, kd);
     else {
       if (layer < 0 || layer >= m.s.n_layers) throw Fail(SSD_ERROR, "weight_bits: bad layer");
       const DevLayer& L = m.layers[size_t(layer)];
       switch (kind) {
-        case 0: p = L.qkv.w + r * d + c; break;
-        case 1: p = L.qkv.w + (size_t(m.qd) + r) * d + c; break;
-        case 2: p = L.qkv.w + (size_t(m.qd + m.kvd) + r) * d + c; break;
-        case 3: p = L.o.w + r * size_t(m.qd) + c; break;
-        case 4: p = L.gu.w + (2 * r) * d + c; break;
-        case 5: p = L.gu.w + (2 * r + 1) * d + c; break;
-        case 6: p = L.dn.w + r * size_t(m.s.ffn) + c; break;
+        case 0: p = L.qkv.w + tiled_at(r, c, kd); break;
+        case 1: p = L.qkv.w + tiled_at(size_t(m.qd) + r, c, kd); break;
+        case 2: p = L.qkv.w + tiled_at(size_t(m.qd + m.kvd) + r, c, kd); break;
+        case 3: p = L.o.w + tiled_at(r, c, kq); break;
+        case 4: p = L.gu.w + tiled_at(2 * r, c, kd); break;
+        case 5: p = L.gu.w + tiled_at(2 * r + 1, c, kd); break;
+        case 6: p = L.dn.w + tiled_at(r, c, kf); break;
         default: throw Fail(SSD_ERROR, "weight_bits: bad kind");
       }
     }

@@ -1,15 +1,22 @@
-// tcgen05 weight-streaming GEMM for the small-M forwards of the Saguaro loop:
-// the (K+1)-token verify / extend forwards and the M = B branch steps of
-// pre-speculation. Swap-AB: the weight tile is the
-// M = 128 operand (A, K-major), the M tokens are the N operand (B, K-major,
-// padded to a multiple of 16); D = W_tile · X^T accumulates in TMEM.
+// tcgen05 weight-streaming GEMM for every linear layer of the decode step
+// (SURVEY §2.3 K1/K2/K3): Y[m][n] (+)= sum_k W[n][k] X[m][k] for M = 1..256
+// tokens. Swap-AB: the weight tile is the M = 128 operand (A, K-major), the
+// tokens are the N operand (B, K-major, padded to NP, a multiple of 16);
+// D = W_tile · X^T accumulates in TMEM.
 //
-// One CTA = one 128-row weight tile x one K split. Warp 0 / lane 0 streams
-// A and B stages with TMA (SWIZZLE_128B) into a 6-deep mbarrier ring; warp 1
-// / lane 0 issues tcgen05.mma; all four warps then drain TMEM (tcgen05.ld,
-// lane i = weight row i) and either apply the epilogue (store / residual add
-// / SwiGLU) or, with split-K, write fp32 partials that the last-arriving CTA
-// of the tile reduces in a fixed order (deterministic).
+// Weights live pre-tiled in HBM: block (tile t, k-block kb)
+// is one contiguous 16 KB run holding the 128 x 64 bf16 tile already in the
+// SWIZZLE_128B K-major order of the UMMA descriptor, so a single 1-D bulk
+// copy (cp.async.bulk) streams it at full DRAM efficiency.
+//
+// Persistent stream-K: the tiles x k-blocks work units are split into
+// gridDim.x contiguous ranges (one CTA per SM); a range crosses tile
+// boundaries, so every SM streams the same number of bytes. Warp 0 / lane 0
+// is the producer (weights before griddepcontrol.wait: they do not depend on
+// the previous kernel — PDL overlaps the weight stream with its tail),
+// warp 1 / lane 0 issues tcgen05.mma into a double-buffered TMEM
+// accumulator, warps 2-5 drain TMEM and apply the epilogue. A tile split
+// between CTAs is reduced by its last-arriving segment in a fixed order.
 #pragma once
 
 #include <cuda.h>
@@ -20,10 +27,17 @@ namespace ssd {
 namespace tc {
 
 constexpr int kBM = 128;        // weight rows per tile (UMMA M)
-constexpr int kBK = 64;         // K per stage: one 128-byte swizzle atom of bf16
-constexpr int kStages = 6;
-constexpr int kThreads = 128;
+constexpr int kBK = 64;         // K per block: one 128-byte swizzle atom of bf16
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+constexpr int kThreads = 192;   // 6 warps
+constexpr int kSmemBudget = 96 * 1024;
+
+// Element (r, c) of a [N][K] matrix in the pre-tiled layout (KB = K / 64).
+__host__ __device__ __forceinline__ size_t tiled_index(size_t r, size_t c, size_t KB) {
+  const size_t t = r >> 7, rr = r & 127, kb = c >> 6, cc = c & 63;
+  const size_t chunk = (cc >> 3) ^ (rr & 7);
+  return ((t * KB + kb) * 128 + rr) * 64 + chunk * 8 + (cc & 7);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
@@ -32,6 +46,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -43,14 +60,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            uint64_t policy) {
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// PDL (programmatic dependent launch)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // sm100 shared-memory matrix descriptor, K-major SWIZZLE_128B (CUTLASS
 // UMMA::SmemDescriptor): start>>4 | LBO 1 | SBO 1024B>>4 | version 1 | layout 2.
@@ -82,31 +110,26 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-  uint32_t r[8];
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 struct GemmArgs {
-  int N;        // weight rows
-  int K;        // reduction length
-  int M;        // tokens (valid columns)
-  int splits;   // K splits
-  int kb_per;   // 64-wide K blocks per split
-  float* Y;     // EPI_STORE / EPI_RESID output [M][ldy]
+  const bf16* W;  // pre-tiled weights
+  int N;          // weight rows (logical)
+  int KB;         // K / 64
+  int M;          // tokens (valid columns)
+  float* Y;       // EPI_STORE / EPI_RESID output [M][ldy]
   int ldy;
-  bf16* Yb;     // EPI_SWIGLU output [M][ldyb]
+  bf16* Yb;       // EPI_SWIGLU output [M][ldyb]
   int ldyb;
-  float* ws;    // split-K partials [splits][M][N]
+  float* ws;      // partials [2 * gridDim][M][128]
   int* counters;  // per-tile arrival counters (zeroed, self-resetting)
 };
 
-template <int EPI, int NP>
+template <int EPI>
 __device__ __forceinline__ void apply_epi(const GemmArgs& g, int row, int tok, float v) {
   if (EPI == EPI_SWIGLU) {
     const float up = __shfl_xor_sync(0xffffffffu, v, 1);
@@ -121,119 +144,171 @@ __device__ __forceinline__ void apply_epi(const GemmArgs& g, int row, int tok, f
   }
 }
 
-// NP: padded token count (UMMA N), multiple of 16 in [16, 256].
+// Unit range of CTA i: [i*U/P, (i+1)*U/P).
+__device__ __forceinline__ int unit_begin(long long i, long long U, long long P) { return int(i * U / P); }
+// CTA owning unit u.
+__device__ __forceinline__ int cta_of(int u, long long U, long long P) {
+  long long i = ((long long)u * P) / U;
+  while (i + 1 < P && unit_begin(i + 1, U, P) <= u) ++i;
+  while (i > 0 && unit_begin(i, U, P) > u) --i;
+  return int(i);
+}
+
+template <int NP>
+struct Cfg {
+  static constexpr int kBBytes = NP * kBK * 2;
+  static constexpr int kStages = (kSmemBudget / (kABytes + kBBytes)) < 2 ? 2
+                                 : ((kSmemBudget / (kABytes + kBBytes)) > 8 ? 8 : kSmemBudget / (kABytes + kBBytes));
+  static constexpr int kAccCols = NP < 32 ? 32 : NP;
+  static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * (kABytes + kBBytes) + 256;
+};
+
 template <int EPI, int NP>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap mapW,
-                                                              const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
-  constexpr int kBBytes = NP * kBK * 2;
-  constexpr int kTmemCols = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
+  using C = Cfg<NP>;
+  constexpr int S = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* accf = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint8_t* sB = smem + S * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * C::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (g.N + kBM - 1) / kBM;
-  const int tile = blockIdx.x % tiles, split = blockIdx.x / tiles;
-  const int row0 = tile * kBM;
-  const int kb0 = split * g.kb_per;
+  const long long U = (long long)tiles * g.KB, P = gridDim.x;
+  const int u0 = unit_begin(blockIdx.x, U, P), u1 = unit_begin(blockIdx.x + 1, U, P);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(accf, 1);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
+                 "r"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_launch();  // let the next kernel start its own prologue / weight prefetch
 
   if (warp == 0 && lane == 0) {
-    // TMA producer: weights are streamed once (evict-first), activations
-    // are re-read by every tile (evict-last).
-    uint64_t pol_w, pol_x;
+    // ---------------- producer
+    uint64_t pol_w;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_x));
-    for (int i = 0; i < g.kb_per; ++i) {
-      const int s = i % kStages;
-      if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-      mbar_expect_tx(&full[s], kABytes + kBBytes);
-      const int kc = (kb0 + i) * kBK;
-      tma_load_2d(sA + s * kABytes, &mapW, &full[s], kc, row0, pol_w);
-      tma_load_2d(sB + s * kBBytes, &mapX, &full[s], kc, 0, pol_x);
+    const int n = u1 - u0;
+    const int pre = n < S ? n : S;
+    for (int i = 0; i < pre; ++i) {  // weights only: independent of the previous kernel
+      const int u = u0 + i;
+      mbar_expect_tx(&full[i], kABytes + C::kBBytes);
+      bulk_load(sA + i * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[i], pol_w);
+    }
+    pdl_wait();  // activations are produced by the previous kernel
+    for (int i = 0; i < pre; ++i) {
+      const int u = u0 + i;
+      tma_load_2d(sB + i * C::kBBytes, &mapX, &full[i], (u % g.KB) * kBK, 0);
+    }
+    for (int i = pre; i < n; ++i) {
+      const int s = i % S;
+      mbar_wait(&empty[s], ((i / S) - 1) & 1);
+      const int u = u0 + i;
+      mbar_expect_tx(&full[s], kABytes + C::kBBytes);
+      bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
+      tma_load_2d(sB + s * C::kBBytes, &mapX, &full[s], (u % g.KB) * kBK, 0);
     }
   } else if (warp == 1 && lane == 0) {
-    // MMA issuer
+    // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
-    for (int i = 0; i < g.kb_per; ++i) {
-      const int s = i % kStages;
-      mbar_wait(&full[s], (i / kStages) & 1);
+    int seg = -1, cur_tile = -1;
+    for (int i = 0; i < u1 - u0; ++i) {
+      const int u = u0 + i, t = u / g.KB, s = i % S;
+      const bool first = t != cur_tile;
+      if (first) {
+        ++seg;
+        cur_tile = t;
+        if (seg >= 2) mbar_wait(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
+      }
+      mbar_wait(&full[s], (i / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+      const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * C::kBBytes);
+      const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
 #pragma unroll
       for (int k = 0; k < kBK / 16; ++k)
-        mma_bf16(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (i | k) ? 1u : 0u);
+        mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (!first || k) ? 1u : 0u);
       mma_commit(&empty[s]);
+      const bool last = (u + 1 == u1) || ((u + 1) / g.KB != t);
+      if (last) mma_commit(&tfull[seg & 1]);
     }
-    mma_commit(accf);
-  }
-  __syncwarp();
-  mbar_wait(accf, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  const int r = row0 + threadIdx.x;  // TMEM lane == weight row within the tile
-  const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16);
-  if (g.splits == 1) {
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 + lane
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    int seg = -1;
+    int u = u0;
+    while (u < u1) {
+      const int t = u / g.KB;
+      const int kb_lo = u % g.KB;
+      const int seg_end = min(u1, (t + 1) * g.KB);
+      const bool whole = kb_lo == 0 && seg_end == (t + 1) * g.KB;
+      ++seg;
+      const int b = seg & 1;
+      mbar_wait(&tfull[b], (seg >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(b * C::kAccCols);
+      const int r = t * kBM + rl;
+      // partial slot: first segment of this CTA -> 2*cta, later -> 2*cta+1
+      float* part = g.ws + (size_t(2 * blockIdx.x + (u == u0 ? 0 : 1)) * g.M) * kBM;
 #pragma unroll 1
-    for (int c = 0; c < NP; c += 8) {
-      float v[8];
-      tmem_ld8(taddr + c, v);
+      for (int c = 0; c < NP; c += 8) {
+        uint32_t v[8];
+        tmem_ld8(taddr + c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + 8 >= NP) {  // accumulator drained: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) apply_epi<EPI, NP>(g, r, c + j, v[j]);
-    }
-  } else {
-    float* part = g.ws + size_t(split) * g.M * g.N;
-#pragma unroll 1
-    for (int c = 0; c < NP; c += 8) {
-      float v[8];
-      tmem_ld8(taddr + c, v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (c + j < g.M && r < g.N) part[size_t(c + j) * g.N + r] = v[j];
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&g.counters[tile], 1) == g.splits - 1;
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      for (int t = 0; t < g.M; ++t) {
-        float acc = 0.f;
-        if (r < g.N)
-          for (int sp = 0; sp < g.splits; ++sp) acc += __ldcg(g.ws + (size_t(sp) * g.M + t) * g.N + r);
-        apply_epi<EPI, NP>(g, r, t, acc);
+        for (int j = 0; j < 8; ++j) {
+          const float f = __uint_as_float(v[j]);
+          if (whole) apply_epi<EPI>(g, r, c + j, f);
+          else if (c + j < g.M) part[size_t(c + j) * kBM + rl] = f;
+        }
       }
-      if (threadIdx.x == 0) g.counters[tile] = 0;
+      if (!whole) {
+        // last-arriving segment of tile t reduces the partials in CTA order
+        const int cf = cta_of(t * g.KB, U, P), cl = cta_of((t + 1) * g.KB - 1, U, P);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) s_last = atomicAdd(&g.counters[t], 1) == (cl - cf);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          for (int tok = 0; tok < g.M; ++tok) {
+            float acc = 0.f;
+            for (int c2 = cf; c2 <= cl; ++c2) {
+              const int slot = 2 * c2 + (unit_begin(c2, U, P) >= t * g.KB ? 0 : 1);
+              acc += __ldcg(g.ws + (size_t(slot) * g.M + tok) * kBM + rl);
+            }
+            apply_epi<EPI>(g, r, tok, acc);
+          }
+          if (threadIdx.x == 64) g.counters[t] = 0;
+        }
+      }
+      u = seg_end;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-}
-
-template <int NP>
-constexpr size_t smem_bytes() {
-  return 1024 + size_t(kStages) * (kABytes + NP * kBK * 2) + (2 * kStages + 1) * 8 + 16;
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
 }
 
 }  // namespace tc

@@ -95,20 +95,30 @@ __device__ inline bf16 layer_elem(const GenShape& self, const GenShape& dr, cons
   return __float2bfloat16_rn(unit_value(key, r * in + c) * scale);
 }
 
-// Fill device rows [row_off + row_stride * r] of dst (row length cols) with
-// logical tensor (role, layer, kind) rows [0, rows).
+// Element (r, c) of a [N][K] matrix in the pre-tiled GEMM layout
+// (gemm_tc.cuh): 128 x 64 tiles, each a contiguous 16 KB run in the
+// SWIZZLE_128B K-major order, tiles ordered (row tile, k block).
+__host__ __device__ __forceinline__ size_t tiled_at(size_t r, size_t c, size_t KB) {
+  const size_t t = r >> 7, rr = r & 127, kb = c >> 6, cc = c & 63;
+  const size_t chunk = (cc >> 3) ^ (rr & 7);
+  return ((t * KB + kb) * 128 + rr) * 64 + chunk * 8 + (cc & 7);
+}
+
+// Fill rows [row_off + row_stride * r] of the pre-tiled matrix dst (row
+// length cols) with logical tensor (role, layer, kind) rows [0, rows).
 __global__ void gen_layer_kernel(bf16* dst, int rows, int cols, int row_stride, int row_off, GenShape self,
                                  GenShape dr, GenPair p, int role, int layer, int kind) {
-  const size_t total = size_t(rows) * size_t(cols);
+  const size_t total = size_t(rows) * size_t(cols), KB = size_t(cols) / 64;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     const size_t r = e / size_t(cols), c = e % size_t(cols);
-    dst[(size_t(row_off) + size_t(row_stride) * r) * size_t(cols) + c] = layer_elem(self, dr, p, role, layer, kind, r, c);
+    dst[tiled_at(size_t(row_off) + size_t(row_stride) * r, c, KB)] = layer_elem(self, dr, p, role, layer, kind, r, c);
   }
 }
 
 // Embedding / LM head [V][d]: shared table S in dims [0, ds), target-private
-// tables beyond (oracle transformer_lm.cpp constructor).
-__global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int which /*0 embed 1 head*/) {
+// tables beyond (oracle transformer_lm.cpp constructor). `tiled` stores it in
+// the GEMM layout (LM heads, and the tied draft table that is both).
+__global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int which /*0 embed 1 head*/, int tiled) {
   const uint64_t kS = derive_seed(p.seed, 0xE0000001u), kPE = derive_seed(p.seed, 0xE0000002u),
                  kPH = derive_seed(p.seed, 0xE0000003u);
   const size_t total = size_t(V) * size_t(d), dp = size_t(d - ds);
@@ -121,203 +131,188 @@ __global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int
       const size_t j = v * dp + (i - size_t(ds));
       val = which == 0 ? unit_value(kPE, j) * p.priv_embed : unit_value(kPH, j) * p.priv_head;
     }
-    dst[e] = __float2bfloat16_rn(val);
+    dst[tiled ? tiled_at(v, i, size_t(d) / 64) : e] = __float2bfloat16_rn(val);
   }
 }
 
+__device__ __forceinline__ void pdl_wait_all() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ forward
-// x[m][:] = E[token_m][:] (fp32 residual stream)
-__global__ void embed_kernel(const bf16* __restrict__ E, int d, const FwdParams* __restrict__ P, float* __restrict__ x) {
+// x[m][:] = E[token_m][:] (fp32 residual stream); E row-major or pre-tiled.
+__global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const FwdParams* __restrict__ P,
+                             float* __restrict__ x) {
+  pdl_wait_all();
   const int m = blockIdx.x;
-  const bf16* row = E + size_t(P->tokens[m]) * size_t(d);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) x[size_t(m) * d + i] = __bfloat162float(row[i]);
+  const size_t tok = size_t(P->tokens[m]);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const size_t at = tiled ? tiled_at(tok, size_t(i), size_t(d) / 64) : tok * size_t(d) + size_t(i);
+    x[size_t(m) * d + i] = __bfloat162float(E[at]);
+  }
 }
 
 // RMSNorm (gain optional) with bf16 rounding of the output: the GEMM input
-// precision (oracle rmsnorm_bf16).
-__global__ void rmsnorm_kernel(const float* __restrict__ x, int d, const float* __restrict__ g, float eps,
-                               bf16* __restrict__ out) {
+// precision (oracle rmsnorm_bf16). One CTA per token, float4 loads.
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int d, const float* __restrict__ g,
+                                                      float eps, bf16* __restrict__ out) {
   __shared__ float sh[32];
+  pdl_wait_all();
+  asm volatile("griddepcontrol.launch_dependents;");
   const int m = blockIdx.x;
-  const float* xr = x + size_t(m) * d;
+  const float4* xr = reinterpret_cast<const float4*>(x + size_t(m) * d);
+  const int n4 = d >> 2;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
   ss = block_sum(ss, sh);
   const float r = 1.0f / sqrtf(ss / float(d) + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = xr[i] * r;
-    out[size_t(m) * d + i] = __float2bfloat16_rn(g ? v * g[i] : v);
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out + size_t(m) * d);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const float4 v = xr[i];
+    float a = v.x * r, b = v.y * r, c = v.z * r, e = v.w * r;
+    if (g) {
+      const float4 gg = reinterpret_cast<const float4*>(g)[i];
+      a *= gg.x; b *= gg.y; c *= gg.z; e *= gg.w;
+    }
+    o2[2 * i] = __floats2bfloat162_rn(a, b);
+    o2[2 * i + 1] = __floats2bfloat162_rn(c, e);
   }
 }
 
 enum Epi { EPI_STORE = 0, EPI_RESID = 1, EPI_SWIGLU = 2 };
 
-// Weight-streaming linear layer on CUDA cores: Y[m][r] (+)= sum_k W[r][k] X[m][k].
-// Each warp owns two weight rows and streams them once with 16-byte
-// non-allocating loads; tokens are processed MT at a time (re-reads of the
-// two rows for further token chunks hit L1/L2). Used for M = 1 decode steps.
-template <int EPI, int MT>
-__global__ void __launch_bounds__(256) linear_cc_kernel(const bf16* __restrict__ W, int N, int K,
-                                                        const bf16* __restrict__ X, int M, float* __restrict__ Y,
-                                                        int ldy, bf16* __restrict__ Yb, int ldyb) {
-  const int lane = threadIdx.x & 31;
-  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int r0 = warp * 2;
-  if (r0 >= N) return;
-  const bool has1 = r0 + 1 < N;
-  const uint4* w0 = reinterpret_cast<const uint4*>(W + size_t(r0) * K);
-  const uint4* w1 = reinterpret_cast<const uint4*>(W + size_t(has1 ? r0 + 1 : r0) * K);
-  const int nvec = K >> 3;
-  constexpr int U = 4;
-  for (int m0 = 0; m0 < M; m0 += MT) {
-    const int mt = min(MT, M - m0);
-    float a0[MT], a1[MT];
-#pragma unroll
-    for (int t = 0; t < MT; ++t) a0[t] = a1[t] = 0.f;
-    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
-      uint4 wa[U], wb[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + 32 * u;
-        if (v < nvec) { wa[u] = ldg_stream(w0 + v); wb[u] = ldg_stream(w1 + v); }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + 32 * u;
-        if (v < nvec) {
-          float fa[8], fb[8];
-          bf16x8_to_f32(wa[u], fa);
-          bf16x8_to_f32(wb[u], fb);
-#pragma unroll
-          for (int t = 0; t < MT; ++t) {
-            if (t < mt) {
-              const uint4 xv = __ldg(reinterpret_cast<const uint4*>(X + size_t(m0 + t) * K) + v);
-              float fx[8];
-              bf16x8_to_f32(xv, fx);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) { a0[t] += fa[i] * fx[i]; a1[t] += fb[i] * fx[i]; }
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < MT; ++t) {
-      if (t < mt) {
-        const float s0 = warp_sum(a0[t]), s1 = warp_sum(a1[t]);
-        if (lane == 0) {
-          const int m = m0 + t;
-          if (EPI == EPI_STORE) {
-            Y[size_t(m) * ldy + r0] = s0;
-            if (has1) Y[size_t(m) * ldy + r0 + 1] = s1;
-          } else if (EPI == EPI_RESID) {
-            Y[size_t(m) * ldy + r0] += s0;
-            if (has1) Y[size_t(m) * ldy + r0 + 1] += s1;
-          } else {  // SwiGLU: rows (2j, 2j+1) = (gate_j, up_j)
-            const float act = s0 / (1.0f + expf(-s0)) * s1;
-            Yb[size_t(m) * ldyb + (r0 >> 1)] = __float2bfloat16_rn(act);
-          }
-        }
-      }
-    }
-  }
-}
+// Decode attention for one (kv head, query token), fused with RoPE and the
+// KV-cache append of this forward's tokens. GQA: the G = H / KVH query heads
+// of the group share every K/V read. Keys are the main-cache prefix
+// [0, main_len) plus a branch-local segment [bbase, bbase + blen): the
+// tree/branch mask of pre-speculation, generated arithmetically instead of
+// materialised. grid (KVH, M), 256 threads; qkv rows are
+// [q: H*hd][k: KVH*hd][v: KVH*hd] (fp32, pre-RoPE).
+constexpr int kAttnThreads = 256;
+constexpr int kMaxGroup = 8;
 
-// RoPE (rotate-half pairs (i, i + hd/2)) on q and k, KV-cache append in bf16.
-// qkv row layout: [q: H*hd][k: KVH*hd][v: KVH*hd]. grid (M, H + KVH).
-__global__ void rope_append_kernel(const float* __restrict__ qkv, int H, int KVH, int hd, const FwdParams* __restrict__ P,
-                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t,
-                                   float* __restrict__ q_out, bf16* __restrict__ kc, bf16* __restrict__ vc, int S) {
-  const int m = blockIdx.x, hh = blockIdx.y, half = hd >> 1;
-  const int pos = P->pos[m], slot = P->slot[m];
-  const size_t row = size_t(m) * size_t((H + 2 * KVH) * hd);
-  const float* cs = cos_t + size_t(pos) * half;
-  const float* sn = sin_t + size_t(pos) * half;
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    if (hh < H) {
-      const float* src = qkv + row + size_t(hh) * hd;
-      const float a = src[i], b = src[i + half];
-      float* dst = q_out + size_t(m) * H * hd + size_t(hh) * hd;
-      dst[i] = a * cs[i] - b * sn[i];
-      dst[i + half] = b * cs[i] + a * sn[i];
-    } else {
-      const int kh = hh - H;
-      const float* ks = qkv + row + size_t(H) * hd + size_t(kh) * hd;
-      const float* vs = qkv + row + size_t(H + KVH) * hd + size_t(kh) * hd;
-      const float a = ks[i], b = ks[i + half];
-      bf16* kd = kc + (size_t(kh) * S + slot) * hd;
-      bf16* vd = vc + (size_t(kh) * S + slot) * hd;
-      kd[i] = __float2bfloat16_rn(a * cs[i] - b * sn[i]);
-      kd[i + half] = __float2bfloat16_rn(b * cs[i] + a * sn[i]);
-      vd[i] = __float2bfloat16_rn(vs[i]);
-      vd[i + half] = __float2bfloat16_rn(vs[i + half]);
-    }
-  }
-}
-
-// Decode attention over a main-cache prefix plus a branch-local segment
-// (the tree/branch mask of pre-speculation, generated arithmetically from
-// (main_len, bbase, blen) instead of materialised). grid (H, M), 128 threads.
-__global__ void __launch_bounds__(128) attention_kernel(const float* __restrict__ q, const bf16* __restrict__ kc,
-                                                        const bf16* __restrict__ vc, int S, const FwdParams* __restrict__ P,
-                                                        int H, int KVH, int hd, float scale, bf16* __restrict__ out) {
+__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __restrict__ qkv, const FwdParams* __restrict__ P,
+                                                                 int M, const float* __restrict__ cos_t,
+                                                                 const float* __restrict__ sin_t, bf16* __restrict__ kc,
+                                                                 bf16* __restrict__ vc, int S, int H, int KVH, int hd,
+                                                                 float scale, bf16* __restrict__ out) {
   extern __shared__ float smem[];
-  __shared__ float red[32];
-  const int h = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
-  const int kvh = h / (H / KVH);
+  pdl_wait_all();
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int kvh = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = kAttnThreads / 32;
+  const int G = H / KVH, half = hd >> 1;
+  const size_t row_len = size_t(H + 2 * KVH) * hd;
+  // 1) RoPE + append K/V of every token of this forward for this kv head
+  //    (identical values from all M CTAs of the head: each CTA sees its own
+  //    writes after the barrier, so no cross-CTA ordering is needed).
+  for (int e = tid; e < M * half; e += kAttnThreads) {
+    const int t = e / half, i = e % half;
+    const int pos = P->pos[t], slot = P->slot[t];
+    const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
+    const float* ks = qkv + size_t(t) * row_len + size_t(H + kvh) * hd;
+    const float* vs = qkv + size_t(t) * row_len + size_t(H + KVH + kvh) * hd;
+    const float a = ks[i], b = ks[i + half];
+    bf16* kd = kc + (size_t(kvh) * S + slot) * hd;
+    bf16* vd = vc + (size_t(kvh) * S + slot) * hd;
+    kd[i] = __float2bfloat16_rn(a * c - b * sn);
+    kd[i + half] = __float2bfloat16_rn(b * c + a * sn);
+    vd[i] = __float2bfloat16_rn(vs[i]);
+    vd[i + half] = __float2bfloat16_rn(vs[i + half]);
+  }
+  // 2) rotated queries of the group into shared memory
   const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
   const int nk = main_len + blen;
-  float* qs = smem;           // hd
-  float* sc = smem + hd;      // nk
-  float* part = sc + nk;      // blockDim
-  for (int i = tid; i < hd; i += blockDim.x) qs[i] = q[size_t(m) * H * hd + size_t(h) * hd + i];
+  float* qs = smem;                  // [G][hd]
+  float* sc = qs + G * hd;           // [G][nk]
+  float* red = sc + G * nk;          // [G][2]
+  float* part = red + 2 * kMaxGroup; // [kAttnThreads][G]
+  {
+    const int pos = P->pos[m];
+    for (int e = tid; e < G * half; e += kAttnThreads) {
+      const int gg = e / half, i = e % half;
+      const float* src = qkv + size_t(m) * row_len + size_t(kvh * G + gg) * hd;
+      const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
+      const float a = src[i], b = src[i + half];
+      qs[gg * hd + i] = a * c - b * sn;
+      qs[gg * hd + i + half] = b * c + a * sn;
+    }
+  }
   __syncthreads();
+  // 3) scores: one key per warp iteration, lanes over head dims
   const bf16* kbase = kc + size_t(kvh) * S * hd;
   const bf16* vbase = vc + size_t(kvh) * S * hd;
-  float mx = -INFINITY;
-  for (int j = tid; j < nk; j += blockDim.x) {
+  const int dpl = hd / 32;  // dims per lane: 2 or 4
+  float qr[kMaxGroup][4];
+  for (int gg = 0; gg < G; ++gg)
+    for (int i = 0; i < dpl; ++i) qr[gg][i] = qs[gg * hd + lane * dpl + i];
+  for (int j = warp; j < nk; j += nwarps) {
     const int slot = j < main_len ? j : bbase + (j - main_len);
-    const uint4* kr = reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
-    float dot = 0.f;
-    for (int c = 0; c < (hd >> 3); ++c) {
-      float f[8];
-      bf16x8_to_f32(kr[c], f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dot += qs[c * 8 + i] * f[i];
+    const bf16* kr = kbase + size_t(slot) * hd + lane * dpl;
+    float kf[4];
+    if (dpl == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(kr);
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      kf[0] = f0.x; kf[1] = f0.y; kf[2] = f1.x; kf[3] = f1.y;
+    } else {
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr));
+      kf[0] = f0.x; kf[1] = f0.y; kf[2] = 0.f; kf[3] = 0.f;
     }
-    const float s = dot * scale;
-    sc[j] = s;
-    mx = fmaxf(mx, s);
+    for (int gg = 0; gg < G; ++gg) {
+      float dot = 0.f;
+      for (int i = 0; i < dpl; ++i) dot += qr[gg][i] * kf[i];
+      dot = warp_sum(dot);
+      if (lane == 0) sc[gg * nk + j] = dot * scale;
+    }
   }
-  mx = warp_max(mx);
   __syncthreads();
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
-  __syncthreads();
-  mx = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
-  float den = 0.f;
-  for (int j = tid; j < nk; j += blockDim.x) {
-    const float e = expf(sc[j] - mx);
-    sc[j] = e;
-    den += e;
+  // 4) softmax per head (warp gg handles head gg)
+  for (int gg = warp; gg < G; gg += nwarps) {
+    float mx = -INFINITY;
+    for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, sc[gg * nk + j]);
+    mx = warp_max(mx);
+    float den = 0.f;
+    for (int j = lane; j < nk; j += 32) {
+      const float e = expf(sc[gg * nk + j] - mx);
+      sc[gg * nk + j] = e;
+      den += e;
+    }
+    den = warp_sum(den);
+    if (lane == 0) red[gg] = den;
   }
-  den = block_sum(den, red);
   __syncthreads();
-  const int parts = blockDim.x / hd;  // hd in {64, 128}
+  // 5) P.V: thread = (dim, key slice); every V element feeds all G heads
+  const int parts = kAttnThreads / hd;
   const int dd = tid % hd, pp = tid / hd;
-  float acc = 0.f;
-  if (pp < parts) {
-    for (int j = pp; j < nk; j += parts) {
-      const int slot = j < main_len ? j : bbase + (j - main_len);
-      acc += sc[j] * __bfloat162float(vbase[size_t(slot) * hd + dd]);
+  float acc[kMaxGroup];
+  for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
+  int j = pp;
+  for (; j + 3 * parts < nk; j += 4 * parts) {
+    float vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jj = j + u * parts;
+      const int slot = jj < main_len ? jj : bbase + (jj - main_len);
+      vv[u] = __bfloat162float(vbase[size_t(slot) * hd + dd]);
     }
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[gg] += sc[gg * nk + j + u * parts] * vv[u];
   }
-  part[tid] = acc;
+  for (; j < nk; j += parts) {
+    const int slot = j < main_len ? j : bbase + (j - main_len);
+    const float v = __bfloat162float(vbase[size_t(slot) * hd + dd]);
+    for (int gg = 0; gg < G; ++gg) acc[gg] += sc[gg * nk + j] * v;
+  }
+  for (int gg = 0; gg < G; ++gg) part[tid * G + gg] = acc[gg];
   __syncthreads();
-  if (tid < hd) {
+  for (int e = tid; e < G * hd; e += kAttnThreads) {
+    const int gg = e / hd, d2 = e % hd;
     float o = 0.f;
-    for (int p2 = 0; p2 < parts; ++p2) o += part[p2 * hd + tid];
-    out[size_t(m) * H * hd + size_t(h) * hd + tid] = __float2bfloat16_rn(o / den);
+    for (int p2 = 0; p2 < parts; ++p2) o += part[(p2 * hd + d2) * G + gg];
+    out[size_t(m) * H * hd + size_t(kvh * G + gg) * hd + d2] = __float2bfloat16_rn(o / red[gg]);
   }
 }
 
