@@ -614,8 +614,12 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup) throw Fail(SSD_CONFIG, "engine: GQA group above 8");
-  CK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(std::max(attn_smem_bytes(E.T, max_lookahead), attn_smem_bytes(E.D, max_lookahead)))));
+  {
+    // the attribute is per function, shared by every engine in the process
+    static size_t attn_smem_max = 0;
+    attn_smem_max = std::max({attn_smem_max, attn_smem_bytes(E.T, max_lookahead), attn_smem_bytes(E.D, max_lookahead)});
+    CK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_smem_max)));
+  }
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));

@@ -30,7 +30,9 @@ constexpr int kBM = 128;        // weight rows per tile (UMMA M)
 constexpr int kBK = 64;         // K per block: one 128-byte swizzle atom of bf16
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kThreads = 192;   // 6 warps
-constexpr int kSmemBudget = 96 * 1024;
+// ~200 KB of stages: one CTA per SM keeps ~180 KB of weights in flight,
+// enough to cover the loaded HBM latency at 1/148 of the chip bandwidth.
+constexpr int kSmemBudget = 200 * 1024;
 
 // Element (r, c) of a [N][K] matrix in the pre-tiled layout (KB = K / 64).
 __host__ __device__ __forceinline__ size_t tiled_index(size_t r, size_t c, size_t KB) {
@@ -158,7 +160,7 @@ template <int NP>
 struct Cfg {
   static constexpr int kBBytes = NP * kBK * 2;
   static constexpr int kStages = (kSmemBudget / (kABytes + kBBytes)) < 2 ? 2
-                                 : ((kSmemBudget / (kABytes + kBBytes)) > 8 ? 8 : kSmemBudget / (kABytes + kBBytes));
+                                 : ((kSmemBudget / (kABytes + kBBytes)) > 12 ? 12 : kSmemBudget / (kABytes + kBBytes));
   static constexpr int kAccCols = NP < 32 ? 32 : NP;
   static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
   static constexpr size_t kSmem = 1024 + size_t(kStages) * (kABytes + kBBytes) + 256;
@@ -292,13 +294,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (s_last) {
           __threadfence();
-          for (int tok = 0; tok < g.M; ++tok) {
-            float acc = 0.f;
+          // only the first contributing CTA can start before the tile
+          const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KB ? 0 : 1);
+          for (int t0 = 0; t0 < g.M; t0 += 8) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
             for (int c2 = cf; c2 <= cl; ++c2) {
-              const int slot = 2 * c2 + (unit_begin(c2, U, P) >= t * g.KB ? 0 : 1);
-              acc += __ldcg(g.ws + (size_t(slot) * g.M + tok) * kBM + rl);
+              const int slot = c2 == cf ? first_slot : 2 * c2;
+              const float* src = g.ws + (size_t(slot) * g.M) * kBM + rl;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (t0 + j < g.M) acc[j] += __ldcg(src + size_t(t0 + j) * kBM);
             }
-            apply_epi<EPI>(g, r, tok, acc);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) apply_epi<EPI>(g, r, t0 + j, acc[j]);
           }
           if (threadIdx.x == 64) g.counters[t] = 0;
         }
