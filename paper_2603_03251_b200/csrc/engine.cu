@@ -126,6 +126,10 @@ struct Model {
   float* rope_cos = nullptr;
   float* rope_sin = nullptr;
   int maxM = 0;
+  int ctx_bound = 0;     // host-known bound on keys per query (attention grid)
+  int branch_len = 0;
+  float* attn_part = nullptr;
+  int* attn_cnt = nullptr;
   float *x = nullptr, *qkv = nullptr, *q = nullptr, *logits = nullptr;
   bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
   int64_t weight_bytes = 0;
@@ -285,6 +289,15 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   m.ws_floats = size_t(16) << 20;  // 64 MB of split-K partials
   m.ws = static_cast<float*>(own(dalloc<float>(m.ws_floats)));
   m.counters = static_cast<int*>(own(dalloc<int>(8192)));
+  // split attention partials: [maxM][KVH][chunks][G][hd + 2]
+  m.branch_len = branch_slots;
+  m.ctx_bound = s.max_ctx;
+  {
+    const int G = s.n_heads / s.n_kv_heads;
+    const int chunks = (s.max_ctx + branch_slots + kAttnChunk) / kAttnChunk + 1;
+    m.attn_part = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.n_kv_heads * chunks * G * (hd + 2))));
+    m.attn_cnt = static_cast<int*>(own(dalloc<int>(size_t(maxM) * s.n_kv_heads)));
+  }
 }
 
 static int E_num_sms = 148;
@@ -335,10 +348,10 @@ static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, flo
   else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s);
 }
 
-static size_t attn_smem_bytes(const Model& m, int maxK) {
-  const int G = m.s.n_heads / m.s.n_kv_heads;
-  const int nk = m.s.max_ctx + maxK + 2;
-  return size_t(G * m.s.head_dim + G * nk + 2 * kMaxGroup + kAttnThreads * G) * sizeof(float);
+// Key chunks of the split attention for the current context bound.
+static int attn_chunks(const Model& m) {
+  const int nk = std::min(m.ctx_bound, m.s.max_ctx + m.branch_len + 1);
+  return std::max(1, (nk + kAttnChunk - 1) / kAttnChunk);
 }
 
 // One forward step of `m` over the M tokens described by P. Logits of all M
@@ -352,15 +365,16 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
   launch_pdl(embed_kernel, dim3(M), dim3(256), 0, s, (const bf16*)m.embed, d, m.embed_tiled, P, m.x);
   ++E.launches;
   const float scale = 1.0f / std::sqrt(float(hd));
-  const size_t attn_smem = attn_smem_bytes(m, E.maxK);
+  const int nch = attn_chunks(m);
+  const AttnWs aws{m.attn_part, m.attn_cnt};
   for (int l = 0; l < sh.n_layers; ++l) {
     const DevLayer& L = m.layers[size_t(l)];
     bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)nullptr, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-    launch_pdl(attention_kernel, dim3(KVH, M), dim3(kAttnThreads), attn_smem, s, (const float*)m.qkv, P, M,
-               (const float*)m.rope_cos, (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn);
+    launch_pdl(attention_kernel, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M,
+               (const float*)m.rope_cos, (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
     linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d,
                (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
@@ -519,6 +533,7 @@ static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_nee
   if (n < 1) throw Fail(SSD_ERROR, "prompt must hold at least one token");
   const int cap = std::min(E.T.s.max_ctx, E.D.s.max_ctx);
   if (max_ctx_needed > cap) throw Fail(SSD_TOO_LARGE, "context exceeds max_ctx");
+  E.T.ctx_bound = E.D.ctx_bound = max_ctx_needed + 2 * E.maxK + 2;
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= E.V) throw Fail(SSD_ERROR, "context_index: token out of range");
   CK(cudaMemcpy(E.hist, prompt, size_t(n) * 4, cudaMemcpyHostToDevice));
@@ -614,12 +629,6 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup) throw Fail(SSD_CONFIG, "engine: GQA group above 8");
-  {
-    // the attribute is per function, shared by every engine in the process
-    static size_t attn_smem_max = 0;
-    attn_smem_max = std::max({attn_smem_max, attn_smem_bytes(E.T, max_lookahead), attn_smem_bytes(E.D, max_lookahead)});
-    CK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_smem_max)));
-  }
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
@@ -981,6 +990,7 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   Model& m = which == 0 ? E.T : E.D;
   if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
   cudaStream_t s = E.sv;
+  m.ctx_bound = pos + M + 1;
   prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M);
   KCHECK();
   const ssd_model_shape& sh = m.s;

@@ -182,138 +182,177 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 
 enum Epi { EPI_STORE = 0, EPI_RESID = 1, EPI_SWIGLU = 2 };
 
-// Decode attention for one (kv head, query token), fused with RoPE and the
-// KV-cache append of this forward's tokens. GQA: the G = H / KVH query heads
-// of the group share every K/V read. Keys are the main-cache prefix
-// [0, main_len) plus a branch-local segment [bbase, bbase + blen): the
-// tree/branch mask of pre-speculation, generated arithmetically instead of
-// materialised. grid (KVH, M), 256 threads; qkv rows are
-// [q: H*hd][k: KVH*hd][v: KVH*hd] (fp32, pre-RoPE).
-constexpr int kAttnThreads = 256;
+// Decode attention, split over keys (flash-decoding) and fused with RoPE and
+// the KV-cache append of this forward's tokens. CTA = (key chunk, kv head,
+// query token); the G = H / KVH query heads of the group share every K/V
+// read. Keys of query m are the main-cache prefix [0, main_len) plus a
+// branch-local segment [bbase, bbase + blen): the tree/branch mask of
+// pre-speculation, generated arithmetically instead of materialised. Each
+// chunk writes (max, sum, unnormalised output) per head; the last chunk to
+// finish for (kv head, token) merges them in chunk order (deterministic).
+// qkv rows are [q: H*hd][k: KVH*hd][v: KVH*hd] (fp32, pre-RoPE).
+constexpr int kAttnThreads = 128;
+constexpr int kAttnChunk = 128;  // keys per CTA
 constexpr int kMaxGroup = 8;
+
+struct AttnWs {
+  float* part;   // [M][KVH][chunks][G][hd + 2]
+  int* counter;  // [M][KVH]
+};
 
 __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __restrict__ qkv, const FwdParams* __restrict__ P,
                                                                  int M, const float* __restrict__ cos_t,
                                                                  const float* __restrict__ sin_t, bf16* __restrict__ kc,
                                                                  bf16* __restrict__ vc, int S, int H, int KVH, int hd,
-                                                                 float scale, bf16* __restrict__ out) {
-  extern __shared__ float smem[];
+                                                                 float scale, bf16* __restrict__ out, AttnWs ws) {
+  __shared__ float qs[kMaxGroup * 128];
+  __shared__ float sc[kMaxGroup * kAttnChunk];
+  __shared__ float stat[kMaxGroup][2];
+  __shared__ int s_last;
   pdl_wait_all();
   asm volatile("griddepcontrol.launch_dependents;");
-  const int kvh = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = kAttnThreads / 32;
+  const int chunk = blockIdx.x, kvh = blockIdx.y, m = blockIdx.z, tid = threadIdx.x;
+  const int nchunks = gridDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int G = H / KVH, half = hd >> 1;
   const size_t row_len = size_t(H + 2 * KVH) * hd;
-  // 1) RoPE + append K/V of every token of this forward for this kv head
-  //    (identical values from all M CTAs of the head: each CTA sees its own
-  //    writes after the barrier, so no cross-CTA ordering is needed).
-  for (int e = tid; e < M * half; e += kAttnThreads) {
-    const int t = e / half, i = e % half;
-    const int pos = P->pos[t], slot = P->slot[t];
-    const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
-    const float* ks = qkv + size_t(t) * row_len + size_t(H + kvh) * hd;
-    const float* vs = qkv + size_t(t) * row_len + size_t(H + KVH + kvh) * hd;
-    const float a = ks[i], b = ks[i + half];
-    bf16* kd = kc + (size_t(kvh) * S + slot) * hd;
-    bf16* vd = vc + (size_t(kvh) * S + slot) * hd;
-    kd[i] = __float2bfloat16_rn(a * c - b * sn);
-    kd[i + half] = __float2bfloat16_rn(b * c + a * sn);
-    vd[i] = __float2bfloat16_rn(vs[i]);
-    vd[i + half] = __float2bfloat16_rn(vs[i + half]);
-  }
-  // 2) rotated queries of the group into shared memory
   const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
   const int nk = main_len + blen;
-  float* qs = smem;                  // [G][hd]
-  float* sc = qs + G * hd;           // [G][nk]
-  float* red = sc + G * nk;          // [G][2]
-  float* part = red + 2 * kMaxGroup; // [kAttnThreads][G]
-  {
-    const int pos = P->pos[m];
-    for (int e = tid; e < G * half; e += kAttnThreads) {
-      const int gg = e / half, i = e % half;
-      const float* src = qkv + size_t(m) * row_len + size_t(kvh * G + gg) * hd;
+  const int j0 = chunk * kAttnChunk, j1 = min(nk, j0 + kAttnChunk);
+  const int used = (nk + kAttnChunk - 1) / kAttnChunk;  // chunks holding keys of this query
+  float* part = ws.part + ((size_t(m) * KVH + kvh) * nchunks) * G * (hd + 2);
+  if (j0 < j1) {
+    // 1) append (RoPE'd) K and V of this forward's tokens whose slot falls
+    //    in this chunk (identical values wherever several CTAs write them)
+    for (int e = tid; e < M * half; e += kAttnThreads) {
+      const int t = e / half, i = e % half;
+      const int slot = P->slot[t];
+      const int j = slot < main_len ? slot : (slot >= bbase && slot < bbase + blen ? main_len + slot - bbase : -1);
+      if (j < j0 || j >= j1) continue;
+      const int pos = P->pos[t];
       const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
-      const float a = src[i], b = src[i + half];
-      qs[gg * hd + i] = a * c - b * sn;
-      qs[gg * hd + i + half] = b * c + a * sn;
+      const float* ks = qkv + size_t(t) * row_len + size_t(H + kvh) * hd;
+      const float* vs = qkv + size_t(t) * row_len + size_t(H + KVH + kvh) * hd;
+      const float a = ks[i], b = ks[i + half];
+      bf16* kd = kc + (size_t(kvh) * S + slot) * hd;
+      bf16* vd = vc + (size_t(kvh) * S + slot) * hd;
+      kd[i] = __float2bfloat16_rn(a * c - b * sn);
+      kd[i + half] = __float2bfloat16_rn(b * c + a * sn);
+      vd[i] = __float2bfloat16_rn(vs[i]);
+      vd[i + half] = __float2bfloat16_rn(vs[i + half]);
     }
-  }
-  __syncthreads();
-  // 3) scores: one key per warp iteration, lanes over head dims
-  const bf16* kbase = kc + size_t(kvh) * S * hd;
-  const bf16* vbase = vc + size_t(kvh) * S * hd;
-  const int dpl = hd / 32;  // dims per lane: 2 or 4
-  float qr[kMaxGroup][4];
-  for (int gg = 0; gg < G; ++gg)
-    for (int i = 0; i < dpl; ++i) qr[gg][i] = qs[gg * hd + lane * dpl + i];
-  for (int j = warp; j < nk; j += nwarps) {
-    const int slot = j < main_len ? j : bbase + (j - main_len);
-    const bf16* kr = kbase + size_t(slot) * hd + lane * dpl;
-    float kf[4];
-    if (dpl == 4) {
-      const uint2 u = *reinterpret_cast<const uint2*>(kr);
-      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-      kf[0] = f0.x; kf[1] = f0.y; kf[2] = f1.x; kf[3] = f1.y;
-    } else {
-      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr));
-      kf[0] = f0.x; kf[1] = f0.y; kf[2] = 0.f; kf[3] = 0.f;
+    // 2) rotated queries of the group
+    {
+      const int pos = P->pos[m];
+      for (int e = tid; e < G * half; e += kAttnThreads) {
+        const int gg = e / half, i = e % half;
+        const float* src = qkv + size_t(m) * row_len + size_t(kvh * G + gg) * hd;
+        const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
+        const float a = src[i], b = src[i + half];
+        qs[gg * hd + i] = a * c - b * sn;
+        qs[gg * hd + i + half] = b * c + a * sn;
+      }
     }
-    for (int gg = 0; gg < G; ++gg) {
-      float dot = 0.f;
-      for (int i = 0; i < dpl; ++i) dot += qr[gg][i] * kf[i];
-      dot = warp_sum(dot);
-      if (lane == 0) sc[gg * nk + j] = dot * scale;
-    }
-  }
-  __syncthreads();
-  // 4) softmax per head (warp gg handles head gg)
-  for (int gg = warp; gg < G; gg += nwarps) {
-    float mx = -INFINITY;
-    for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, sc[gg * nk + j]);
-    mx = warp_max(mx);
-    float den = 0.f;
-    for (int j = lane; j < nk; j += 32) {
-      const float e = expf(sc[gg * nk + j] - mx);
-      sc[gg * nk + j] = e;
-      den += e;
-    }
-    den = warp_sum(den);
-    if (lane == 0) red[gg] = den;
-  }
-  __syncthreads();
-  // 5) P.V: thread = (dim, key slice); every V element feeds all G heads
-  const int parts = kAttnThreads / hd;
-  const int dd = tid % hd, pp = tid / hd;
-  float acc[kMaxGroup];
-  for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
-  int j = pp;
-  for (; j + 3 * parts < nk; j += 4 * parts) {
-    float vv[4];
+    __syncthreads();
+    // 3) scores: one key per thread, full K row (16-byte loads, all issued)
+    const bf16* kbase = kc + size_t(kvh) * S * hd;
+    const bf16* vbase = vc + size_t(kvh) * S * hd;
+    {
+      const int j = j0 + tid;
+      if (j < j1) {
+        const int slot = j < main_len ? j : bbase + (j - main_len);
+        const uint4* kr = reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
+        float dot[kMaxGroup];
+        for (int gg = 0; gg < G; ++gg) dot[gg] = 0.f;
+        for (int c0 = 0; c0 < hd / 8; c0 += 4) {
+          uint4 kv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int jj = j + u * parts;
-      const int slot = jj < main_len ? jj : bbase + (jj - main_len);
-      vv[u] = __bfloat162float(vbase[size_t(slot) * hd + dd]);
-    }
-    for (int gg = 0; gg < G; ++gg)
+          for (int u = 0; u < 4; ++u) kv[u] = kr[c0 + u];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[gg] += sc[gg * nk + j + u * parts] * vv[u];
+          for (int u = 0; u < 4; ++u) {
+            float f[8];
+            bf16x8_to_f32(kv[u], f);
+            for (int gg = 0; gg < G; ++gg) {
+              const float* qq = qs + gg * hd + (c0 + u) * 8;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dot[gg] += qq[i] * f[i];
+            }
+          }
+        }
+        for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + tid] = dot[gg] * scale;
+      }
+    }
+    __syncthreads();
+    // 4) chunk softmax statistics (warp gg -> head gg)
+    const int n = j1 - j0;
+    for (int gg = warp; gg < G; gg += kAttnThreads / 32) {
+      float mx = -INFINITY;
+      for (int j = lane; j < n; j += 32) mx = fmaxf(mx, sc[gg * kAttnChunk + j]);
+      mx = warp_max(mx);
+      float den = 0.f;
+      for (int j = lane; j < n; j += 32) {
+        const float e = expf(sc[gg * kAttnChunk + j] - mx);
+        sc[gg * kAttnChunk + j] = e;
+        den += e;
+      }
+      den = warp_sum(den);
+      if (lane == 0) { stat[gg][0] = mx; stat[gg][1] = den; }
+    }
+    __syncthreads();
+    // 5) unnormalised P.V of the chunk: thread = head dim (x2 for hd = 64)
+    const int dpt = hd / kAttnThreads > 0 ? 1 : 1;
+    (void)dpt;
+    for (int dd = tid; dd < hd; dd += kAttnThreads) {
+      float acc[kMaxGroup];
+      for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
+      int j = 0;
+      for (; j + 8 <= n; j += 8) {
+        float vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int jj = j0 + j + u;
+          const int slot = jj < main_len ? jj : bbase + (jj - main_len);
+          vv[u] = __bfloat162float(vbase[size_t(slot) * hd + dd]);
+        }
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[gg] += sc[gg * kAttnChunk + j + u] * vv[u];
+      }
+      for (; j < n; ++j) {
+        const int jj = j0 + j;
+        const int slot = jj < main_len ? jj : bbase + (jj - main_len);
+        const float v = __bfloat162float(vbase[size_t(slot) * hd + dd]);
+        for (int gg = 0; gg < G; ++gg) acc[gg] += sc[gg * kAttnChunk + j] * v;
+      }
+      for (int gg = 0; gg < G; ++gg) part[(size_t(chunk) * G + gg) * (hd + 2) + dd] = acc[gg];
+    }
+    if (tid < G) {
+      part[(size_t(chunk) * G + tid) * (hd + 2) + hd] = stat[tid][0];
+      part[(size_t(chunk) * G + tid) * (hd + 2) + hd + 1] = stat[tid][1];
+    }
   }
-  for (; j < nk; j += parts) {
-    const int slot = j < main_len ? j : bbase + (j - main_len);
-    const float v = __bfloat162float(vbase[size_t(slot) * hd + dd]);
-    for (int gg = 0; gg < G; ++gg) acc[gg] += sc[gg * nk + j] * v;
-  }
-  for (int gg = 0; gg < G; ++gg) part[tid * G + gg] = acc[gg];
+  // 6) the last of this query's chunks merges them in chunk order
+  if (chunk >= used) return;
+  __threadfence();
   __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&ws.counter[m * KVH + kvh], 1) == used - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   for (int e = tid; e < G * hd; e += kAttnThreads) {
-    const int gg = e / hd, d2 = e % hd;
-    float o = 0.f;
-    for (int p2 = 0; p2 < parts; ++p2) o += part[(p2 * hd + d2) * G + gg];
-    out[size_t(m) * H * hd + size_t(kvh * G + gg) * hd + d2] = __float2bfloat16_rn(o / red[gg]);
+    const int gg = e / hd, dd = e % hd;
+    float mx = -INFINITY;
+    for (int c = 0; c < used; ++c) mx = fmaxf(mx, __ldcg(part + (size_t(c) * G + gg) * (hd + 2) + hd));
+    float den = 0.f, o = 0.f;
+    for (int c = 0; c < used; ++c) {
+      const float* pc = part + (size_t(c) * G + gg) * (hd + 2);
+      const float w = expf(__ldcg(pc + hd) - mx);
+      den += w * __ldcg(pc + hd + 1);
+      o += w * __ldcg(pc + dd);
+    }
+    out[size_t(m) * H * hd + size_t(kvh * G + gg) * hd + dd] = __float2bfloat16_rn(o / den);
   }
+  if (tid == 0) ws.counter[m * KVH + kvh] = 0;
 }
 
 // ------------------------------------------------------------------ top-k
