@@ -373,8 +373,11 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)nullptr, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-    launch_pdl(attention_kernel, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M,
-               (const float*)m.rope_cos, (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
+    {
+      auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
+      launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
+                 (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
+    }
     linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d,
                (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
@@ -628,7 +631,8 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
   build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
   for (const ssd_model_shape* s : {target, draft})
-    if (s->n_heads / s->n_kv_heads > kMaxGroup) throw Fail(SSD_CONFIG, "engine: GQA group above 8");
+    if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
+      throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));

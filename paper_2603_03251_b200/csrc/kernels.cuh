@@ -200,6 +200,7 @@ struct AttnWs {
   int* counter;  // [M][KVH]
 };
 
+template <int G>
 __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __restrict__ qkv, const FwdParams* __restrict__ P,
                                                                  int M, const float* __restrict__ cos_t,
                                                                  const float* __restrict__ sin_t, bf16* __restrict__ kc,
@@ -208,13 +209,14 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
   __shared__ float qs[kMaxGroup * 128];
   __shared__ float sc[kMaxGroup * kAttnChunk];
   __shared__ float stat[kMaxGroup][2];
+  __shared__ float pv_red[8192];  // [key groups][G][hd]: ngrp * hd = 1024, G <= 8
   __shared__ int s_last;
   pdl_wait_all();
   asm volatile("griddepcontrol.launch_dependents;");
   const int chunk = blockIdx.x, kvh = blockIdx.y, m = blockIdx.z, tid = threadIdx.x;
   const int nchunks = gridDim.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int G = H / KVH, half = hd >> 1;
+  const int half = hd >> 1;
   const size_t row_len = size_t(H + 2 * KVH) * hd;
   const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
   const int nk = main_len + blen;
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
       }
     }
     __syncthreads();
-    // 3) scores: one key per thread, full K row (16-byte loads, all issued)
+    // 3) scores: one key per thread; the whole K row is loaded up front
+    //    (hd/8 independent 16-byte loads in flight per thread)
     const bf16* kbase = kc + size_t(kvh) * S * hd;
     const bf16* vbase = vc + size_t(kvh) * S * hd;
     {
@@ -262,23 +265,31 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
       if (j < j1) {
         const int slot = j < main_len ? j : bbase + (j - main_len);
         const uint4* kr = reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
+        uint4 kv[16];
+        const int nv = hd >> 3;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (u < nv) kv[u] = kr[u];
         float dot[kMaxGroup];
+        
+#pragma unroll
         for (int gg = 0; gg < G; ++gg) dot[gg] = 0.f;
-        for (int c0 = 0; c0 < hd / 8; c0 += 4) {
-          uint4 kv[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) kv[u] = kr[c0 + u];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 16; ++u) {
+          if (u < nv) {
             float f[8];
             bf16x8_to_f32(kv[u], f);
-            for (int gg = 0; gg < G; ++gg) {
-              const float* qq = qs + gg * hd + (c0 + u) * 8;
+            
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+              const float* qq = qs + gg * hd + u * 8;
 #pragma unroll
               for (int i = 0; i < 8; ++i) dot[gg] += qq[i] * f[i];
             }
           }
         }
+        
+#pragma unroll
         for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + tid] = dot[gg] * scale;
       }
     }
@@ -299,32 +310,57 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
       if (lane == 0) { stat[gg][0] = mx; stat[gg][1] = den; }
     }
     __syncthreads();
-    // 5) unnormalised P.V of the chunk: thread = head dim (x2 for hd = 64)
-    const int dpt = hd / kAttnThreads > 0 ? 1 : 1;
-    (void)dpt;
-    for (int dd = tid; dd < hd; dd += kAttnThreads) {
-      float acc[kMaxGroup];
-      for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
-      int j = 0;
-      for (; j + 8 <= n; j += 8) {
-        float vv[8];
+    // 5) unnormalised P.V of the chunk. Thread = (key group, 8-dim chunk);
+    //    its <= 16 V vectors are loaded up front; partial sums are reduced
+    //    over key groups through shared memory.
+    {
+      const int nd = hd >> 3;                 // 16-byte chunks per row
+      const int ngrp = kAttnThreads / nd;     // key groups
+      const int dc = tid % nd, kg = tid / nd;
+      uint4 vv[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int jj = j0 + j + u;
-          const int slot = jj < main_len ? jj : bbase + (jj - main_len);
-          vv[u] = __bfloat162float(vbase[size_t(slot) * hd + dd]);
+      for (int u = 0; u < 16; ++u) {
+        const int jj = kg + u * ngrp;
+        if (jj < n) {
+          const int jabs = j0 + jj;
+          const int slot = jabs < main_len ? jabs : bbase + (jabs - main_len);
+          vv[u] = reinterpret_cast<const uint4*>(vbase + size_t(slot) * hd)[dc];
         }
+      }
+      float acc[kMaxGroup][8];
+      
+#pragma unroll
         for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[gg] += sc[gg * kAttnChunk + j + u] * vv[u];
+        for (int i = 0; i < 8; ++i) acc[gg][i] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int jj = kg + u * ngrp;
+        if (jj < n) {
+          float f[8];
+          bf16x8_to_f32(vv[u], f);
+          
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+            const float p = sc[gg * kAttnChunk + jj];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[gg][i] += p * f[i];
+          }
+        }
       }
-      for (; j < n; ++j) {
-        const int jj = j0 + j;
-        const int slot = jj < main_len ? jj : bbase + (jj - main_len);
-        const float v = __bfloat162float(vbase[size_t(slot) * hd + dd]);
-        for (int gg = 0; gg < G; ++gg) acc[gg] += sc[gg * kAttnChunk + j] * v;
+      float* red = pv_red;  // [ngrp][G][hd]
+      
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) red[(kg * G + gg) * hd + dc * 8 + i] = acc[gg][i];
+      __syncthreads();
+      for (int e = tid; e < G * hd; e += kAttnThreads) {
+        const int gg = e / hd, dd = e % hd;
+        float o = 0.f;
+        for (int k2 = 0; k2 < ngrp; ++k2) o += red[(k2 * G + gg) * hd + dd];
+        part[(size_t(chunk) * G + gg) * (hd + 2) + dd] = o;
       }
-      for (int gg = 0; gg < G; ++gg) part[(size_t(chunk) * G + gg) * (hd + 2) + dd] = acc[gg];
     }
     if (tid < G) {
       part[(size_t(chunk) * G + tid) * (hd + 2) + hd] = stat[tid][0];
