@@ -213,6 +213,10 @@ ssd_status ssd_verify_rows(ssd_engine* e, const float* target_rows, const float*
 ssd_status ssd_profile_forward(ssd_engine* e, int32_t which, int32_t M, int32_t pos, int32_t iters,
                                double* ms_forward, double* ms_gemm, int64_t* gemm_bytes, int32_t* gemm_launches);
 
+/* Read-only HBM streaming probe: achievable read bandwidth (GB/s) of a
+ * plain vectorised load kernel over `bytes`, averaged over `iters`. */
+ssd_status ssd_bench_read_bw(ssd_engine* e, int64_t bytes, int32_t iters, double* gbs);
+
 /* mt19937_64 parity: n outputs of Stream(seed).next_u64() computed on the GPU. */
 ssd_status ssd_rng_u64(ssd_engine* e, uint64_t seed, int32_t n, uint64_t* out);
 

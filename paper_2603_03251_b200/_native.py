@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libssd_b200.so")
+LIB_PATH = os.environ.get("SSD_B200_LIB", os.path.join(HERE, "libssd_b200.so"))
 MAX_LOOKAHEAD = 16
 
 # ---------------------------------------------------------------- structs
@@ -78,6 +78,7 @@ SIGNATURES = {
                                   C.c_uint64, i32p, i32p]),
     "ssd_profile_forward": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
                                       P(C.c_double), i64p, i32p]),
+    "ssd_bench_read_bw": (C.c_int, [EngineP, C.c_int64, C.c_int32, P(C.c_double)]),
     "ssd_rng_u64": (C.c_int, [EngineP, C.c_uint64, C.c_int32, u64p]),
     "ssd_weight_bits": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, C.c_int32, u16p]),
 }

@@ -393,6 +393,11 @@ class Engine:
                                             C.byref(n)))
         return {"ms_forward": f.value, "ms_gemm": g.value, "gemm_bytes": b.value, "gemm_launches": n.value}
 
+    def read_bw(self, nbytes: int = 4 << 30, iters: int = 10) -> float:
+        g = C.c_double()
+        _check(self.lib.ssd_bench_read_bw(self.h, nbytes, iters, C.byref(g)))
+        return g.value
+
     def rng_u64(self, seed: int, n: int) -> list:
         out = np.zeros(n, dtype=np.uint64)
         _check(self.lib.ssd_rng_u64(self.h, seed, n, _ptr(out, C.c_uint64)))

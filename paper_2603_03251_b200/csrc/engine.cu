@@ -21,6 +21,7 @@
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "rowops.cuh"
 
 namespace ssd {
 
@@ -131,6 +132,7 @@ struct Model {
   float* attn_part = nullptr;
   int* attn_cnt = nullptr;
   float *x = nullptr, *qkv = nullptr, *q = nullptr, *logits = nullptr;
+  float *dlt1 = nullptr, *dlt2 = nullptr;  // attention / MLP projections (residual deltas)
   bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
   int64_t weight_bytes = 0;
   float* ws = nullptr;   // split-K partials
@@ -163,6 +165,9 @@ struct Engine {
   RowStat* rstat = nullptr;
   double* cum = nullptr;
   int* tok_scratch = nullptr;
+  VI* cand = nullptr;       // row-op candidates [rows][chunks][T]
+  RowChunk* rstat2 = nullptr;
+  int nch = 1;              // vocabulary chunks of the row ops
   std::vector<void*> owned;
   long long launches = 0;
 };
@@ -208,7 +213,7 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   auto own = [&](void* p) { m.owned.push_back(p); return p; };
   auto padded = [](int N) { return size_t((N + tc::kBM - 1) / tc::kBM) * tc::kBM; };
   auto wmat = [&](WMat& w, int N, int K) {
-    if (K % tc::kBK) throw Fail(SSD_CONFIG, "engine: every GEMM K must be a multiple of 64");
+    if (K % (tc::kBK * tc::kKPS)) throw Fail(SSD_CONFIG, "engine: every GEMM K must be a multiple of 128");
     w.N = N;
     w.K = K;
     if (!w.w) w.w = static_cast<bf16*>(own(dalloc<bf16>(padded(N) * K)));
@@ -280,6 +285,9 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   // activations
   m.maxM = maxM;
   m.x = static_cast<float*>(own(dalloc<float>(size_t(maxM) * d)));
+  m.dlt1 = static_cast<float*>(own(dalloc<float>(size_t(maxM) * d)));
+  m.dlt2 = static_cast<float*>(own(dalloc<float>(size_t(maxM) * d)));
+  if (d > 8 * 4 * kNormThreads) throw Fail(SSD_CONFIG, "engine: d_model above 8192");
   m.xb = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * std::max(d, m.qd))));
   m.qkv = static_cast<float*>(own(dalloc<float>(size_t(maxM) * (m.qd + 2 * m.kvd))));
   m.q = static_cast<float*>(own(dalloc<float>(size_t(maxM) * m.qd)));
@@ -320,17 +328,65 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
                            cudaStream_t s) {
   using C = tc::Cfg<NP>;
   const int tiles = (W.N + tc::kBM - 1) / tc::kBM;
-  const int units = tiles * (W.K / tc::kBK);
-  const int grid = std::min(units, E_num_sms);
+  const int KU = W.K / (tc::kBK * tc::kKPS);
+  const int units = tiles * KU;
+#ifndef SSD_GEMM_CTAS_PER_SM
+// One CTA per SM with <= ~110 KB of stages: the next GEMM's CTA fits beside
+// it and prefetches its weights (PDL) while this one drains.
+#define SSD_GEMM_CTAS_PER_SM 1
+#endif
+  const int grid = std::min(units, E_num_sms * SSD_GEMM_CTAS_PER_SM);
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
-  tc::GemmArgs g{W.w, W.N, W.K / tc::kBK, M, Y, ldy, Yb, ldyb, m.ws, m.counters};
-  static bool configured = false;
-  if (!configured) {
-    CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
-    configured = true;
-  }
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters};
   launch_pdl(tc::gemm_tc_kernel<EPI, NP>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP), g);
 }
+
+template <int EPI, int NP>
+static void configure_gemm() {
+  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(tc::Cfg<NP>::kSmem)));
+}
+
+// Kernel attributes are set once, outside any stream capture.
+static void configure_kernels() {
+  configure_gemm<EPI_STORE, 16>(); configure_gemm<EPI_SWIGLU, 16>();
+  configure_gemm<EPI_STORE, 32>(); configure_gemm<EPI_SWIGLU, 32>();
+  configure_gemm<EPI_STORE, 48>(); configure_gemm<EPI_SWIGLU, 48>();
+  configure_gemm<EPI_STORE, 64>(); configure_gemm<EPI_SWIGLU, 64>();
+  configure_gemm<EPI_STORE, 96>(); configure_gemm<EPI_SWIGLU, 96>();
+  configure_gemm<EPI_STORE, 128>(); configure_gemm<EPI_SWIGLU, 128>();
+  configure_gemm<EPI_STORE, 192>(); configure_gemm<EPI_SWIGLU, 192>();
+  configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
+}
+
+// Stream capture of one round / step into an executable graph. All kernel
+// parameters (including the activation TMA maps) are baked in by value.
+template <class F>
+static cudaGraphExec_t capture_graph(cudaStream_t s, F&& body) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(s, &g));
+  cudaGraphExec_t ge = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  return ge;
+}
+
+struct GraphSet {
+  std::vector<cudaGraphExec_t> g;
+  ~GraphSet() {
+    for (auto x : g)
+      if (x) cudaGraphExecDestroy(x);
+  }
+};
 
 // Weight-streaming linear layer: tcgen05 swap-AB stream-K GEMM for every M
 // (M = 1 decode steps pad the token operand to 16).
@@ -371,23 +427,26 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
     const DevLayer& L = m.layers[size_t(l)];
     bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)nullptr, sh.norm_eps, m.xb);
+    // x += (previous layer's down projection); xb = norm(x)
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
+               (const float*)nullptr, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
     {
       auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
       launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
                  (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
     }
-    linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d,
+    linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s);
+    // x += attention projection; xb = norm(x) * g
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
                (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
     linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
-    linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s);
     E.launches += 3;
   }
   if (logits) {
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, s, (const float*)m.x, d, (const float*)m.final_gain, sh.norm_eps,
-               m.xb);
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt2, d,
+               (const float*)m.final_gain, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s);
     ++E.launches;
   }
@@ -451,6 +510,30 @@ static void raise_device_error(const LoopState& h) {
   if (h.error) throw Fail(SSD_ERROR, "device error " + std::to_string(h.error));
 }
 
+// Draw one token per row (greedy argmax or the scheme's law with the row's
+// uniform u[r * u_stride]) into out[r * out_stride]: two-phase row op.
+static void row_pick(Engine& E, const float* base, size_t stride, int rows, int V, const DScheme& ds, const double* u,
+                     int u_stride, int* out, int out_stride, cudaStream_t s) {
+  int T = 1;
+  if (ds.saguaro) T = ds.tau == 0.0 ? (ds.C == 0.0 ? ds.fan_out + 1 : 1) : ds.fan_out;
+  row_phase1_kernel<<<dim3(E.nch, rows), kRowThreads, 0, s>>>(base, stride, V, T, ds.tau, E.cand, E.rstat2);
+  row_sample_kernel<<<rows, kRowThreads, 0, s>>>(base, stride, V, E.nch, T, ds, E.cand, E.rstat2, u, u_stride, out,
+                                                 out_stride);
+  KCHECK();
+  E.launches += 2;
+}
+
+// Cache keys from K+1 contiguous logit rows (cache.cpp:249-270).
+static void row_keys(Engine& E, const float* rows, int nrows, int V, int max_f, const LoopState* st, const int* excl,
+                     int n_excl, cudaStream_t s) {
+  const int T = std::min(max_f + 1, kMaxTopF + 1);
+  row_phase1_kernel<<<dim3(E.nch, nrows), kRowThreads, 0, s>>>(rows, size_t(V), V, T, 0.0, E.cand, E.rstat2);
+  row_keys_kernel<<<nrows, kRowThreads, 0, s>>>(E.nch, T, E.cand, E.plans, E.offs, st, excl, n_excl, max_f, E.keys, E.bk,
+                                                E.btok);
+  KCHECK();
+  E.launches += 2;
+}
+
 // K sequential draft steps from the current history (specdec::draft,
 // specdec.cpp:8-25): rows into dmain, tokens into st->spec.
 static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int src, cudaStream_t s) {
@@ -459,9 +542,9 @@ static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int 
     prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i);
     forward(E, E.D, E.P_s, 1, E.dmain + size_t(i) * E.V, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
-    sample_rows_kernel<<<1, kSampleThreads, 0, s>>>(E.dmain + size_t(i) * E.V, E.V, ds, E.ubuf, 1, &E.st->spec[i], 1);
+    row_pick(E, E.dmain + size_t(i) * E.V, size_t(E.V), 1, E.V, ds, E.ubuf, 1, &E.st->spec[i], 1, s);
     KCHECK();
-    E.launches += 3;
+    E.launches += 2;
   }
   set_spec_rows_kernel<<<1, 32, 0, s>>>(E.st, E.dmain, E.V, origin, src);
   KCHECK();
@@ -489,20 +572,20 @@ static void prespeculate(Engine& E, int K, int B, int max_f, const ssd_scheme& s
   prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1);
   KCHECK();
   forward(E, E.D, E.P_x, K + 1, E.xrows, s);
-  keys_kernel<<<K + 1, 256, 0, s>>>(E.xrows, E.V, E.plans, E.offs, E.st, nullptr, K, max_f, E.keys, E.bk, E.btok);
+  row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s);
   const bool sampled = sc.temperature > 0.0;
   branch_streams_kernel<<<1, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
-  E.launches += 3;
+  E.launches += 2;
   const DScheme ds = dscheme(sc);
   float* rows = E.brows[parity];
   for (int j = 0; j < K; ++j) {
     prep_branch_kernel<<<(B + 127) / 128, 128, 0, s>>>(E.st, E.bk, E.btok, E.bt, E.P_b, B, j, E.D.s.max_ctx);
     float* out = rows + size_t(j) * B * E.V;
     forward(E, E.D, E.P_b, B, out, s);
-    sample_rows_kernel<<<B, kSampleThreads, 0, s>>>(out, E.V, ds, sampled ? E.bu + j : nullptr, K, E.bt + j, K);
+    row_pick(E, out, size_t(E.V), B, E.V, ds, sampled ? E.bu + j : nullptr, K, E.bt + j, K, s);
     KCHECK();
-    E.launches += 2;
+    E.launches += 1;
   }
 }
 
@@ -633,6 +716,7 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
       throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
+  configure_kernels();
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
@@ -664,6 +748,12 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   E.offs = static_cast<int*>(own(dalloc<int>(size_t(2 * (K + 1)))));
   E.rstat = static_cast<RowStat*>(own(dalloc<RowStat>(size_t(2 * K + 1))));
   E.tok_scratch = static_cast<int*>(own(dalloc<int>(64)));
+  E.nch = std::max(1, std::min(kMaxChunks, (V + 1023) / 1024));
+  {
+    const int rows = std::max(B, K + 1);
+    E.cand = static_cast<VI*>(own(dalloc<VI>(size_t(rows) * E.nch * (kMaxTopF + 1))));
+    E.rstat2 = static_cast<RowChunk*>(own(dalloc<RowChunk>(size_t(rows) * E.nch)));
+  }
   // exact sequential cumulative of the uniform law (FastRandom tokens)
   std::vector<double> cum(static_cast<size_t>(V));
   double c = 0.0;
@@ -712,18 +802,23 @@ ssd_status ssd_run_ar(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   cudaStream_t s = E.sv;
   reset_state(E, 1, n0, tokens, derive_seed(seed, 0), 0, nullptr, s);
   if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, s);
-  E.launches = 0;
   const DScheme d = dscheme(*ts);
-  CK(cudaEventRecord(E.ev_t0, s));
-  for (int64_t i = 0; i < tokens; ++i) {
+  // one decode step = one graph (device-resident state: no host round trip)
+  E.launches = 0;
+  GraphSet gs;
+  gs.g.push_back(capture_graph(s, [&] {
     prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1);
     forward(E, E.T, E.P_t, 1, E.tlogits, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
-    sample_rows_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.V, d, E.ubuf, 1, E.tok_scratch, 1);
+    row_pick(E, E.tlogits, size_t(E.V), 1, E.V, d, E.ubuf, 1, E.tok_scratch, 1, s);
     ar_commit_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.tok_scratch);
     KCHECK();
-    E.launches += 4;
-  }
+    E.launches += 3;
+  }));
+  const long long per_step = E.launches;
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t i = 0; i < tokens; ++i) CK(cudaGraphLaunch(gs.g[0], s));
+  E.launches = per_step * tokens;
   CK(cudaEventRecord(E.ev_t1, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
@@ -748,15 +843,20 @@ ssd_status ssd_run_sd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   reset_state(E, K, n0, c->rounds, derive_seed(c->seed, 0), 0, c, s);
   if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
   if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, s);
+  // one round (K draft steps, verify forward, decision, commit) = one graph
   E.launches = 0;
-  CK(cudaEventRecord(E.ev_t0, s));
-  for (int64_t r = 0; r < c->rounds; ++r) {
+  GraphSet gs;
+  gs.g.push_back(capture_graph(s, [&] {
     draft_steps(E, K, c->scheme, 0, 0, s);
     verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, /*single stream*/ 1, s);
     commit_kernel<<<1, 32, 0, s>>>(E.st);
     KCHECK();
     ++E.launches;
-  }
+  }));
+  const long long per_round = E.launches;
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t r = 0; r < c->rounds; ++r) CK(cudaGraphLaunch(gs.g[0], s));
+  E.launches = per_round * c->rounds;
   CK(cudaEventRecord(E.ev_t1, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
@@ -800,30 +900,45 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
                        cudaMemcpyHostToDevice, sv));
   }
   CK(cudaStreamSynchronize(sv));
-  E.launches = 0;
   const bool jit = c->backup_kind == 0;
+  // One SSD round = one graph: the verifier branch (verify forward +
+  // decision) and the speculator branch (extend, keys, K branch steps) fork
+  // from the verifier stream and join at the lookup. Two graphs alternate the
+  // branch-row buffers (the next round's verifier reads this round's rows).
+  E.launches = 0;
+  GraphSet gs;
+  for (int parity = 0; parity < 2; ++parity) {
+    gs.g.push_back(capture_graph(sv, [&] {
+      CK(cudaEventRecord(E.ev_fork, sv));
+      CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
+      prespeculate(E, K, B, max_f, c->scheme, parity, ss);
+      verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv);
+      CK(cudaEventRecord(E.ev_verified, sv));
+      CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
+      lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], B, E.V, E.cum, d_out, d_hit);
+      KCHECK();
+      ++E.launches;
+      CK(cudaEventRecord(E.ev_join, ss));
+      CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
+    }));
+  }
+  const long long per_round = E.launches / 2;
+  long long jit_launches = 0;
   CK(cudaEventRecord(E.ev_t0, sv));
   for (int64_t r = 0; r < R; ++r) {
-    const int parity = int(r & 1);
-    // fork: speculator follows everything enqueued on the verifier stream
-    CK(cudaEventRecord(E.ev_fork, sv));
-    CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
-    prespeculate(E, K, B, max_f, c->scheme, parity, ss);
-    verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv);
-    CK(cudaEventRecord(E.ev_verified, sv));
-    CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
-    lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], B, E.V, E.cum, d_out, d_hit);
-    KCHECK();
-    ++E.launches;
-    CK(cudaEventRecord(E.ev_join, ss));
-    CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
+    CK(cudaGraphLaunch(gs.g[size_t(r & 1)], sv));
     if (jit && r + 1 < R) {
       CK(cudaStreamSynchronize(sv));
       int hit = 0;
       CK(cudaMemcpy(&hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int), cudaMemcpyDeviceToHost));
-      if (!hit) draft_steps(E, K, c->scheme, 1, 2, sv);
+      if (!hit) {
+        const long long before = E.launches;
+        draft_steps(E, K, c->scheme, 1, 2, sv);
+        jit_launches += E.launches - before;
+      }
     }
   }
+  E.launches = per_round * R + jit_launches;
   CK(cudaEventRecord(E.ev_t1, sv));
   CK(cudaStreamSynchronize(sv));
   float ms = 0.f;
@@ -937,9 +1052,7 @@ ssd_status ssd_topk_keys(ssd_engine* h, const float* rows, int32_t n_rows, int32
   CK(cudaMemcpy(E.offs, off2.data(), off2.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(E.xrows, rows, size_t(n_rows) * V * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(E.tok_scratch, excluded, size_t(n_rows) * 4, cudaMemcpyHostToDevice));
-  keys_kernel<<<n_rows, 256, 0, E.sv>>>(E.xrows, V, E.plans, E.offs, nullptr, E.tok_scratch, n_rows, max_f, E.keys, E.bk,
-                                        E.btok);
-  KCHECK();
+  row_keys(E, E.xrows, n_rows, V, max_f, nullptr, E.tok_scratch, n_rows, E.sv);
   CK(cudaStreamSynchronize(E.sv));
   CK(cudaMemcpy(keys, E.keys, size_t(n_rows) * max_f * 4, cudaMemcpyDeviceToHost));
   API_END
@@ -1003,9 +1116,9 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
     for (int l = 0; l < sh.n_layers; ++l) {
       const DevLayer& L = m.layers[size_t(l)];
       linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-      linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s);
+      linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s);
       linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
-      linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s);
+      linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s);
     }
     linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits, sh.vocab, nullptr, 0, s);
   };
@@ -1031,6 +1144,27 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
                                     2LL * d + 4LL * sh.vocab);
   *gemm_bytes = m.weight_bytes + act;
   *gemm_launches = 4 * sh.n_layers + 1;
+  API_END
+}
+
+ssd_status ssd_bench_read_bw(ssd_engine* h, int64_t bytes, int32_t iters, double* gbs) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  const size_t n = size_t(bytes) / 16;
+  uint4* buf = dalloc<uint4>(n);
+  uint4* sink = dalloc<uint4>(1);
+  int sms = E_num_sms;
+  read_bw_kernel<<<sms * 8, 512, 0, E.sv>>>(buf, n, sink);
+  CK(cudaEventRecord(E.ev_t0, E.sv));
+  for (int i = 0; i < iters; ++i) read_bw_kernel<<<sms * 8, 512, 0, E.sv>>>(buf, n, sink);
+  CK(cudaEventRecord(E.ev_t1, E.sv));
+  CK(cudaEventSynchronize(E.ev_t1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  *gbs = double(n) * 16.0 * iters / (ms * 1e-3) / 1e9;
+  cudaFree(buf);
+  cudaFree(sink);
   API_END
 }
 

@@ -6,40 +6,45 @@
 //
 // Weights live pre-tiled in HBM: block (tile t, k-block kb)
 // is one contiguous 16 KB run holding the 128 x 64 bf16 tile already in the
-// SWIZZLE_128B K-major order of the UMMA descriptor, so a single 1-D bulk
-// copy (cp.async.bulk) streams it at full DRAM efficiency.
+// SWIZZLE_128B K-major order of the UMMA descriptor, and the k-blocks of a
+// tile are adjacent, so one 1-D bulk copy (cp.async.bulk) streams KPS
+// k-blocks (a "unit") at full DRAM efficiency.
 //
-// Persistent stream-K: the tiles x k-blocks work units are split into
-// gridDim.x contiguous ranges (one CTA per SM); a range crosses tile
-// boundaries, so every SM streams the same number of bytes. Warp 0 / lane 0
-// is the producer (weights before griddepcontrol.wait: they do not depend on
-// the previous kernel — PDL overlaps the weight stream with its tail),
-// warp 1 / lane 0 issues tcgen05.mma into a double-buffered TMEM
-// accumulator, warps 2-5 drain TMEM and apply the epilogue. A tile split
-// between CTAs is reduced by its last-arriving segment in a fixed order.
+// Persistent stream-K: the tiles x units work items are split into gridDim.x
+// contiguous ranges; a range crosses tile boundaries, so every CTA streams
+// the same number of bytes. Warp 0 / lane 0 is the producer (weights are
+// issued before griddepcontrol.wait: they do not depend on the previous
+// kernel — PDL overlaps the weight stream with its tail), warp 1 / lane 0
+// issues tcgen05.mma into a double-buffered TMEM accumulator, warps 2-5
+// drain TMEM and apply the epilogue. A tile split between CTAs is reduced by
+// its last-arriving segment in a fixed order (deterministic).
 #pragma once
 
 #include <cuda.h>
 
 #include "kernels.cuh"
 
+#ifndef SSD_GEMM_SMEM_KB
+#define SSD_GEMM_SMEM_KB 100
+#endif
+#ifndef SSD_GEMM_KPS
+#define SSD_GEMM_KPS 2
+#endif
+#ifndef SSD_GEMM_SPIN
+#define SSD_GEMM_SPIN 0
+#endif
+
 namespace ssd {
 namespace tc {
 
 constexpr int kBM = 128;        // weight rows per tile (UMMA M)
 constexpr int kBK = 64;         // K per block: one 128-byte swizzle atom of bf16
-constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+constexpr int kKPS = SSD_GEMM_KPS;          // k-blocks per pipeline stage
+constexpr int kABlock = kBM * kBK * 2;      // 16 KB
+constexpr int kABytes = kABlock * kKPS;
 constexpr int kThreads = 192;   // 6 warps
-// ~200 KB of stages: one CTA per SM keeps ~180 KB of weights in flight,
-// enough to cover the loaded HBM latency at 1/148 of the chip bandwidth.
-constexpr int kSmemBudget = 200 * 1024;
-
-// Element (r, c) of a [N][K] matrix in the pre-tiled layout (KB = K / 64).
-__host__ __device__ __forceinline__ size_t tiled_index(size_t r, size_t c, size_t KB) {
-  const size_t t = r >> 7, rr = r & 127, kb = c >> 6, cc = c & 63;
-  const size_t chunk = (cc >> 3) ^ (rr & 7);
-  return ((t * KB + kb) * 128 + rr) * 64 + chunk * 8 + (cc & 7);
-}
+// Stage budget per CTA; the host launches enough CTAs per SM to fill it.
+constexpr int kSmemBudget = SSD_GEMM_SMEM_KB * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
@@ -52,6 +57,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// Blocking wait (try_wait suspends the thread in hardware between probes).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -60,6 +66,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// Polling wait for the latency-critical producer / MMA threads.
+__device__ __forceinline__ void mbar_spin(uint64_t* b, uint32_t parity) {
+#if SSD_GEMM_SPIN
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra SPIN_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+#else
+  mbar_wait(b, parity);
+#endif
 }
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
@@ -121,7 +141,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
 struct GemmArgs {
   const bf16* W;  // pre-tiled weights
   int N;          // weight rows (logical)
-  int KB;         // K / 64
+  int KU;         // units per tile (K / (64 * KPS))
   int M;          // tokens (valid columns)
   float* Y;       // EPI_STORE / EPI_RESID output [M][ldy]
   int ldy;
@@ -158,12 +178,14 @@ __device__ __forceinline__ int cta_of(int u, long long U, long long P) {
 
 template <int NP>
 struct Cfg {
-  static constexpr int kBBytes = NP * kBK * 2;
-  static constexpr int kStages = (kSmemBudget / (kABytes + kBBytes)) < 2 ? 2
-                                 : ((kSmemBudget / (kABytes + kBBytes)) > 12 ? 12 : kSmemBudget / (kABytes + kBBytes));
+  static constexpr int kBBlock = NP * kBK * 2;
+  static constexpr int kBBytes = kBBlock * kKPS;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (kSmemBudget / kStageBytes) < 2 ? 2
+                                 : ((kSmemBudget / kStageBytes) > 12 ? 12 : kSmemBudget / kStageBytes);
   static constexpr int kAccCols = NP < 32 ? 32 : NP;
   static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
-  static constexpr size_t kSmem = 1024 + size_t(kStages) * (kABytes + kBBytes) + 256;
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + 256;
 };
 
 template <int EPI, int NP>
@@ -183,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (g.N + kBM - 1) / kBM;
-  const long long U = (long long)tiles * g.KB, P = gridDim.x;
+  const long long U = (long long)tiles * g.KU, P = gridDim.x;
   const int u0 = unit_begin(blockIdx.x, U, P), u1 = unit_begin(blockIdx.x + 1, U, P);
 
   if (threadIdx.x == 0) {
@@ -209,44 +231,52 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const int n = u1 - u0;
     const int pre = n < S ? n : S;
     for (int i = 0; i < pre; ++i) {  // weights only: independent of the previous kernel
-      const int u = u0 + i;
-      mbar_expect_tx(&full[i], kABytes + C::kBBytes);
-      bulk_load(sA + i * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[i], pol_w);
+      mbar_expect_tx(&full[i], C::kStageBytes);
+      bulk_load(sA + i * kABytes, g.W + size_t(u0 + i) * (kABytes / 2), kABytes, &full[i], pol_w);
     }
     pdl_wait();  // activations are produced by the previous kernel
     for (int i = 0; i < pre; ++i) {
-      const int u = u0 + i;
-      tma_load_2d(sB + i * C::kBBytes, &mapX, &full[i], (u % g.KB) * kBK, 0);
+      const int kb = ((u0 + i) % g.KU) * kKPS;
+#pragma unroll
+      for (int h = 0; h < kKPS; ++h)
+        tma_load_2d(sB + i * C::kBBytes + h * C::kBBlock, &mapX, &full[i], (kb + h) * kBK, 0);
     }
     for (int i = pre; i < n; ++i) {
       const int s = i % S;
-      mbar_wait(&empty[s], ((i / S) - 1) & 1);
+      mbar_spin(&empty[s], ((i / S) - 1) & 1);
       const int u = u0 + i;
-      mbar_expect_tx(&full[s], kABytes + C::kBBytes);
+      mbar_expect_tx(&full[s], C::kStageBytes);
       bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
-      tma_load_2d(sB + s * C::kBBytes, &mapX, &full[s], (u % g.KB) * kBK, 0);
+      const int kb = (u % g.KU) * kKPS;
+#pragma unroll
+      for (int h = 0; h < kKPS; ++h)
+        tma_load_2d(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kb + h) * kBK, 0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
     int seg = -1, cur_tile = -1;
     for (int i = 0; i < u1 - u0; ++i) {
-      const int u = u0 + i, t = u / g.KB, s = i % S;
+      const int u = u0 + i, t = u / g.KU, s = i % S;
       const bool first = t != cur_tile;
       if (first) {
         ++seg;
         cur_tile = t;
-        if (seg >= 2) mbar_wait(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
+        if (seg >= 2) mbar_spin(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
       }
-      mbar_wait(&full[s], (i / S) & 1);
+      mbar_spin(&full[s], (i / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * C::kBBytes);
       const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
 #pragma unroll
-      for (int k = 0; k < kBK / 16; ++k)
-        mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (!first || k) ? 1u : 0u);
+      for (int h = 0; h < kKPS; ++h) {
+        const uint32_t a0 = smem_u32(sA + s * kABytes + h * kABlock);
+        const uint32_t b0 = smem_u32(sB + s * C::kBBytes + h * C::kBBlock);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+          mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (!first || h || k) ? 1u : 0u);
+      }
       mma_commit(&empty[s]);
-      const bool last = (u + 1 == u1) || ((u + 1) / g.KB != t);
+      const bool last = (u + 1 == u1) || ((u + 1) / g.KU != t);
       if (last) mma_commit(&tfull[seg & 1]);
     }
   } else if (warp >= 2) {
@@ -256,10 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     int seg = -1;
     int u = u0;
     while (u < u1) {
-      const int t = u / g.KB;
-      const int kb_lo = u % g.KB;
-      const int seg_end = min(u1, (t + 1) * g.KB);
-      const bool whole = kb_lo == 0 && seg_end == (t + 1) * g.KB;
+      const int t = u / g.KU;
+      const int ku_lo = u % g.KU;
+      const int seg_end = min(u1, (t + 1) * g.KU);
+      const bool whole = ku_lo == 0 && seg_end == (t + 1) * g.KU;
       ++seg;
       const int b = seg & 1;
       mbar_wait(&tfull[b], (seg >> 1) & 1);
@@ -287,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       }
       if (!whole) {
         // last-arriving segment of tile t reduces the partials in CTA order
-        const int cf = cta_of(t * g.KB, U, P), cl = cta_of((t + 1) * g.KB - 1, U, P);
+        const int cf = cta_of(t * g.KU, U, P), cl = cta_of((t + 1) * g.KU - 1, U, P);
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (threadIdx.x == 64) s_last = atomicAdd(&g.counters[t], 1) == (cl - cf);
@@ -295,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if (s_last) {
           __threadfence();
           // only the first contributing CTA can start before the tile
-          const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KB ? 0 : 1);
+          const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KU ? 0 : 1);
           for (int t0 = 0; t0 < g.M; t0 += 8) {
             float acc[8];
 #pragma unroll

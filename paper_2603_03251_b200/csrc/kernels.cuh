@@ -141,6 +141,7 @@ __device__ __forceinline__ void pdl_wait_all() { asm volatile("griddepcontrol.wa
 // x[m][:] = E[token_m][:] (fp32 residual stream); E row-major or pre-tiled.
 __global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const FwdParams* __restrict__ P,
                              float* __restrict__ x) {
+  asm volatile("griddepcontrol.launch_dependents;");
   pdl_wait_all();
   const int m = blockIdx.x;
   const size_t tok = size_t(P->tokens[m]);
@@ -150,26 +151,49 @@ __global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const
   }
 }
 
-// RMSNorm (gain optional) with bf16 rounding of the output: the GEMM input
-// precision (oracle rmsnorm_bf16). One CTA per token, float4 loads.
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int d, const float* __restrict__ g,
-                                                      float eps, bf16* __restrict__ out) {
+// Residual add + RMSNorm (gain optional) with bf16 rounding of the output:
+// x += delta (the previous block's projection, when given), then
+// out = bf16(x * rsqrt(mean(x^2) + eps) * g) — the GEMM input precision
+// (oracle rmsnorm_bf16). Folding the residual add here keeps every GEMM
+// epilogue a plain store. One CTA per token, float4 accesses, d <= 8192.
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
+                                                               int d, const float* __restrict__ g, float eps,
+                                                               bf16* __restrict__ out) {
   __shared__ float sh[32];
-  pdl_wait_all();
+  // let the next kernel (a GEMM) launch now and prefetch its weights; it
+  // still waits for this grid, which waits for its own predecessor
   asm volatile("griddepcontrol.launch_dependents;");
+  pdl_wait_all();
   const int m = blockIdx.x;
-  const float4* xr = reinterpret_cast<const float4*>(x + size_t(m) * d);
+  float4* xr = reinterpret_cast<float4*>(x + size_t(m) * d);
+  const float4* dr = delta ? reinterpret_cast<const float4*>(delta + size_t(m) * d) : nullptr;
   const int n4 = d >> 2;
+  float4 keep[8];  // n4 / kNormThreads <= 8
   float ss = 0.f;
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-    const float4 v = xr[i];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < n4) {
+      float4 v = xr[i];
+      if (dr) {
+        const float4 e = dr[i];
+        v.x += e.x; v.y += e.y; v.z += e.z; v.w += e.w;
+        xr[i] = v;
+      }
+      keep[k] = v;
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
   }
   ss = block_sum(ss, sh);
   const float r = 1.0f / sqrtf(ss / float(d) + eps);
   __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out + size_t(m) * d);
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-    const float4 v = xr[i];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i >= n4) break;
+    const float4 v = keep[k];
     float a = v.x * r, b = v.y * r, c = v.z * r, e = v.w * r;
     if (g) {
       const float4 gg = reinterpret_cast<const float4*>(g)[i];
@@ -211,8 +235,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
   __shared__ float stat[kMaxGroup][2];
   __shared__ float pv_red[8192];  // [key groups][G][hd]: ngrp * hd = 1024, G <= 8
   __shared__ int s_last;
-  pdl_wait_all();
+  // let the next kernel (a GEMM) launch now and prefetch its weights; it
+  // still waits for this grid, which waits for its own predecessor
   asm volatile("griddepcontrol.launch_dependents;");
+  pdl_wait_all();
   const int chunk = blockIdx.x, kvh = blockIdx.y, m = blockIdx.z, tid = threadIdx.x;
   const int nchunks = gridDim.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -919,6 +945,22 @@ __global__ void commit_kernel(LoopState* st) {
 // AR: append sampled token.
 __global__ void ar_commit_kernel(LoopState* st, int* hist, const int* tok) {
   if (threadIdx.x == 0) { hist[st->n] = tok[0]; st->n += 1; st->tokens += 1; st->round += 1; }
+}
+
+// Read-only HBM streaming probe (the achievable read bandwidth).
+__global__ void __launch_bounds__(512) read_bw_kernel(const uint4* __restrict__ p, size_t n, uint4* sink) {
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  for (; i + 7 * stride < n; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ldg_stream(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { acc.x ^= v[u].x; acc.y ^= v[u].y; acc.z ^= v[u].z; acc.w ^= v[u].w; }
+  }
+  for (; i < n; i += stride) { const uint4 v = ldg_stream(p + i); acc.x ^= v.x; }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) *sink = acc;
 }
 
 __global__ void mt_init_kernel(Mt64* m, uint64_t seed) {
