@@ -217,6 +217,12 @@ ssd_status ssd_profile_forward(ssd_engine* e, int32_t which, int32_t M, int32_t 
  * plain vectorised load kernel over `bytes`, averaged over `iters`. */
 ssd_status ssd_bench_read_bw(ssd_engine* e, int64_t bytes, int32_t iters, double* gbs);
 
+/* TMA bulk-copy streaming probe (the GEMM's weight-stream shape): blocks of
+ * `block_bytes` through `stages`-deep mbarrier rings, mode 0 = contiguous
+ * range per CTA, 1 = round-robin blocks (chip-wide contiguous window). */
+ssd_status ssd_bench_tma_stream(ssd_engine* e, int64_t bytes, int32_t block_bytes, int32_t stages, int32_t mode,
+                                int32_t ctas_per_sm, int32_t iters, double* gbs);
+
 /* mt19937_64 parity: n outputs of Stream(seed).next_u64() computed on the GPU. */
 ssd_status ssd_rng_u64(ssd_engine* e, uint64_t seed, int32_t n, uint64_t* out);
 

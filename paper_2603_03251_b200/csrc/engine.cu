@@ -21,6 +21,7 @@
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "probe.cuh"
 #include "rowops.cuh"
 
 namespace ssd {
@@ -81,7 +82,12 @@ static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint
 struct WMat {
   bf16* w = nullptr;
   int N = 0, K = 0;
+  const WMat* next = nullptr;  // the GEMM that follows in a forward (L2 prefetch)
 };
+
+static long long gemm_units(const WMat& W) {
+  return (long long)((W.N + tc::kBM - 1) / tc::kBM) * (W.K / (tc::kBK * tc::kKPS));
+}
 
 // Launch with programmatic dependent launch (PDL): the kernel may start
 // while its predecessor drains; it calls griddepcontrol.wait before reading
@@ -170,6 +176,7 @@ struct Engine {
   int nch = 1;              // vocabulary chunks of the row ops
   std::vector<void*> owned;
   long long launches = 0;
+  int skip_mask = 0;  // profiling only (SSD_B200_SKIP): drop norms / attention
 };
 
 // ----------------------------------------------------------------- helpers
@@ -271,6 +278,16 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
     wb += int64_t(m.qd + 2 * m.kvd) * d + int64_t(d) * m.qd + int64_t(2 * s.ffn) * d + int64_t(d) * s.ffn;
   }
   wb += int64_t(s.vocab) * d;  // LM head
+  // forward order of the GEMMs: each one L2-prefetches the next one's first
+  // stages (qkv -> o -> gate/up -> down -> next layer ... -> head -> layer 0)
+  for (int l = 0; l < s.n_layers; ++l) {
+    DevLayer& L = m.layers[size_t(l)];
+    L.qkv.next = &L.o;
+    L.o.next = &L.gu;
+    L.gu.next = &L.dn;
+    L.dn.next = l + 1 < s.n_layers ? &m.layers[size_t(l + 1)].qkv : &m.head;
+  }
+  m.head.next = &m.layers[0].qkv;
   m.weight_bytes = wb * 2;
   // KV cache
   m.S = s.max_ctx + branch_slots;
@@ -337,7 +354,12 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
 #endif
   const int grid = std::min(units, E_num_sms * SSD_GEMM_CTAS_PER_SM);
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
-  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters};
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, nullptr, 0, 0};
+  if (W.next) {
+    g.nextW = W.next->w;
+    g.nextU = gemm_units(*W.next);
+    g.nextP = int(std::min<long long>(g.nextU, E_num_sms * SSD_GEMM_CTAS_PER_SM));
+  }
   launch_pdl(tc::gemm_tc_kernel<EPI, NP>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP), g);
 }
 
@@ -345,10 +367,41 @@ template <int EPI, int NP>
 static void configure_gemm() {
   CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           int(tc::Cfg<NP>::kSmem)));
+  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                          int(cudaSharedmemCarveoutMaxShared)));
+}
+
+// Every kernel of the step asks for the same (max shared) L1/SMEM carveout,
+// so consecutive kernels never force an SM carveout reconfiguration.
+template <typename F>
+static void carveout_max(F* f) {
+  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributePreferredSharedMemoryCarveout,
+                          int(cudaSharedmemCarveoutMaxShared)));
 }
 
 // Kernel attributes are set once, outside any stream capture.
 static void configure_kernels() {
+  carveout_max(embed_kernel);
+  carveout_max(rmsnorm_kernel);
+  carveout_max(attention_kernel<1>);
+  carveout_max(attention_kernel<2>);
+  carveout_max(attention_kernel<4>);
+  carveout_max(attention_kernel<8>);
+  carveout_max(row_phase1_kernel);
+  carveout_max(row_sample_kernel);
+  carveout_max(row_keys_kernel);
+  carveout_max(verify_stats_kernel);
+  carveout_max(verify_decide_kernel);
+  carveout_max(prep_chain_kernel);
+  carveout_max(prep_draft_step_kernel);
+  carveout_max(prep_prefill_kernel);
+  carveout_max(prep_branch_kernel);
+  carveout_max(branch_streams_kernel);
+  carveout_max(lookup_kernel);
+  carveout_max(set_spec_rows_kernel);
+  carveout_max(commit_kernel);
+  carveout_max(ar_commit_kernel);
+  carveout_max(draw_uniforms_kernel);
   configure_gemm<EPI_STORE, 16>(); configure_gemm<EPI_SWIGLU, 16>();
   configure_gemm<EPI_STORE, 32>(); configure_gemm<EPI_SWIGLU, 32>();
   configure_gemm<EPI_STORE, 48>(); configure_gemm<EPI_SWIGLU, 48>();
@@ -423,23 +476,27 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
   const float scale = 1.0f / std::sqrt(float(hd));
   const int nch = attn_chunks(m);
   const AttnWs aws{m.attn_part, m.attn_cnt};
+  // E.skip_mask: profiling only (results are wrong): 1 = norms, 2 = attention
+  const bool do_norm = !(E.skip_mask & 1), do_attn = !(E.skip_mask & 2);
   for (int l = 0; l < sh.n_layers; ++l) {
     const DevLayer& L = m.layers[size_t(l)];
     bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
     // x += (previous layer's down projection); xb = norm(x)
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
-               (const float*)nullptr, sh.norm_eps, m.xb);
+    if (do_norm)
+      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
+                 (const float*)nullptr, sh.norm_eps, m.xb);
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-    {
+    if (do_attn) {
       auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
       launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
                  (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
     }
     linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s);
     // x += attention projection; xb = norm(x) * g
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
-               (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
+    if (do_norm)
+      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
+                 (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
     linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
     linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s);
     E.launches += 3;
@@ -705,6 +762,7 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   E.maxB = max_branches;
   E.maxK = max_lookahead;
   E.V = target->vocab;
+  if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1167,6 +1225,38 @@ ssd_status ssd_bench_read_bw(ssd_engine* h, int64_t bytes, int32_t iters, double
   cudaFree(sink);
   API_END
 }
+
+ssd_status ssd_bench_tma_stream(ssd_engine* h, int64_t bytes, int32_t ublk, int32_t stages, int32_t mode,
+                                int32_t ctas_per_sm, int32_t iters, double* gbs) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (ublk % 16 || stages < 1 || ublk <= 0) throw Fail(SSD_CONFIG, "probe: bad block");
+  const long long units = bytes / ublk;
+  uint8_t* buf = dalloc<uint8_t>(size_t(units) * ublk);
+  unsigned* sink = dalloc<unsigned>(1);
+  const size_t smem = 1024 + size_t(stages) * ublk + 2 * 8 * size_t(stages);
+  CK(cudaFuncSetAttribute(tma_stream_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int grid = E_num_sms * ctas_per_sm;
+  tma_stream_probe<<<grid, 64, smem, E.sv>>>(buf, units, ublk, stages, mode, sink);
+  CK(cudaEventRecord(E.ev_t0, E.sv));
+  for (int i = 0; i < iters; ++i) tma_stream_probe<<<grid, 64, smem, E.sv>>>(buf, units, ublk, stages, mode, sink);
+  CK(cudaEventRecord(E.ev_t1, E.sv));
+  CK(cudaEventSynchronize(E.ev_t1));
+  KCHECK();
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  *gbs = double(units) * ublk * iters / (ms * 1e-3) / 1e9;
+  cudaFree(buf);
+  cudaFree(sink);
+  API_END
+}
+
+#if SSD_GEMM_TRACE
+extern "C" int ssd_debug_gemm_trace(unsigned long long* out /* 5 x 512 */) {
+  return int(cudaMemcpyFromSymbol(out, tc::g_trace, sizeof(unsigned long long) * 5 * 512));
+}
+#endif
 
 ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {
   API_BEGIN

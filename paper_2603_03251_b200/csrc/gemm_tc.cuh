@@ -24,18 +24,52 @@
 
 #include "kernels.cuh"
 
+// Measured on B200 (scripts/tma_probe.py, scripts/gemm_trace.py, profiles/):
+// bulk copies need >= 16 KB blocks (8 KB blocks halve the bandwidth), the
+// loaded issue->land latency is ~2.6 us, so one SM needs ~140 KB in flight
+// for its 1/148 share of 7.1 TB/s: 6 stages of 32 KB (two k-blocks per
+// stage, which also halves the per-stage barrier round trips). With this
+// ring the 8B LM head streams at ~7.1 TB/s; the per-kernel cold start is
+// hidden by the L2 prefetch chain (GemmArgs::nextW).
 #ifndef SSD_GEMM_SMEM_KB
-#define SSD_GEMM_SMEM_KB 100
+#define SSD_GEMM_SMEM_KB 220
 #endif
 #ifndef SSD_GEMM_KPS
 #define SSD_GEMM_KPS 2
 #endif
+#ifndef SSD_GEMM_MAX_STAGES
+#define SSD_GEMM_MAX_STAGES 6
+#endif
 #ifndef SSD_GEMM_SPIN
 #define SSD_GEMM_SPIN 0
+#endif
+#ifndef SSD_GEMM_SLEEP_EPI
+#define SSD_GEMM_SLEEP_EPI 0
+#endif
+#ifndef SSD_GEMM_NO_B_RELOAD
+#define SSD_GEMM_NO_B_RELOAD 0
 #endif
 
 namespace ssd {
 namespace tc {
+
+#ifndef SSD_GEMM_TRACE
+#define SSD_GEMM_TRACE 0
+#endif
+#if SSD_GEMM_TRACE
+// [0][i]: producer issue of unit i; [1][i]: MMA saw full; [2][i]: MMA
+// committed; [3][i]: producer saw empty (slot reuse); [4][0..1]: start/end.
+__device__ unsigned long long g_trace[5][512];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(row, i) \
+  do { if (blockIdx.x == 0 && (i) < 512) g_trace[row][i] = gtime(); } while (0)
+#else
+#define TRACE(row, i) do {} while (0)
+#endif
 
 constexpr int kBM = 128;        // weight rows per tile (UMMA M)
 constexpr int kBK = 64;         // K per block: one 128-byte swizzle atom of bf16
@@ -67,6 +101,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Sleeping wait for threads that idle for the whole main loop (epilogue):
+// keeps 128 waiting threads off the shared-memory barrier unit.
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* b, uint32_t parity) {
+#if SSD_GEMM_SLEEP_EPI
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(SSD_GEMM_SLEEP_EPI);
+  }
+#else
+  mbar_wait(b, parity);
+#endif
+}
+
 // Polling wait for the latency-critical producer / MMA threads.
 __device__ __forceinline__ void mbar_spin(uint64_t* b, uint32_t parity) {
 #if SSD_GEMM_SPIN
@@ -149,6 +204,12 @@ struct GemmArgs {
   int ldyb;
   float* ws;      // partials [2 * gridDim][M][128]
   int* counters;  // per-tile arrival counters (zeroed, self-resetting)
+  // The next GEMM of the forward (nullptr = none): once this CTA's weight
+  // stream is issued, it prefetches into L2 the first units that the same
+  // CTA index will stream in the next GEMM, hiding that kernel's cold start.
+  const bf16* nextW;
+  long long nextU;  // next GEMM's units
+  int nextP;        // next GEMM's grid size
 };
 
 template <int EPI>
@@ -182,7 +243,8 @@ struct Cfg {
   static constexpr int kBBytes = kBBlock * kKPS;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) < 2 ? 2
-                                 : ((kSmemBudget / kStageBytes) > 12 ? 12 : kSmemBudget / kStageBytes);
+                                 : ((kSmemBudget / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
+                                                                                      : kSmemBudget / kStageBytes);
   static constexpr int kAccCols = NP < 32 ? 32 : NP;
   static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + 256;
@@ -228,11 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // ---------------- producer
     uint64_t pol_w;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
     const int n = u1 - u0;
     const int pre = n < S ? n : S;
+    if (threadIdx.x == 0) TRACE(4, 0);
     for (int i = 0; i < pre; ++i) {  // weights only: independent of the previous kernel
       mbar_expect_tx(&full[i], C::kStageBytes);
       bulk_load(sA + i * kABytes, g.W + size_t(u0 + i) * (kABytes / 2), kABytes, &full[i], pol_w);
+      TRACE(0, i);
     }
     pdl_wait();  // activations are produced by the previous kernel
     for (int i = 0; i < pre; ++i) {
@@ -244,13 +309,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     for (int i = pre; i < n; ++i) {
       const int s = i % S;
       mbar_spin(&empty[s], ((i / S) - 1) & 1);
+      TRACE(3, i);
       const int u = u0 + i;
+#if SSD_GEMM_NO_B_RELOAD  // bandwidth experiment only: stale activations
+      mbar_expect_tx(&full[s], kABytes);
+      bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
+#else
       mbar_expect_tx(&full[s], C::kStageBytes);
       bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
       const int kb = (u % g.KU) * kKPS;
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
         tma_load_2d(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kb + h) * kBK, 0);
+#endif
+      TRACE(0, i);
+    }
+    if (g.nextW != nullptr && blockIdx.x < g.nextP) {
+      const long long b0 = (long long)blockIdx.x * g.nextU / g.nextP;
+      const long long b1 = (long long)(blockIdx.x + 1) * g.nextU / g.nextP;
+      const long long k = (b1 - b0) < S ? (b1 - b0) : S;
+      if (k > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.nextW + size_t(b0) * (kABytes / 2)),
+                     "r"(uint32_t(k * kABytes))
+                     : "memory");
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
@@ -265,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if (seg >= 2) mbar_spin(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
       }
       mbar_spin(&full[s], (i / S) & 1);
+      TRACE(1, i);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
 #pragma unroll
@@ -276,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (!first || h || k) ? 1u : 0u);
       }
       mma_commit(&empty[s]);
+      TRACE(2, i);
       const bool last = (u + 1 == u1) || ((u + 1) / g.KU != t);
       if (last) mma_commit(&tfull[seg & 1]);
     }
@@ -292,6 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const bool whole = ku_lo == 0 && seg_end == (t + 1) * g.KU;
       ++seg;
       const int b = seg & 1;
+      if (lane == 0) mbar_sleep_wait(&tfull[b], (seg >> 1) & 1);
+      __syncwarp();
       mbar_wait(&tfull[b], (seg >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(b * C::kAccCols);
@@ -349,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+  if (threadIdx.x == 0) TRACE(4, 1);
 }
 
 }  // namespace tc

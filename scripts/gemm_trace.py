@@ -1,0 +1,28 @@
+"""Per-stage timeline of CTA 0 of the last GEMM of a forward (trace build)."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_2603_03251_b200 as P  # noqa: E402
+from paper_2603_03251_b200.configs import shapes  # noqa: E402
+
+ts, ds = shapes("llama8b_1b", max_ctx=1024)
+e = P.Engine(ts, ds, P.Pair(), max_branches=20, max_lookahead=4)
+e.profile_forward(0, 1, 128, 3)  # last GEMM: the 8B LM head (M = 1)
+buf = (C.c_ulonglong * (5 * 512))()
+e.lib.ssd_debug_gemm_trace(buf)
+t = np.array(buf, dtype=np.float64).reshape(5, 512)
+t0 = t[4][0]
+n = int((t[0] > 0).sum())
+print("units traced", n, "kernel span us", (t[4][1] - t0) / 1e3)
+iss, full, com, emp = [(t[r][:n] - t0) / 1e3 for r in range(4)]
+for i in list(range(0, 14)) + list(range(n - 4, n)):
+    print(f"unit {i:3d} issue {iss[i]:8.2f} full {full[i]:8.2f} commit {com[i]:8.2f} empty_seen {emp[i]:8.2f}")
+lat = full[:n] - iss[:n]
+print("issue->full latency us: median %.2f p90 %.2f" % (np.median(lat), np.percentile(lat, 90)))
+gaps = np.diff(full[:n])
+print("MMA-side unit interval us: median %.3f mean %.3f" % (np.median(gaps), gaps.mean()))
