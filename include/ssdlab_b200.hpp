@@ -1,0 +1,322 @@
+// ssdlab_b200.hpp — header-only C++ shim over the C-ABI (ssd_b200.h) that
+// re-exports the reference's speculator / verifier / speculation-cache
+// interfaces (ssd-lab, proj/include/ssdlab/{specdec,cache,sim,categorical,
+// errors}.hpp) with the model parameter widened to a B200-resident
+// transformer pair (SURVEY.md §8b "Model parameter").
+//
+// Mapping (reference -> this shim):
+//   ssdlab::Error and subclasses (errors.hpp:9-61)  -> ssdlab_b200::Error ... (same names, thrown from ssd_status)
+//   dist::SamplingScheme (categorical.hpp:43-60)    -> ssdlab_b200::SamplingScheme
+//   cache::FanOutPlan (cache.hpp:18-25)             -> ssdlab_b200::FanOutPlan
+//   cache::geometric_fanout / uniform_fanout        -> same names (cache.hpp:57-64)
+//   specdec::draft (specdec.hpp:59-61)              -> Engine::draft
+//   specdec::verify (specdec.hpp:81-83)             -> Engine::verify_rows (decision on given logit rows)
+//   cache::build_cache (cache.hpp:149-154)          -> Engine::build_cache -> SpeculationCache
+//   SpeculationCache::lookup (cache.hpp:123-126)    -> SpeculationCache::lookup (non-owning pointer or nullptr)
+//   sim::run_ar / run_sd / run_protocol_harness     -> Engine::run_ar / run_sd / run_ssd
+//   lm::SyntheticLM::logits_at (lm.cpp:82-84)       -> Engine::logits
+//
+// Differences the caller must know: randomness is passed as a seed (the
+// engine seeds mt19937_64 streams on the device exactly as rng::Stream(seed)
+// does) instead of a mutable rng::Stream&; distributions stay on the device
+// (Speculation carries tokens and, on request, the fp32 logit rows).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ssd_b200.h"
+
+namespace ssdlab_b200 {
+
+// ------------------------------------------------------------ errors.hpp:9-61
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+#define SSDLAB_B200_ERR(name) \
+  struct name : Error {       \
+    using Error::Error;       \
+  };
+SSDLAB_B200_ERR(AllZeroError)
+SSDLAB_B200_ERR(DegenerateResidualError)
+SSDLAB_B200_ERR(TooLargeError)
+SSDLAB_B200_ERR(BudgetTooSmallError)
+SSDLAB_B200_ERR(DivergentError)
+SSDLAB_B200_ERR(InsufficientDataError)
+SSDLAB_B200_ERR(UnreachableError)
+SSDLAB_B200_ERR(NoCrossoverError)
+SSDLAB_B200_ERR(ProtocolViolationError)
+SSDLAB_B200_ERR(ConfigError)
+SSDLAB_B200_ERR(CudaError)
+#undef SSDLAB_B200_ERR
+
+// Re-throw an ssd_status as the reference exception class it stands for.
+inline void check(ssd_status s) {
+  if (s == SSD_OK) return;
+  const std::string m = ssd_last_error();
+  switch (s) {
+    case SSD_ALL_ZERO: throw AllZeroError(m);
+    case SSD_DEGENERATE_RESIDUAL: throw DegenerateResidualError(m);
+    case SSD_TOO_LARGE: throw TooLargeError(m);
+    case SSD_BUDGET_TOO_SMALL: throw BudgetTooSmallError(m);
+    case SSD_DIVERGENT: throw DivergentError(m);
+    case SSD_INSUFFICIENT_DATA: throw InsufficientDataError(m);
+    case SSD_UNREACHABLE: throw UnreachableError(m);
+    case SSD_NO_CROSSOVER: throw NoCrossoverError(m);
+    case SSD_PROTOCOL_VIOLATION: throw ProtocolViolationError(m);
+    case SSD_CONFIG: throw ConfigError(m);
+    case SSD_CUDA: throw CudaError(m);
+    default: throw Error(m);
+  }
+}
+
+// ------------------------------------------------------- categorical.hpp:43-60
+struct SamplingScheme {
+  enum class Kind { Standard, Saguaro } kind = Kind::Standard;
+  double temperature = 1.0;  // 0 = greedy (the tau -> 0 limit)
+  int fan_out = 0;
+  double downweight = 1.0;
+  static SamplingScheme standard(double t = 1.0) { return {Kind::Standard, t, 0, 1.0}; }
+  static SamplingScheme greedy() { return {Kind::Standard, 0.0, 0, 1.0}; }
+  static SamplingScheme saguaro(int f, double c, double t = 1.0) { return {Kind::Saguaro, t, f, c}; }
+  ssd_scheme c() const { return ssd_scheme{kind == Kind::Saguaro ? 1 : 0, fan_out, temperature, downweight}; }
+};
+
+enum class Origin { Primary = 0, Backup = 1 };       // specdec.hpp:14-20
+enum class BackupKind { SamePrimaryJIT = 0, FastRandom = 1 };  // sim.hpp:17-20
+
+// ----------------------------------------------------------- cache.hpp:18-68
+struct FanOutPlan {
+  std::vector<int> fan_out;
+  Origin role = Origin::Primary;
+  int budget = 0;
+  int lookahead() const { return int(fan_out.size()) - 1; }
+  int total() const {
+    int t = 0;
+    for (int f : fan_out) t += f;
+    return t;
+  }
+  ssd_plan c() const {
+    if (fan_out.empty() || fan_out.size() > SSD_MAX_LOOKAHEAD + 1) throw TooLargeError("plan: lookahead out of range");
+    ssd_plan p{};
+    p.lookahead = lookahead();
+    p.role = int(role);
+    p.budget = budget ? budget : total();
+    for (size_t k = 0; k < fan_out.size(); ++k) p.fan_out[k] = fan_out[k];
+    return p;
+  }
+  static FanOutPlan from_c(const ssd_plan& p) {
+    FanOutPlan f;
+    f.fan_out.assign(p.fan_out, p.fan_out + p.lookahead + 1);
+    f.role = Origin(p.role);
+    f.budget = p.budget;
+    return f;
+  }
+};
+
+inline FanOutPlan geometric_fanout(double acceptance, double exponent, int lookahead, int budget,
+                                   Origin role = Origin::Primary) {
+  ssd_plan p{};
+  check(ssd_geometric_fanout(acceptance, exponent, lookahead, budget, int(role), &p));
+  return FanOutPlan::from_c(p);
+}
+inline FanOutPlan uniform_fanout(int lookahead, int budget, Origin role = Origin::Primary) {
+  ssd_plan p{};
+  check(ssd_uniform_fanout(lookahead, budget, int(role), &p));
+  return FanOutPlan::from_c(p);
+}
+
+// ---------------------------------------------------------- specdec.hpp:22-52
+struct Speculation {
+  std::vector<int> tokens;
+  std::vector<float> rows;  // [K][V] fp32 draft logits (empty unless requested)
+  Origin origin = Origin::Primary;
+};
+struct VerificationOutcome {
+  int accepted = 0;
+  int bonus = 0;
+  bool operator==(const VerificationOutcome& o) const { return accepted == o.accepted && bonus == o.bonus; }
+  bool operator<(const VerificationOutcome& o) const {
+    return accepted != o.accepted ? accepted < o.accepted : bonus < o.bonus;
+  }
+};
+
+// cache.hpp:114-135: immutable after build; lookup returns a non-owning
+// pointer valid while the cache lives.
+class SpeculationCache {
+ public:
+  const Speculation* lookup(const VerificationOutcome& key) const {
+    auto it = entries_.find(key);
+    return it == entries_.end() ? nullptr : &it->second;
+  }
+  size_t size() const { return entries_.size(); }
+  const std::map<VerificationOutcome, Speculation>& entries() const { return entries_; }
+  Origin role = Origin::Primary;
+
+ private:
+  friend class Engine;
+  std::map<VerificationOutcome, Speculation> entries_;
+};
+
+// --------------------------------------------------------------- sim.hpp:28-104
+struct SimConfig {
+  int lookahead = 4;
+  SamplingScheme scheme = SamplingScheme::standard();
+  SamplingScheme target_scheme = SamplingScheme::standard();
+  FanOutPlan primary_plan, backup_plan;
+  BackupKind backup = BackupKind::FastRandom;
+  double primary_time = 0.3, backup_time = 0.0;
+  long rounds = 1000;
+  std::uint64_t seed = 0;
+  double accept_scale = 1.0;
+  ssd_sim_config c() const {
+    ssd_sim_config s{};
+    s.lookahead = lookahead;
+    s.scheme = scheme.c();
+    s.target_scheme = target_scheme.c();
+    s.primary_plan = primary_plan.c();
+    s.backup_plan = backup_plan.c();
+    s.backup_kind = int(backup);
+    s.primary_time = primary_time;
+    s.backup_time = backup_time;
+    s.rounds = rounds;
+    s.seed = seed;
+    s.accept_scale = accept_scale;
+    return s;
+  }
+};
+
+struct RunResult {
+  ssd_run_stats stats{};
+  std::vector<int> tokens;
+  std::vector<VerificationOutcome> outcomes;  // run_ssd only
+  std::vector<int> hits;                      // run_ssd only (-1 on the last round)
+  double hit_rate() const {
+    const long l = stats.primary_origin_lookups + stats.backup_origin_lookups;
+    return l ? double(stats.primary_origin_hits + stats.backup_origin_hits) / double(l) : 0.0;
+  }
+};
+
+// ------------------------------------------------------------------- engine
+class Engine {
+ public:
+  Engine(const ssd_model_shape& target, const ssd_model_shape& draft, const ssd_pair_params& pair, int device = 0,
+         int max_branches = 64, int max_lookahead = 8) {
+    ssd_engine* e = nullptr;
+    check(ssd_engine_create(&target, &draft, &pair, device, max_branches, max_lookahead, &e));
+    h_.reset(e);
+    vocab_ = target.vocab;
+  }
+  int vocab() const { return vocab_; }
+  ssd_engine* handle() const { return h_.get(); }
+
+  // lm::SyntheticLM::logits_at (lm.cpp:82-84); which: 0 target, 1 draft
+  std::vector<float> logits(int which, std::span<const int> ctx) const {
+    std::vector<float> out(static_cast<size_t>(vocab_));
+    check(ssd_logits(h_.get(), which, ctx.data(), int(ctx.size()), out.data()));
+    return out;
+  }
+
+  // specdec::draft (specdec.cpp:8-25) with Stream(seed)
+  Speculation draft(std::span<const int> ctx, int lookahead, const SamplingScheme& scheme, std::uint64_t seed,
+                    bool with_rows = false, Origin origin = Origin::Primary) const {
+    Speculation s;
+    s.tokens.resize(size_t(lookahead));
+    if (with_rows) s.rows.resize(size_t(lookahead) * size_t(vocab_));
+    const ssd_scheme sc = scheme.c();
+    check(ssd_draft(h_.get(), ctx.data(), int(ctx.size()), lookahead, &sc, seed, s.tokens.data(),
+                    with_rows ? s.rows.data() : nullptr));
+    s.origin = origin;
+    return s;
+  }
+
+  // specdec::verify decision (specdec.cpp:27-69) on target rows [K+1][V] and
+  // the speculation's draft rows [K][V] (empty = uniform, the FastRandom backup)
+  VerificationOutcome verify_rows(std::span<const float> target_rows, const Speculation& spec,
+                                  const SamplingScheme& draft_scheme, const SamplingScheme& target_scheme,
+                                  std::uint64_t seed, double accept_scale = 1.0) const {
+    const int K = int(spec.tokens.size());
+    if (target_rows.size() != size_t(K + 1) * size_t(vocab_)) throw Error("verify: target rows must be [K+1][V]");
+    const ssd_scheme ds = draft_scheme.c(), ts = target_scheme.c();
+    VerificationOutcome o;
+    check(ssd_verify_rows(h_.get(), target_rows.data(), spec.rows.empty() ? nullptr : spec.rows.data(),
+                          spec.tokens.data(), K, vocab_, &ds, &ts, accept_scale, seed, &o.accepted, &o.bonus));
+    return o;
+  }
+
+  // cache::build_cache (cache.cpp:232-277); base_seed = the one draw the
+  // reference takes from the caller's stream (cache.cpp:245)
+  SpeculationCache build_cache(std::span<const int> ctx, const Speculation& spec, const FanOutPlan& plan,
+                               const SamplingScheme& scheme, int next_lookahead, std::uint64_t base_seed) const {
+    if (plan.role != spec.origin) throw Error("build_cache: plan role does not match speculation origin");
+    const ssd_plan p = plan.c();
+    const ssd_scheme sc = scheme.c();
+    const int tot = std::max(1, plan.total());
+    std::vector<int> keys(size_t(2 * tot)), toks(size_t(tot) * size_t(next_lookahead));
+    int count = 0;
+    check(ssd_build_cache(h_.get(), ctx.data(), int(ctx.size()), spec.tokens.data(), int(spec.tokens.size()), &p,
+                          &sc, next_lookahead, base_seed, keys.data(), toks.data(), &count));
+    SpeculationCache c;
+    c.role = plan.role;
+    for (int i = 0; i < count; ++i) {
+      Speculation e;
+      e.tokens.assign(toks.begin() + i * next_lookahead, toks.begin() + (i + 1) * next_lookahead);
+      e.origin = Origin::Primary;
+      c.entries_.emplace(VerificationOutcome{keys[size_t(2 * i)], keys[size_t(2 * i + 1)]}, std::move(e));
+    }
+    return c;
+  }
+
+  RunResult run_ar(std::span<const int> prompt, const SamplingScheme& target_scheme, long tokens,
+                   std::uint64_t seed) const {
+    RunResult r;
+    r.tokens.resize(size_t(tokens));
+    const ssd_scheme ts = target_scheme.c();
+    check(ssd_run_ar(h_.get(), prompt.data(), int(prompt.size()), &ts, tokens, seed, r.tokens.data(), tokens,
+                     &r.stats));
+    return r;
+  }
+
+  RunResult run_sd(std::span<const int> prompt, const SimConfig& cfg) const {
+    RunResult r;
+    const long cap = cfg.rounds * (cfg.lookahead + 1);
+    r.tokens.resize(size_t(cap));
+    const ssd_sim_config c = cfg.c();
+    int64_t n = 0;
+    check(ssd_run_sd(h_.get(), prompt.data(), int(prompt.size()), &c, r.tokens.data(), cap, &n, &r.stats));
+    r.tokens.resize(size_t(n));
+    return r;
+  }
+
+  // sim::run_protocol_harness (sim.cpp:502-601)
+  RunResult run_ssd(std::span<const int> prompt, const SimConfig& cfg) const {
+    RunResult r;
+    const long cap = cfg.rounds * (cfg.lookahead + 1);
+    r.tokens.resize(size_t(cap));
+    std::vector<int> oc(size_t(2 * cfg.rounds));
+    r.hits.resize(size_t(cfg.rounds));
+    const ssd_sim_config c = cfg.c();
+    int64_t n = 0;
+    check(ssd_run_ssd(h_.get(), prompt.data(), int(prompt.size()), &c, r.tokens.data(), cap, &n, oc.data(),
+                      r.hits.data(), &r.stats));
+    r.tokens.resize(size_t(n));
+    for (long i = 0; i < cfg.rounds; ++i) r.outcomes.push_back({oc[size_t(2 * i)], oc[size_t(2 * i + 1)]});
+    return r;
+  }
+
+ private:
+  struct Del {
+    void operator()(ssd_engine* e) const { ssd_engine_destroy(e); }
+  };
+  std::unique_ptr<ssd_engine, Del> h_;
+  int vocab_ = 0;
+};
+
+}  // namespace ssdlab_b200

@@ -19,9 +19,12 @@ def load(path):
         v = float(d["Metric Value"].replace(",", ""))
         u = d["Metric Unit"]
         if d["Metric Name"] == "gpu__time_duration.sum":
-            e["us"] = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1e-3)
-        else:
-            e["mb"] = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
+            e["us"] = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                           "second": 1e6}.get(u, 1e-3)
+        elif d["Metric Name"].startswith("dram__bytes"):
+            # read + write (traffic)
+            e["mb"] = e.get("mb", 0.0) + v * {"byte": 1e-6, "Kbyte": 1e-3, "KB": 1e-3, "Mbyte": 1.0, "MB": 1.0,
+                                              "Gbyte": 1e3, "GB": 1e3}.get(u, 1e-6)
     return by
 
 
@@ -42,8 +45,8 @@ def summary(path, tail_from=None, top=25):
     tot = sum(a[1] for a in agg.values())
     print(f"{path}: {len(ids)} launches, {tot/1e3:.3f} ms total")
     for k, a in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-        gbs = a[2] / a[1] * 1e3 / 1e3 if a[1] else 0  # MB/us = TB/s -> GB/s
-        print(f"  {k[:44]:44s} n={a[0]:5d} {a[1]/1e3:8.3f} ms avg {a[1]/a[0]:8.2f} us  {100*a[1]/tot:5.1f}%  {gbs*1e3:8.0f} GB/s")
+        gbs = a[2] / a[1] * 1e3 if a[1] else 0  # MB/us -> GB/s
+        print(f"  {k[:44]:44s} n={a[0]:5d} {a[1]/1e3:8.3f} ms avg {a[1]/a[0]:8.2f} us  {100*a[1]/tot:5.1f}%  {gbs:8.0f} GB/s")
 
 
 if __name__ == "__main__":
