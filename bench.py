@@ -124,7 +124,7 @@ def cpu_sample(args, threads, rounds):
         args = argparse.Namespace(**{**vars(args), "config": "tiny"})
         P, ts, ds, cfg, prompt, fan, temp = workload(args)
     t0 = time.perf_counter()
-    pair = pyoracle.TfPair(P.shape_dict(ts), P.shape_dict(ds), P.Pair().as_dict(), threads=threads)
+    pair = pyoracle.TfPair(P.shape_dict(ts), P.shape_dict(ds), pair_for(args, P).as_dict(), threads=threads)
     build_s = time.perf_counter() - t0
     req = {"op": "simulate", "mode": "harness", "lookahead": cfg.lookahead, "rounds": rounds, "seed": cfg.seed,
            "prompt": prompt, "scheme": {"temperature": temp}, "primary_plan": {"fan": fan},
@@ -162,17 +162,114 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_split(args):
+    """N > 1: the split SSD run of DESIGN.md §6 — rank 0 verifier (target on
+    its own GPU), ranks 1..N-1 speculators (draft replicas, branch-sharded),
+    messages GPU -> GPU through NVLink-mapped mailboxes. One decode stream:
+    total work is fixed as N grows ("strong")."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_03251_b200.split import SplitEngine
+    ws, rank, local = dist_env()
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    # NCCL needs one GPU per rank; fewer GPUs than ranks (a functional run of
+    # the split protocol on one GPU) falls back to gloo for the plumbing
+    backend = "nccl" if ndev >= ws else "gloo"
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    else:
+        dist.init_process_group("gloo")
+    P, ts, ds, cfg, prompt, fan, temp = workload(args)
+    B = sum(fan)
+    se = SplitEngine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+    for _ in range(args.warmup):
+        se.run(prompt, cfg)
+    torch.cuda.synchronize()
+    dist.barrier()
+    runs, walls = [], []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = se.run(prompt, cfg)
+            walls.append(time.perf_counter() - t0)
+            runs.append(r)
+    torch.cuda.synchronize()
+    dist.barrier()
+    se.close()
+    # device time: each run's merged device_ms is already the max over ranks
+    dev_ms = sum(r.merged["device_ms"] for r in runs) if rank == 0 else 0.0
+    wall = sum(walls)
+    t = torch.tensor([wall], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall = float(t[0])
+    if rank == 0:
+        m = [r.merged for r in runs]
+        tokens = sum(x["tokens"] for x in m)
+        hits = sum(x["primary_origin_hits"] + x["backup_origin_hits"] for x in m)
+        lookups = sum(x["primary_origin_lookups"] + x["backup_origin_lookups"] for x in m)
+        acc = sum(x["accepted_sum"] for x in m) / sum(x["rounds"] for x in m)
+        value = tokens / (dev_ms * 1e-3)
+        # same-box baselines: AR and synchronous SD on the verifier's GPU
+        eng = P.Engine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+        ar = eng.run_ar(prompt, cfg.target_scheme or P.SamplingScheme.standard(temp), max(16, tokens // len(runs)),
+                        cfg.seed)
+        sd = eng.run_sd(prompt, cfg)
+        eng.close()
+        ar_tps = ar.tokens / (ar.device_ms * 1e-3)
+        sd_tps = sd.tokens / (sd.device_ms * 1e-3)
+        line = {"metric": "batch-1 decode tokens/sec (SSD)", "value": value, "unit": "tokens/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / len(runs),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (random-init correlated pair, random prompt)",
+                "config": {"workload": f"{args.config} ssd greedy K={cfg.lookahead} F={args.fanout} batch1 "
+                                       f"split 1 verifier + {ws - 1} speculators (branch-sharded)",
+                           "prompt_len": args.prompt_len, "rounds_per_step": args.rounds, "branches": B,
+                           "l2": "no flush: weights streamed per round >> 126 MB L2",
+                           "parallelism": f"verifier x1 + speculator x{ws - 1}, NVLink mailboxes",
+                           "gpus_visible": ndev},
+                "e2e": {"value": tokens / wall, "unit": "tokens/s", "h2d_bytes_per_step": 4 * len(prompt),
+                        "d2h_bytes_per_step": 4 * (tokens // len(runs))},
+                "gpu_launches": sum(x["kernel_launches"] for x in m) // len(m),
+                "ssd_tokens_per_s": value, "ar_tokens_per_s": ar_tps, "sd_tokens_per_s": sd_tps,
+                "speedup_vs_ar": value / ar_tps, "speedup_vs_sd": value / sd_tps,
+                "hit_rate": hits / lookups if lookups else None, "mean_accepted": acc,
+                "alpha": alpha_of(acc, cfg.lookahead),
+                "tokens_per_round": tokens / sum(x["rounds"] for x in m), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def alpha_of(mean_accepted: float, K: int) -> float:
+    """Per-token acceptance alpha from the mean accepted length
+    (E[accepted] = sum_{i=1..K} alpha^i)."""
+    lo, hi = 0.0, 1.0
+    for _ in range(60):
+        a = 0.5 * (lo + hi)
+        lo, hi = (a, hi) if sum(a ** i for i in range(1, K + 1)) < mean_accepted else (lo, a)
+    return lo
+
+
+def pair_for(args, P):
+    """The correlated random pair; --block-out-scale is the divergence knob
+     that sets the acceptance rate."""
+    return P.Pair(block_out_scale=args.block_out_scale)
+
+
 def run_ours(args):
     import numpy as np
     import torch
     ws, rank, local = dist_env()
+    if ws > 1 and args.multi == "split":
+        return run_split(args)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     P, ts, ds, cfg, prompt, fan, temp = workload(args)
     B = sum(fan)
-    eng = P.Engine(ts, ds, P.Pair(), device=local, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+    eng = P.Engine(ts, ds, pair_for(args, P), device=local, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
 
     def barrier():
         torch.cuda.synchronize()
@@ -239,6 +336,7 @@ def run_ours(args):
             "ssd_tokens_per_s": ssd_tps, "ar_tokens_per_s": ar_tps, "sd_tokens_per_s": sd_tps,
             "speedup_vs_ar": ssd_tps / ar_tps, "speedup_vs_sd": ssd_tps / sd_tps,
             "hit_rate": hits / lookups if lookups else None, "mean_accepted": acc,
+            "alpha": alpha_of(acc, cfg.lookahead),
             "tokens_per_round": tokens / sum(r.rounds for r in runs),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_kind": pk_kind,
@@ -279,6 +377,9 @@ def main():
     ap.add_argument("--sampled", dest="greedy", action="store_false")
     ap.add_argument("--seed", type=int, default=20250809)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--block-out-scale", type=float, default=0.1)
+    ap.add_argument("--multi", default="split", choices=["split", "replicas"],
+                    help="N>1: split verifier/speculator processes (default) or independent replicas")
     ap.set_defaults(greedy=True)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -118,6 +118,18 @@ typedef struct ssd_run_stats {
 
 typedef struct ssd_engine ssd_engine;
 
+/* Process roles of a split run: the reference's
+ * VerifierProcess / DraftProcess (sim.cpp:321-485) as separate OS processes
+ * on separate GPUs. A verifier materialises only the target, a speculator
+ * only the draft. */
+typedef enum ssd_role {
+  SSD_ROLE_COLOCATED = 0,
+  SSD_ROLE_VERIFIER = 1,
+  SSD_ROLE_SPECULATOR = 2
+} ssd_role;
+
+#define SSD_MAILBOX_HANDLE_BYTES 64
+
 /* ------------------------------------------------- plans (host-only) */
 
 /* cache::geometric_fanout (cache.hpp:57-60, cache.cpp:39-113). */
@@ -136,6 +148,10 @@ double ssd_conditional_hit_rate(const ssd_plan* plan, double acceptance, double 
 ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shape* draft,
                              const ssd_pair_params* pair, int32_t device, int32_t max_branches,
                              int32_t max_lookahead, ssd_engine** out);
+/* Same, for one role of a split run (ssd_role). */
+ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                  const ssd_pair_params* pair, int32_t device, int32_t role, int32_t max_branches,
+                                  int32_t max_lookahead, ssd_engine** out);
 ssd_status ssd_engine_destroy(ssd_engine* e);
 /* Bytes of weights streamed per forward step of model `which` (0 target,
  * 1 draft): the algorithmic bytes of one decode step. */
@@ -162,6 +178,34 @@ ssd_status ssd_run_ssd(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
                        const ssd_sim_config* cfg, int32_t* out_tokens, int64_t out_capacity,
                        int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits,
                        ssd_run_stats* stats);
+
+/* ------------------------------------------ split processes (sim.cpp:258-601)
+ * The reference's Channel between VerifierProcess and DraftProcess becomes
+ * device mailboxes in HBM, mapped across processes/GPUs by CUDA IPC (NVLink
+ * peer memory); messages are written by the sender's kernels inside the
+ * round graph. Peer table order: [0] verifier, [1..G] speculators. */
+
+/* Export this engine's mailbox (SSD_MAILBOX_HANDLE_BYTES bytes). */
+ssd_status ssd_mailbox_export(ssd_engine* e, uint8_t* handle);
+/* Map the peers' mailboxes: handles[i * SSD_MAILBOX_HANDLE_BYTES ..] for
+ * i in [0, n_peers); entry `self` is this engine's own. */
+ssd_status ssd_mailbox_connect(ssd_engine* e, int32_t n_peers, const uint8_t* handles, int32_t self);
+
+/* VerifierProcess side of run_protocol_harness (sim.cpp:321-351, 502-601):
+ * per round wait for the speculation, verify (M = K+1 target forward +
+ * fused verification), send (k*, t*) to the n_spec speculators. Writes the
+ * emitted tokens and per-round outcomes. */
+ssd_status ssd_run_ssd_verifier(ssd_engine* e, const int32_t* prompt, int32_t prompt_len, const ssd_sim_config* cfg,
+                                int32_t n_spec, int32_t* out_tokens, int64_t out_capacity, int64_t* out_len,
+                                int32_t* out_outcomes, ssd_run_stats* stats);
+
+/* DraftProcess side (sim.cpp:376-485) for speculator `rank` of n_spec:
+ * pre-speculates its block of branches while the verifier verifies, rebuilds
+ * the history from (k*, t*), looks up, backs up, and sends the next
+ * speculation when it owns the hit (or, rank 0, for a backup). Stats hold
+ * the full RunStats counters (identical on every speculator). */
+ssd_status ssd_run_ssd_speculator(ssd_engine* e, const int32_t* prompt, int32_t prompt_len, const ssd_sim_config* cfg,
+                                  int32_t rank, int32_t n_spec, int32_t* out_hits, ssd_run_stats* stats);
 
 /* ------------------------------------------ single operations (specdec.hpp,
  * cache.hpp). Each starts from `context` (prefilled into the model's KV). */

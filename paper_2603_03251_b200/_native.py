@@ -8,6 +8,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSD_B200_LIB", os.path.join(HERE, "libssd_b200.so"))
 MAX_LOOKAHEAD = 16
+MAILBOX_HANDLE_BYTES = 64
+ROLE_COLOCATED, ROLE_VERIFIER, ROLE_SPECULATOR = 0, 1, 2
 
 # ---------------------------------------------------------------- structs
 
@@ -62,7 +64,15 @@ SIGNATURES = {
     "ssd_conditional_hit_rate": (C.c_double, [P(Plan), C.c_double, C.c_double]),
     "ssd_engine_create": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32, C.c_int32,
                                     P(EngineP)]),
+    "ssd_engine_create_role": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32,
+                                         C.c_int32, C.c_int32, P(EngineP)]),
     "ssd_engine_destroy": (C.c_int, [EngineP]),
+    "ssd_mailbox_export": (C.c_int, [EngineP, P(C.c_uint8)]),
+    "ssd_mailbox_connect": (C.c_int, [EngineP, C.c_int32, P(C.c_uint8), C.c_int32]),
+    "ssd_run_ssd_verifier": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, i32p, C.c_int64, i64p,
+                                       i32p, P(RunStatsC)]),
+    "ssd_run_ssd_speculator": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, C.c_int32, i32p,
+                                         P(RunStatsC)]),
     "ssd_engine_weight_bytes": (C.c_int64, [EngineP, C.c_int32]),
     "ssd_run_ar": (C.c_int, [EngineP, i32p, C.c_int32, P(Scheme), C.c_int64, C.c_uint64, i32p, C.c_int64,
                              P(RunStatsC)]),

@@ -271,13 +271,16 @@ class Engine:
     """A (target, draft) pair resident on one B200 plus its decode loops."""
 
     def __init__(self, target: N.ModelShape, draft: N.ModelShape, pair: Pair = Pair(), device: int = 0,
-                 max_branches: int = 64, max_lookahead: int = 8):
+                 max_branches: int = 64, max_lookahead: int = 8, role: int = N.ROLE_COLOCATED):
+        """role: ROLE_COLOCATED (both models), ROLE_VERIFIER (target only) or
+        ROLE_SPECULATOR (draft only) — the processes of a split run."""
         self.lib = N.load()
         self.target, self.draft, self.pair = target, draft, pair
         self.vocab = target.vocab
+        self.role = role
         h = C.c_void_p()
-        _check(self.lib.ssd_engine_create(C.byref(target), C.byref(draft), C.byref(pair.c()), device, max_branches,
-                                          max_lookahead, C.byref(h)))
+        _check(self.lib.ssd_engine_create_role(C.byref(target), C.byref(draft), C.byref(pair.c()), device, role,
+                                               max_branches, max_lookahead, C.byref(h)))
         self.h = h
 
     def close(self):
@@ -326,6 +329,46 @@ class Engine:
                                     C.byref(n), _ptr(oc, C.c_int32), _ptr(hits, C.c_int32), C.byref(st)))
         r = RunStats._from_c(st, out[: n.value].tolist())
         r.outcomes = oc.reshape(-1, 2)
+        r.hits = hits
+        return r
+
+    # ---- split processes (sim.cpp:258-601 over NVLink mailboxes; paper_2603_03251_b200/split.py)
+    def mailbox_handle(self) -> bytes:
+        buf = (C.c_uint8 * N.MAILBOX_HANDLE_BYTES)()
+        _check(self.lib.ssd_mailbox_export(self.h, buf))
+        return bytes(buf)
+
+    def connect(self, handles: Sequence[bytes], self_index: int):
+        """Map the peers' mailboxes; order [verifier, speculator 0, ...]."""
+        blob = b"".join(handles)
+        if len(blob) != N.MAILBOX_HANDLE_BYTES * len(handles):
+            raise ConfigError("mailbox: every handle must be 64 bytes")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(self.lib.ssd_mailbox_connect(self.h, len(handles), buf, self_index))
+
+    def run_ssd_verifier(self, prompt: Sequence[int], cfg: SimConfig, n_spec: int) -> RunStats:
+        """VerifierProcess side of run_protocol_harness (sim.cpp:321-351)."""
+        p = _i32(prompt)
+        cap = cfg.rounds * (cfg.lookahead + 1)
+        out = np.zeros(cap, dtype=np.int32)
+        oc = np.zeros(2 * cfg.rounds, dtype=np.int32)
+        n = C.c_int64()
+        st = N.RunStatsC()
+        _check(self.lib.ssd_run_ssd_verifier(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), n_spec,
+                                             _ptr(out, C.c_int32), cap, C.byref(n), _ptr(oc, C.c_int32),
+                                             C.byref(st)))
+        r = RunStats._from_c(st, out[:n.value].tolist())
+        r.outcomes = oc.reshape(-1, 2)
+        return r
+
+    def run_ssd_speculator(self, prompt: Sequence[int], cfg: SimConfig, rank: int, n_spec: int) -> RunStats:
+        """DraftProcess side (sim.cpp:376-485) for speculator `rank` of n_spec."""
+        p = _i32(prompt)
+        hits = np.zeros(cfg.rounds, dtype=np.int32)
+        st = N.RunStatsC()
+        _check(self.lib.ssd_run_ssd_speculator(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), rank, n_spec,
+                                               _ptr(hits, C.c_int32), C.byref(st)))
+        r = RunStats._from_c(st)
         r.hits = hits
         return r
 

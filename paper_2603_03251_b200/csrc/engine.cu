@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "probe.cuh"
 #include "rowops.cuh"
+#include "split.cuh"
 
 namespace ssd {
 
@@ -177,6 +178,14 @@ struct Engine {
   std::vector<void*> owned;
   long long launches = 0;
   int skip_mask = 0;  // profiling only (SSD_B200_SKIP): drop norms / attention
+  // split processes (split.cuh)
+  int role = 0;                      // 0 colocated, 1 verifier, 2 speculator
+  Inbox* inbox = nullptr;            // this process's mailbox (+ draft rows)
+  std::vector<Inbox*> peers;         // mapped peer inboxes: [0] verifier, [1..G] speculators
+  std::vector<void*> ipc_opened;     // handles to close
+  Inbox** peers_dev = nullptr;       // device copy of `peers`
+  int* send_counter = nullptr;
+  int seq_base = 0;                  // advances by rounds + 2 per split run
 };
 
 // ----------------------------------------------------------------- helpers
@@ -525,6 +534,11 @@ static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t
   }
 }
 
+// A split process holds only its own model.
+static void need(const Model& m, const char* what) {
+  if (m.layers.empty()) throw Fail(SSD_CONFIG, std::string(what) + ": model not materialised in this engine's role");
+}
+
 static DScheme dscheme(const ssd_scheme& s) {
   return DScheme{s.kind == 1 ? 1 : 0, s.fan_out, s.temperature, s.downweight};
 }
@@ -549,6 +563,7 @@ static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed,
   h.backup_kind = c ? c->backup_kind : 1;
   h.primary_time = c ? c->primary_time : 0.0;
   h.backup_time = c ? (c->backup_kind == 0 ? c->primary_time : c->backup_time) : 0.0;
+  h.seq_base = E.seq_base;
   CK(cudaMemcpyAsync(E.st, &h, offsetof(LoopState, vrng), cudaMemcpyHostToDevice, s));
   mt_init_kernel<<<1, 32, 0, s>>>(&E.st->vrng, vseed);
   mt_init_kernel<<<1, 32, 0, s>>>(&E.st->drng, dseed);
@@ -625,7 +640,10 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 // Pre-speculation for the in-flight speculation (cache::build_cache,
 // cache.cpp:232-277, batched): extend over [last, s_1..s_K], candidate keys,
 // per-branch streams, K branch decode steps at M = B.
-static void prespeculate(Engine& E, int K, int B, int max_f, const ssd_scheme& sc, int parity, cudaStream_t s) {
+// Branch sharding: every speculator computes the full key
+// table and the per-branch streams, and decodes branches [lo, lo + Bl).
+static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
+                         cudaStream_t s) {
   prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1);
   KCHECK();
   forward(E, E.D, E.P_x, K + 1, E.xrows, s);
@@ -634,13 +652,15 @@ static void prespeculate(Engine& E, int K, int B, int max_f, const ssd_scheme& s
   branch_streams_kernel<<<1, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
   E.launches += 2;
+  if (Bl <= 0) return;
   const DScheme ds = dscheme(sc);
   float* rows = E.brows[parity];
   for (int j = 0; j < K; ++j) {
-    prep_branch_kernel<<<(B + 127) / 128, 128, 0, s>>>(E.st, E.bk, E.btok, E.bt, E.P_b, B, j, E.D.s.max_ctx);
-    float* out = rows + size_t(j) * B * E.V;
-    forward(E, E.D, E.P_b, B, out, s);
-    row_pick(E, out, size_t(E.V), B, E.V, ds, sampled ? E.bu + j : nullptr, K, E.bt + j, K, s);
+    prep_branch_kernel<<<(Bl + 127) / 128, 128, 0, s>>>(E.st, E.bk + lo, E.btok + lo, E.bt, E.P_b, Bl, j,
+                                                         E.D.s.max_ctx);
+    float* out = rows + size_t(j) * Bl * E.V;
+    forward(E, E.D, E.P_b, Bl, out, s);
+    row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * K + j : nullptr, K, E.bt + j, K, s);
     KCHECK();
     E.launches += 1;
   }
@@ -744,8 +764,15 @@ int ssd_abi_version(void) { return SSD_B200_ABI_VERSION; }
 
 ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shape* draft, const ssd_pair_params* pair,
                              int32_t device, int32_t max_branches, int32_t max_lookahead, ssd_engine** out) {
+  return ssd_engine_create_role(target, draft, pair, device, SSD_ROLE_COLOCATED, max_branches, max_lookahead, out);
+}
+
+ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                  const ssd_pair_params* pair, int32_t device, int32_t role, int32_t max_branches,
+                                  int32_t max_lookahead, ssd_engine** out) {
   API_BEGIN
   if (!target || !draft || !pair || !out) throw Fail(SSD_CONFIG, "engine: null argument");
+  if (role < SSD_ROLE_COLOCATED || role > SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "engine: unknown role");
   if (target->vocab != draft->vocab) throw Fail(SSD_ERROR, "sim: target and draft shapes differ");
   if (draft->d_model > target->d_model || draft->ffn > target->ffn || !draft->tied)
     throw Fail(SSD_CONFIG, "engine: the draft must be tied and no wider than the target");
@@ -762,6 +789,7 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   E.maxB = max_branches;
   E.maxK = max_lookahead;
   E.V = target->vocab;
+  E.role = role;
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   {
     int sms = 0;
@@ -769,8 +797,12 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
     E_num_sms = sms;
   }
   const int maxM = std::max(max_branches, max_lookahead + 1);
-  build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
-  build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
+  // a split process materialises only its own model
+  if (role != SSD_ROLE_SPECULATOR) build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
+  else E.T.s = *target;
+  if (role != SSD_ROLE_VERIFIER)
+    build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
+  else E.D.s = *draft;
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
       throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
@@ -818,6 +850,14 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
   for (int i = 0; i < V; ++i) { c += 1.0 / V; cum[size_t(i)] = c; }
   E.cum = static_cast<double*>(own(dalloc<double>(size_t(V))));
   CK(cudaMemcpy(E.cum, cum.data(), size_t(V) * 8, cudaMemcpyHostToDevice));
+  // mailbox (own allocation so it can be exported alone by CUDA IPC)
+  {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, kInboxRows + size_t(K) * V * 4));
+    CK(cudaMemset(p, 0, kInboxRows + size_t(K) * V * 4));
+    E.inbox = static_cast<Inbox*>(p);
+    E.send_counter = static_cast<int*>(own(dalloc<int>(1)));
+  }
   CK(cudaDeviceSynchronize());
   *out = h;
   API_END
@@ -831,6 +871,9 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   cudaDeviceSynchronize();
   free_model(E.T);
   free_model(E.D);
+  for (void* p : E.ipc_opened) cudaIpcCloseMemHandle(p);
+  if (E.inbox) cudaFree(E.inbox);
+  if (E.peers_dev) cudaFree(E.peers_dev);
   for (void* p : E.owned) cudaFree(p);
   cudaStreamDestroy(E.sv);
   cudaStreamDestroy(E.ss);
@@ -853,6 +896,7 @@ ssd_status ssd_run_ar(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
+  need(E.T, "run_ar");
   if (tokens < 1) throw Fail(SSD_ERROR, "run_ar: tokens must be >= 1");
   if (!ts) throw Fail(SSD_CONFIG, "run_ar: scheme required");
   check_scheme(*ts, E.V);
@@ -895,6 +939,8 @@ ssd_status ssd_run_sd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   validate_cfg(E, c);
+  need(E.T, "run_sd");
+  need(E.D, "run_sd");
   const int K = c->lookahead;
   set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + K + 2));
   cudaStream_t s = E.sv;
@@ -933,8 +979,9 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   validate_cfg(E, c);
+  need(E.T, "run_ssd");
+  need(E.D, "run_ssd");
   const int K = c->lookahead;
-  if (c->primary_time < 1.0 && false) {}
   int B = 0, max_f = 0;
   upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);
   set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2));
@@ -969,11 +1016,12 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
     gs.g.push_back(capture_graph(sv, [&] {
       CK(cudaEventRecord(E.ev_fork, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
-      prespeculate(E, K, B, max_f, c->scheme, parity, ss);
+      prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss);
       verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv);
       CK(cudaEventRecord(E.ev_verified, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
-      lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], B, E.V, E.cum, d_out, d_hit);
+      lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, B, E.V, E.cum, d_out,
+                                      d_hit);
       KCHECK();
       ++E.launches;
       CK(cudaEventRecord(E.ev_join, ss));
@@ -1012,12 +1060,219 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
   API_END
 }
 
+// ------------------------------------------------- split processes (§6)
+
+ssd_status ssd_mailbox_export(ssd_engine* h, uint8_t* handle64) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!handle64) throw Fail(SSD_CONFIG, "mailbox: null handle buffer");
+  cudaIpcMemHandle_t mh;
+  CK(cudaIpcGetMemHandle(&mh, E.inbox));
+  static_assert(sizeof(mh) == SSD_MAILBOX_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle64, &mh, sizeof(mh));
+  API_END
+}
+
+ssd_status ssd_mailbox_connect(ssd_engine* h, int32_t n_peers, const uint8_t* handles, int32_t self) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (n_peers < 2 || !handles || self < 0 || self >= n_peers) throw Fail(SSD_CONFIG, "mailbox: bad peer table");
+  for (void* p : E.ipc_opened) cudaIpcCloseMemHandle(p);
+  E.ipc_opened.clear();
+  E.peers.assign(size_t(n_peers), nullptr);
+  for (int i = 0; i < n_peers; ++i) {
+    if (i == self) {
+      E.peers[size_t(i)] = E.inbox;
+      continue;
+    }
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, handles + size_t(i) * SSD_MAILBOX_HANDLE_BYTES, sizeof(mh));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+    E.ipc_opened.push_back(p);
+    E.peers[size_t(i)] = static_cast<Inbox*>(p);
+  }
+  if (E.peers_dev) cudaFree(E.peers_dev);
+  E.peers_dev = dalloc<Inbox*>(size_t(n_peers));
+  CK(cudaMemcpy(E.peers_dev, E.peers.data(), size_t(n_peers) * sizeof(Inbox*), cudaMemcpyHostToDevice));
+  // a fresh connection starts from a clean inbox and sequence 0
+  CK(cudaMemset(E.inbox, 0, kInboxRows));
+  E.seq_base = 0;
+  CK(cudaDeviceSynchronize());
+  API_END
+}
+
+// Branch block of speculator `rank` out of G (contiguous, sizes differ by <= 1).
+static void branch_block(int B, int rank, int G, int& lo, int& Bl) {
+  lo = int((long long)B * rank / G);
+  Bl = int((long long)B * (rank + 1) / G) - lo;
+}
+
+static void split_common_checks(Engine& E, const ssd_sim_config* c, int G) {
+  validate_cfg(E, c);
+  if (G < 1) throw Fail(SSD_CONFIG, "split: at least one speculator");
+  if (int(E.peers.size()) != G + 1) throw Fail(SSD_CONFIG, "split: mailbox not connected to 1 verifier + G speculators");
+  if (E.V % 4) throw Fail(SSD_CONFIG, "split: vocabulary must be a multiple of 4");
+}
+
+ssd_status ssd_run_ssd_verifier(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c,
+                                int32_t n_spec, int32_t* out, int64_t cap, int64_t* out_len, int32_t* out_outcomes,
+                                ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (E.role != SSD_ROLE_VERIFIER) throw Fail(SSD_CONFIG, "run_ssd_verifier: engine role is not verifier");
+  need(E.T, "run_ssd_verifier");
+  split_common_checks(E, c, n_spec);
+  const int K = c->lookahead;
+  const int64_t R = c->rounds;
+  set_history(E, prompt, n0, int(n0 + R * (K + 1) + 2 * K + 2));
+  cudaStream_t s = E.sv;
+  // VerifierProcess streams: derive_seed(derive_seed(seed, 0x5EED), j) (sim.cpp:323-331)
+  reset_state(E, K, n0, R, 0, derive_seed(derive_seed(c->seed, 0x5EED), 0), c, s);
+  E.seq_base += int(R) + 2;
+  if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, s);
+  int* d_out = dalloc<int>(size_t(2 * R));
+  const float* rows = reinterpret_cast<const float*>(reinterpret_cast<const char*>(E.inbox) + kInboxRows);
+  E.launches = 0;
+  GraphSet gs;
+  gs.g.push_back(capture_graph(s, [&] {
+    recv_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, rows, E.V);
+    verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, s);
+    send_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.peers_dev + 1, n_spec, d_out);
+    commit_kernel<<<1, 32, 0, s>>>(E.st);
+    KCHECK();
+    E.launches += 3;
+  }));
+  const long long per_round = E.launches;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t r = 0; r < R; ++r) CK(cudaGraphLaunch(gs.g[0], s));
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  LoopState st = read_state(E);
+  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_out);
+  if (st.error == 10) {
+    Inbox ib;
+    CK(cudaMemcpy(&ib, E.inbox, sizeof(Inbox), cudaMemcpyDeviceToHost));
+    throw Fail(SSD_PROTOCOL_VIOLATION, "verifier: speculation message missing or out of order at round " +
+                                           std::to_string(st.round) + " (want seq " +
+                                           std::to_string(st.seq_base + st.round + 1) + ", inbox seq " +
+                                           std::to_string(ib.d2v.seq) + ")");
+  }
+  raise_device_error(st);
+  fill_stats(st, R, ms, per_round * R, stats);
+  copy_out(E, n0, st.n, out, cap, out_len);
+  API_END
+}
+
+ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c,
+                                  int32_t rank, int32_t n_spec, int32_t* out_hits, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (E.role != SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "run_ssd_speculator: engine role is not speculator");
+  need(E.D, "run_ssd_speculator");
+  split_common_checks(E, c, n_spec);
+  if (rank < 0 || rank >= n_spec) throw Fail(SSD_CONFIG, "run_ssd_speculator: rank out of range");
+  const int K = c->lookahead;
+  int B = 0, max_f = 0;
+  upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);
+  int lo = 0, Bl = 0;
+  branch_block(B, rank, n_spec, lo, Bl);
+  const int64_t R = c->rounds;
+  set_history(E, prompt, n0, int(n0 + R * (K + 1) + 2 * K + 2));
+  int* d_hit = dalloc<int>(size_t(R));
+  cudaStream_t s = E.sv;
+  // DraftProcess streams: derive_seed(seed, j) (sim.cpp:376-386); identical on every speculator
+  reset_state(E, K, n0, R, derive_seed(c->seed, 0), 0, c, s);
+  {  // every message of earlier runs counts as consumed (credit flow control, split.cuh)
+    const int run_base = E.seq_base;
+    CK(cudaMemcpyAsync(&E.inbox->credit.done, &run_base, sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  E.seq_base += int(R) + 2;
+  if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
+  Inbox** vpeers = E.peers_dev;  // [0] verifier, [1..G] speculators
+  const int send_blocks = 2 * E_num_sms;
+  // initial synchronous draft, clock starts at T_p (sim.cpp:524-526)
+  draft_steps(E, K, c->scheme, 0, 0, s);
+  {
+    LoopState tmp;
+    tmp.clock = c->primary_time;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, clock), &tmp.clock, sizeof(double),
+                       cudaMemcpyHostToDevice, s));
+  }
+  send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 1, E.send_counter);
+  KCHECK();
+  const bool jit = c->backup_kind == 0;
+  E.launches = 0;
+  GraphSet gs;
+  for (int parity = 0; parity < 2; ++parity) {
+    gs.g.push_back(capture_graph(s, [&] {
+      prespeculate(E, K, B, lo, Bl, max_f, c->scheme, parity, s);
+      recv_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, E.hist);
+      lookup_kernel<<<1, 32, 0, s>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, E.V, E.cum, nullptr,
+                                     d_hit);
+      send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 0, E.send_counter);
+      recv_peer_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox);
+      KCHECK();
+      E.launches += 4;
+    }));
+  }
+  const long long per_round = E.launches / 2;
+  long long jit_launches = 0;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(E.ev_t0, s));
+  for (int64_t r = 0; r < R; ++r) {
+    CK(cudaGraphLaunch(gs.g[size_t(r & 1)], s));
+    if (jit && r + 1 < R) {
+      CK(cudaStreamSynchronize(s));
+      int hit = 0;
+      CK(cudaMemcpy(&hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int), cudaMemcpyDeviceToHost));
+      if (!hit) {  // SamePrimaryJIT re-draft (sim.cpp:229-232), identical on every speculator; rank 0 sends
+        const long long before = E.launches;
+        draft_steps(E, K, c->scheme, 1, 2, s);
+        send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 1, E.send_counter);
+        KCHECK();
+        jit_launches += E.launches - before + 1;
+      }
+    }
+  }
+  CK(cudaEventRecord(E.ev_t1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
+  LoopState st = read_state(E);
+  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_hit);
+  if (st.error == 10) {
+    Inbox ib;
+    CK(cudaMemcpy(&ib, E.inbox, sizeof(Inbox), cudaMemcpyDeviceToHost));
+    throw Fail(SSD_PROTOCOL_VIOLATION,
+               "speculator " + std::to_string(rank) + ": message missing or out of order at round " +
+                   std::to_string(st.round) + " (base " + std::to_string(st.seq_base) + ", hit " +
+                   std::to_string(st.hit) + ", own " + std::to_string(st.own) + ", v2d seq " +
+                   std::to_string(ib.v2d[0].seq) + "/" + std::to_string(ib.v2d[1].seq) + ", peer seq " +
+                   std::to_string(ib.peer[0].seq) + "/" + std::to_string(ib.peer[1].seq) + ")");
+  }
+  raise_device_error(st);
+  fill_stats(st, R, ms, per_round * R + jit_launches, stats);
+  API_END
+}
+
 ssd_status ssd_logits(ssd_engine* h, int32_t which, const int32_t* ctx, int32_t n, float* out) {
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
-  set_history(E, ctx, n, n + 1);
   Model& m = which == 0 ? E.T : E.D;
+  need(m, "logits");
+  set_history(E, ctx, n, n + 1);
   prefill(E, m, n, E.tlogits, E.sv);
   CK(cudaStreamSynchronize(E.sv));
   CK(cudaMemcpy(out, E.tlogits, size_t(E.V) * 4, cudaMemcpyDeviceToHost));
@@ -1029,6 +1284,7 @@ ssd_status ssd_draft(ssd_engine* h, const int32_t* ctx, int32_t n, int32_t K, co
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
+  need(E.D, "draft");
   if (K < 1) throw Fail(SSD_ERROR, "draft: lookahead must be >= 1");
   if (K > E.maxK) throw Fail(SSD_TOO_LARGE, "draft: lookahead exceeds the engine's capacity");
   if (!sc) throw Fail(SSD_CONFIG, "draft: scheme required");
@@ -1051,6 +1307,7 @@ ssd_status ssd_build_cache(ssd_engine* h, const int32_t* ctx, int32_t n, const i
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
+  need(E.D, "build_cache");
   if (!plan || !sc) throw Fail(SSD_CONFIG, "build_cache: plan and scheme required");
   if (plan->lookahead != K) throw Fail(SSD_ERROR, "build_cache: plan length does not match speculation");
   if (next_K != K) throw Fail(SSD_CONFIG, "build_cache: the engine drafts continuations of the same lookahead");
@@ -1075,7 +1332,7 @@ ssd_status ssd_build_cache(ssd_engine* h, const int32_t* ctx, int32_t n, const i
                        cudaMemcpyHostToDevice, s));
   }
   if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
-  if (total > 0) prespeculate(E, K, B, max_f, *sc, 0, s);
+  if (total > 0) prespeculate(E, K, B, 0, B, max_f, *sc, 0, s);
   else branch_streams_kernel<<<1, 32, 0, s>>>(E.st, 0, E.bu, 0);
   CK(cudaStreamSynchronize(s));
   std::vector<int> bkh(static_cast<size_t>(B)), bth(static_cast<size_t>(B)), tt(static_cast<size_t>(B) * K);
@@ -1163,6 +1420,7 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   Model& m = which == 0 ? E.T : E.D;
+  need(m, "profile_forward");
   if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
   cudaStream_t s = E.sv;
   m.ctx_bound = pos + M + 1;

@@ -39,6 +39,8 @@ struct LoopState {
   int hit;           // last lookup
   int error;         // ssd_status raised on the device (0 = ok)
   int backup_kind;   // 0 SamePrimaryJIT, 1 FastRandom
+  int own;           // split speculator: the hit slot's branch is decoded here
+  int seq_base;      // split runs: mailbox sequence numbers of this run start above it
   int pad_;
   double clock;      // harness virtual clock
   double primary_time, backup_time;
@@ -876,8 +878,10 @@ __global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__
 // (sim.cpp:418-463) and the harness clock (sim.cpp:528-577).
 // cum: exact sequential fp64 cumulative of the uniform law (categorical.cpp
 // :133-138 on a vector of 1/V), for the FastRandom tokens (sim.cpp:35-48).
+// Branch sharding: this engine decodes branches [lo, lo + Bl)
+// of the B keyed ones; bt / brows hold only those ([Bl][K], [K][Bl][V]).
 __global__ void lookup_kernel(LoopState* st, const int* __restrict__ keys, int max_f, const int* __restrict__ off,
-                              const int* __restrict__ bt, const float* __restrict__ brows, int B, int V,
+                              const int* __restrict__ bt, const float* __restrict__ brows, int lo, int Bl, int V,
                               const double* __restrict__ cum, int* __restrict__ log_outcomes, int* __restrict__ log_hits) {
   if (threadIdx.x != 0) return;
   const int K = st->K;
@@ -906,13 +910,18 @@ __global__ void lookup_kernel(LoopState* st, const int* __restrict__ keys, int m
   if (log_hits) log_hits[r] = hit ? 1 : 0;
   st->hit = hit;
   if (hit) {
-    for (int i = 0; i < K; ++i) {
-      st->spec[i] = bt[b * K + i];
-      st->spec_rows[i] = brows + (size_t(i) * B + b) * size_t(V);
+    const int lb = b - lo;
+    st->own = lb >= 0 && lb < Bl;
+    if (st->own) {  // otherwise the owning speculator broadcasts the tokens
+      for (int i = 0; i < K; ++i) {
+        st->spec[i] = bt[lb * K + i];
+        st->spec_rows[i] = brows + (size_t(i) * Bl + lb) * size_t(V);
+      }
     }
     st->spec_origin = 0; st->spec_src = 1; st->spec_uniform = 0;
     st->clock = fmax(v1, ready);
   } else {
+    st->own = 0;
     st->spec_origin = 1; st->spec_src = 2;
     st->clock = v1 + st->backup_time;
     if (st->backup_kind == 1) {  // FastRandom: K uniform draws, exact CDF

@@ -1,0 +1,111 @@
+"""Split verifier / speculator processes on the GPU: one OS
+process per role, device mailboxes mapped by CUDA IPC, every message written
+by the sender's kernels. On the 1-GPU box all processes share cuda:0 (the
+IPC / peer-memory path is the same one NVLink peers use). The split run must
+reproduce the colocated harness run (itself pinned to the CPU oracle's
+run_protocol_harness in test_gpu_parity.py) token for token and counter for
+counter, for every speculator count."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+ROUNDS = 8
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cfg(P, temperature, backup):
+    return P.SimConfig(lookahead=4, scheme=P.SamplingScheme.standard(temperature),
+                       primary_plan=P.FanOutPlan([3, 3, 2, 2, 2], P.PRIMARY),
+                       backup_plan=P.FanOutPlan([3, 3, 2, 2, 2], P.BACKUP), primary_time=0.4,
+                       backup_kind=backup, rounds=ROUNDS, seed=5)
+
+
+def _prompt():
+    return np.random.default_rng(11).integers(0, 32000, 10).tolist()
+
+
+def _worker(rank, world, port, temperature, backup, runs, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2603_03251_b200 as P
+        from paper_2603_03251_b200.configs import shapes
+        from paper_2603_03251_b200.split import SplitEngine
+        ts, ds = shapes("tiny", max_ctx=512)
+        se = SplitEngine(ts, ds, P.Pair(), device=0, max_branches=16, max_lookahead=4)
+        out = []
+        for _ in range(runs):  # repeated runs reuse the mapped mailboxes (monotonic sequence numbers)
+            r = se.run(_prompt(), _cfg(P, temperature, backup))
+            out.append((r.tokens, r.merged, None if r.stats.hits is None else r.stats.hits.tolist()))
+        se.close()
+        q.put((rank, "ok", out))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, f"{type(e).__name__}: {e}", None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _split(world, temperature, backup, runs=1):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, temperature, backup, runs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, status, out = q.get(timeout=600)
+        res[rank] = (status, out)
+    for p in procs:
+        p.join(timeout=120)
+    bad = {r: res[r][0] for r in range(world) if res[r][0] != "ok"}
+    assert not bad, bad
+    return res
+
+
+@pytest.fixture(scope="module")
+def colocated():
+    import paper_2603_03251_b200 as P
+    from paper_2603_03251_b200.configs import shapes
+    ts, ds = shapes("tiny", max_ctx=512)
+    eng = P.Engine(ts, ds, P.Pair(), max_branches=16, max_lookahead=4)
+    cache = {}
+
+    def run(temperature, backup):
+        key = (temperature, backup)
+        if key not in cache:
+            cache[key] = eng.run_ssd(_prompt(), _cfg(P, temperature, backup))
+        return cache[key]
+    yield run
+    eng.close()
+
+
+@pytest.mark.parametrize("world,temperature,backup", [
+    (2, 0.0, "fast_random"), (2, 1.0, "fast_random"), (2, 0.0, "same_primary_jit"),
+    (3, 0.0, "fast_random"), (3, 1.0, "fast_random"), (4, 0.0, "fast_random"), (4, 0.0, "same_primary_jit")])
+def test_split_run_matches_colocated_harness(colocated, world, temperature, backup):
+    res = _split(world, temperature, backup, runs=2)
+    ref = colocated(temperature, backup)
+    tokens, merged, _ = res[0][1][0]
+    assert tokens == ref.streams[0]
+    for f in ("tokens", "accepted_sum", "primary_origin_lookups", "primary_origin_hits", "backup_origin_lookups",
+              "backup_origin_hits", "hit_rounds", "miss_rounds", "hit_round_tokens", "miss_round_tokens"):
+        assert merged[f] == getattr(ref, f), f
+    assert abs(merged["virtual_time"] - ref.virtual_time) < 1e-9
+    # speculator hit logs agree with the colocated lookups, on every speculator
+    for rank in range(1, world):
+        assert res[rank][1][0][2] == ref.hits.tolist()
+    # a second run over the same mapped mailboxes is identical
+    assert res[0][1][1][0] == tokens
