@@ -20,6 +20,7 @@
 
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
+#include "fwd_mk.cuh"
 #include "kernels.cuh"
 #include "probe.cuh"
 #include "rowops.cuh"
@@ -83,7 +84,8 @@ static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint
 struct WMat {
   bf16* w = nullptr;
   int N = 0, K = 0;
-  const WMat* next = nullptr;  // the GEMM that follows in a forward (L2 prefetch)
+  long long off = 0;           // byte offset in the model's weight arena (forward order)
+  long long bytes = 0;         // padded bytes streamed
 };
 
 static long long gemm_units(const WMat& W) {
@@ -142,11 +144,21 @@ struct Model {
   float *dlt1 = nullptr, *dlt2 = nullptr;  // attention / MLP projections (residual deltas)
   bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
   int64_t weight_bytes = 0;
+  const char* arena = nullptr;  // every GEMM weight, contiguous in forward order (L2 prefetch stream)
+  long long arena_bytes = 0;
   float* ws = nullptr;   // split-K partials
   size_t ws_floats = 0;
   int* counters = nullptr;
   std::vector<ActMap> amaps;
   std::vector<void*> owned;
+  // persistent forward kernel (fwd_mk.cuh)
+  mk::Op* mk_ops[2] = {nullptr, nullptr};  // [0] without, [1] with the LM head
+  int mk_nops[2] = {0, 0};
+  mk::LayerKV* mk_kv = nullptr;
+  float* mk_sumsq = nullptr;                // [d / 128][maxM]
+  unsigned* mk_bar = nullptr;
+  int mk_ctas = 0;                          // CTAs (SMs) of its launches; 0 = all
+  int gemm_ctas = 0;                        // cap on a GEMM's CTAs (0 = every SM)
 
   size_t kv_layer_elems() const { return size_t(s.n_kv_heads) * size_t(S) * size_t(s.head_dim); }
 };
@@ -178,6 +190,22 @@ struct Engine {
   std::vector<void*> owned;
   long long launches = 0;
   int skip_mask = 0;  // profiling only (SSD_B200_SKIP): drop norms / attention
+  long long pf_ahead = 32LL << 20;  // L2 prefetch look-ahead of the weight stream (SSD_B200_PF_MB)
+  // Persistent forward kernel (fwd_mk.cuh) for M <= 64: SSD_B200_MK=1. Off by
+  // default: measured slower than the per-op PDL chain (profiles/r01_summary.md:
+  // tcgen05 at N <= 32 consumes a 32 KB unit per ~0.77 us per SM, i.e. no faster
+  // than HBM, so the phase barriers / attention latency it exposes are never
+  // caught up).
+  int use_mk = 0;
+  long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
+  // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
+  // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
+  // 0 = all SMs, the default: no partition measured faster, profiles/)
+  int split_t = 0, split_d = 0;
+  unsigned long long* mk_trace = nullptr;  // debug timeline buffer (ssd_debug_mk_trace)
+  int mk_pf_units = 0;  // L2 look-ahead of the persistent kernel's weight stream (SSD_B200_MK_PF)
+  unsigned long long* mk_utrace = nullptr;
+  int mk_utrace_op[4] = {-1, -1, -1, -1};
   // split processes (split.cuh)
   int role = 0;                      // 0 colocated, 1 verifier, 2 speculator
   Inbox* inbox = nullptr;            // this process's mailbox (+ draft rows)
@@ -232,12 +260,34 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
     if (K % (tc::kBK * tc::kKPS)) throw Fail(SSD_CONFIG, "engine: every GEMM K must be a multiple of 128");
     w.N = N;
     w.K = K;
-    if (!w.w) w.w = static_cast<bf16*>(own(dalloc<bf16>(padded(N) * K)));
+    w.bytes = (long long)padded(N) * K * 2;
   };
+  // Weight arena: every GEMM's pre-tiled weights back to back in the order a
+  // forward streams them (qkv, o, gate/up, down per layer, then the LM head),
+  // so "the next X bytes of the stream" is one address range (L2 prefetch
+  // windows, forward()).
+  m.layers.resize(size_t(s.n_layers));
+  for (int l = 0; l < s.n_layers; ++l) {
+    DevLayer& L = m.layers[size_t(l)];
+    wmat(L.qkv, m.qd + 2 * m.kvd, d);
+    wmat(L.o, d, m.qd);
+    wmat(L.gu, 2 * s.ffn, d);
+    wmat(L.dn, d, s.ffn);
+  }
+  wmat(m.head, s.vocab, d);
+  {
+    long long at = 0;
+    auto place = [&](WMat& w) { w.off = at; at += (w.bytes + 1023) / 1024 * 1024; };
+    for (DevLayer& L : m.layers) { place(L.qkv); place(L.o); place(L.gu); place(L.dn); }
+    place(m.head);
+    m.arena_bytes = at;
+    char* base = static_cast<char*>(own(dalloc<char>(size_t(at))));
+    m.arena = base;
+    for (DevLayer& L : m.layers)
+      for (WMat* w : {&L.qkv, &L.o, &L.gu, &L.dn}) w->w = reinterpret_cast<bf16*>(base + w->off);
+    m.head.w = reinterpret_cast<bf16*>(base + m.head.off);
+  }
   // tables: the LM head is pre-tiled for the GEMM; a tied table is both
-  m.head.N = s.vocab;
-  m.head.K = d;
-  m.head.w = static_cast<bf16*>(own(dalloc<bf16>(padded(s.vocab) * d)));
   gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, s.tied ? 0 : 1, 1);
   KCHECK();
   if (s.tied) {
@@ -269,14 +319,9 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   CK(cudaMemcpy(m.final_gain, fg.data(), fg.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(m.ffn_gain0, g0.data(), g0.size() * 4, cudaMemcpyHostToDevice));
   // layers: fused QKV [q; k; v], interleaved gate/up rows (2j gate, 2j+1 up)
-  m.layers.resize(size_t(s.n_layers));
   int64_t wb = 0;
   for (int l = 0; l < s.n_layers; ++l) {
     DevLayer& L = m.layers[size_t(l)];
-    wmat(L.qkv, m.qd + 2 * m.kvd, d);
-    wmat(L.o, d, m.qd);
-    wmat(L.gu, 2 * s.ffn, d);
-    wmat(L.dn, d, s.ffn);
     gen_launch(L.qkv.w, m.qd, d, 1, 0, s, dr, gp, role, l, 0);
     gen_launch(L.qkv.w, m.kvd, d, 1, m.qd, s, dr, gp, role, l, 1);
     gen_launch(L.qkv.w, m.kvd, d, 1, m.qd + m.kvd, s, dr, gp, role, l, 2);
@@ -287,16 +332,6 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
     wb += int64_t(m.qd + 2 * m.kvd) * d + int64_t(d) * m.qd + int64_t(2 * s.ffn) * d + int64_t(d) * s.ffn;
   }
   wb += int64_t(s.vocab) * d;  // LM head
-  // forward order of the GEMMs: each one L2-prefetches the next one's first
-  // stages (qkv -> o -> gate/up -> down -> next layer ... -> head -> layer 0)
-  for (int l = 0; l < s.n_layers; ++l) {
-    DevLayer& L = m.layers[size_t(l)];
-    L.qkv.next = &L.o;
-    L.o.next = &L.gu;
-    L.gu.next = &L.dn;
-    L.dn.next = l + 1 < s.n_layers ? &m.layers[size_t(l + 1)].qkv : &m.head;
-  }
-  m.head.next = &m.layers[0].qkv;
   m.weight_bytes = wb * 2;
   // KV cache
   m.S = s.max_ctx + branch_slots;
@@ -332,6 +367,38 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
     m.attn_part = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.n_kv_heads * chunks * G * (hd + 2))));
     m.attn_cnt = static_cast<int*>(own(dalloc<int>(size_t(maxM) * s.n_kv_heads)));
   }
+  // persistent forward kernel: op lists (with / without the LM head), KV table
+  {
+    std::vector<mk::Op> ops;
+    auto gemm_op = [&](int kind, int l, const WMat& w) {
+      ops.push_back(mk::Op{kind, l, w.w, w.N, w.K / (tc::kBK * tc::kKPS), 0});
+    };
+    ops.push_back(mk::Op{mk::OP_EMBED, 0, nullptr, 0, 0, 0});
+    for (int l = 0; l < s.n_layers; ++l) {
+      const DevLayer& L = m.layers[size_t(l)];
+      ops.push_back(mk::Op{mk::OP_NORM, l, nullptr, 0, 0, 0});
+      gemm_op(mk::OP_QKV, l, L.qkv);
+      ops.push_back(mk::Op{mk::OP_ATTN, l, nullptr, 0, 0, 0});
+      gemm_op(mk::OP_O, l, L.o);
+      ops.push_back(mk::Op{mk::OP_NORM, l, nullptr, 0, 0, l == 0 ? 1 : 0});
+      gemm_op(mk::OP_GU, l, L.gu);
+      gemm_op(mk::OP_DN, l, L.dn);
+    }
+    m.mk_nops[0] = int(ops.size());
+    ops.push_back(mk::Op{mk::OP_NORM, s.n_layers, nullptr, 0, 0, 2});
+    gemm_op(mk::OP_HEAD, s.n_layers, m.head);
+    m.mk_nops[1] = int(ops.size());
+    m.mk_ops[1] = static_cast<mk::Op*>(own(dalloc<mk::Op>(ops.size())));
+    CK(cudaMemcpy(m.mk_ops[1], ops.data(), ops.size() * sizeof(mk::Op), cudaMemcpyHostToDevice));
+    m.mk_ops[0] = m.mk_ops[1];  // same list, one op shorter
+    std::vector<mk::LayerKV> kv(static_cast<size_t>(s.n_layers));
+    for (int l = 0; l < s.n_layers; ++l)
+      kv[size_t(l)] = mk::LayerKV{m.kc + size_t(l) * m.kv_layer_elems(), m.vc + size_t(l) * m.kv_layer_elems()};
+    m.mk_kv = static_cast<mk::LayerKV*>(own(dalloc<mk::LayerKV>(kv.size())));
+    CK(cudaMemcpy(m.mk_kv, kv.data(), kv.size() * sizeof(mk::LayerKV), cudaMemcpyHostToDevice));
+    m.mk_sumsq = static_cast<float*>(own(dalloc<float>(size_t(d / tc::kBM + 1) * maxM)));
+    m.mk_bar = static_cast<unsigned*>(own(dalloc<unsigned>(2)));
+  }
 }
 
 static int E_num_sms = 148;
@@ -349,10 +416,10 @@ static const CUtensorMap& act_map(Model& m, const void* X, int K, int np) {
   return m.amaps.back().map;
 }
 
-template <int EPI, int NP>
+template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                           cudaStream_t s) {
-  using C = tc::Cfg<NP>;
+                           cudaStream_t s, Prefetch pf) {
+  using C = tc::Cfg<NP, BUDGET_KB>;
   const int tiles = (W.N + tc::kBM - 1) / tc::kBM;
   const int KU = W.K / (tc::kBK * tc::kKPS);
   const int units = tiles * KU;
@@ -361,22 +428,19 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
 // it and prefetches its weights (PDL) while this one drains.
 #define SSD_GEMM_CTAS_PER_SM 1
 #endif
-  const int grid = std::min(units, E_num_sms * SSD_GEMM_CTAS_PER_SM);
+  const int cap = m.gemm_ctas > 0 ? std::min(m.gemm_ctas, E_num_sms) : E_num_sms * SSD_GEMM_CTAS_PER_SM;
+  const int grid = std::min(units, cap);
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
-  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, nullptr, 0, 0};
-  if (W.next) {
-    g.nextW = W.next->w;
-    g.nextU = gemm_units(*W.next);
-    g.nextP = int(std::min<long long>(g.nextU, E_num_sms * SSD_GEMM_CTAS_PER_SM));
-  }
-  launch_pdl(tc::gemm_tc_kernel<EPI, NP>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP), g);
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf};
+  launch_pdl(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP),
+             g);
 }
 
-template <int EPI, int NP>
+template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 static void configure_gemm() {
-  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(tc::Cfg<NP>::kSmem)));
-  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(tc::Cfg<NP, BUDGET_KB>::kSmem)));
+  CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           int(cudaSharedmemCarveoutMaxShared)));
 }
 
@@ -386,6 +450,12 @@ template <typename F>
 static void carveout_max(F* f) {
   CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributePreferredSharedMemoryCarveout,
                           int(cudaSharedmemCarveoutMaxShared)));
+}
+
+template <int NP, int G>
+static void mk_configure() {
+  CK(cudaFuncSetAttribute(mk::fwd_kernel<NP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(mk::Cfg<NP, G>::kSmem)));
 }
 
 // Kernel attributes are set once, outside any stream capture.
@@ -419,6 +489,11 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 128>(); configure_gemm<EPI_SWIGLU, 128>();
   configure_gemm<EPI_STORE, 192>(); configure_gemm<EPI_SWIGLU, 192>();
   configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
+  configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
+  configure_gemm<EPI_STORE, 32, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 32, tc::kSmallBudgetKB>();
+  mk_configure<16, 1>(); mk_configure<16, 2>(); mk_configure<16, 4>(); mk_configure<16, 8>();
+  mk_configure<32, 1>(); mk_configure<32, 2>(); mk_configure<32, 4>(); mk_configure<32, 8>();
+  mk_configure<64, 1>(); mk_configure<64, 2>(); mk_configure<64, 4>(); mk_configure<64, 8>();
 }
 
 // Stream capture of one round / step into an executable graph. All kernel
@@ -454,17 +529,70 @@ struct GraphSet {
 // (M = 1 decode steps pad the token operand to 16).
 template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                   cudaStream_t s) {
+                   cudaStream_t s, Prefetch pf) {
   ++E.launches;
-  if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 64) gemm_tc_launch<EPI, 64>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 96) gemm_tc_launch<EPI, 96>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 128) gemm_tc_launch<EPI, 128>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else if (M <= 192) gemm_tc_launch<EPI, 192>(m, W, X, M, Y, ldy, Yb, ldyb, s);
-  else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s);
+  // small weight matrices: the co-resident (small-budget) configuration
+  if (W.bytes <= E.small_gemm_bytes && M <= 32) {
+    if (M <= 16) gemm_tc_launch<EPI, 16, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    else gemm_tc_launch<EPI, 32, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    return;
+  }
+  if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 64) gemm_tc_launch<EPI, 64>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 96) gemm_tc_launch<EPI, 96>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 128) gemm_tc_launch<EPI, 128>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else if (M <= 192) gemm_tc_launch<EPI, 192>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
 }
+
+// L2 prefetch cursor over the GEMM sequence of one forward: the stream
+// position is (GEMM index, fraction of every stream-K range consumed), and
+// each kernel extends the prefetched frontier to (start of the next GEMM it
+// feeds + the look-ahead distance in bytes). Windows are baked into the
+// kernels' arguments (and so into captured graphs).
+struct PfCursor {
+  std::vector<const WMat*> seq;  // GEMMs in forward order
+  long long ahead;
+  int gi = 0;        // frontier: GEMM index ...
+  double frac = 0;   // ... and fraction of its ranges already prefetched
+  PfCursor(const Model& m, long long a, bool head) : ahead(a) {
+    cap = m.gemm_ctas > 0 ? std::min(m.gemm_ctas, E_num_sms) : E_num_sms * SSD_GEMM_CTAS_PER_SM;
+    for (const DevLayer& L : m.layers)
+      for (const WMat* w : {&L.qkv, &L.o, &L.gu, &L.dn}) seq.push_back(w);
+    if (head) seq.push_back(&m.head);
+  }
+  int cap = 0;
+  int parts(const WMat& w) const { return int(std::min<long long>(gemm_units(w), cap)); }
+  // Window up to `ahead` bytes past the start of GEMM `next` (index in seq).
+  Prefetch upto(int next) {
+    Prefetch p{};
+    p.n = 0;
+    if (ahead <= 0) return p;
+    int tg = next;
+    double tf = 0;
+    long long left = ahead;
+    while (tg < int(seq.size()) && left > 0) {
+      const long long b = seq[size_t(tg)]->bytes;
+      if (left >= b) { left -= b; ++tg; }
+      else { tf = double(left) / double(b); left = 0; }
+    }
+    while ((gi < tg || (gi == tg && frac < tf)) && gi < int(seq.size()) && p.n < kPfSegs) {
+      const WMat& w = *seq[size_t(gi)];
+      const double end = gi < tg ? 1.0 : tf;
+      p.seg[p.n++] = PfSeg{reinterpret_cast<const char*>(w.w), int(gemm_units(w)), parts(w), float(frac), float(end)};
+      if (gi < tg) { ++gi; frac = 0; } else { frac = tf; }
+    }
+    return p;
+  }
+  // Window of GEMM g itself (issued after its own stream): g's bytes are
+  // already loaded by g, so the frontier starts at GEMM g + 1 at the latest.
+  Prefetch after(int g) {
+    if (gi <= g) { gi = g + 1; frac = 0; }
+    return upto(g + 1);
+  }
+};
 
 // Key chunks of the split attention for the current context bound.
 static int attn_chunks(const Model& m) {
@@ -472,15 +600,79 @@ static int attn_chunks(const Model& m) {
   return std::max(1, (nk + kAttnChunk - 1) / kAttnChunk);
 }
 
+// Persistent forward kernel launch (fwd_mk.cuh): the whole step in one
+// cooperative launch (all CTAs co-resident: grid barriers).
+template <int NP, int G>
+static void mk_launch(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
+  using C = mk::Cfg<NP, G>;
+  const ssd_model_shape& sh = m.s;
+  const int grid = m.mk_ctas > 0 ? std::min(m.mk_ctas, E_num_sms) : E_num_sms;
+  if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "forward: split-K workspace");
+  mk::MkArgs a{};
+  a.ops = m.mk_ops[logits ? 1 : 0];
+  a.n_ops = m.mk_nops[logits ? 1 : 0];
+  a.M = M;
+  a.P = P;
+  a.d = sh.d_model; a.H = sh.n_heads; a.KVH = sh.n_kv_heads; a.hd = sh.head_dim; a.ffn = sh.ffn; a.V = sh.vocab;
+  a.S = m.S; a.nqkv = m.qd + 2 * m.kvd; a.qd = m.qd;
+  a.eps = sh.norm_eps;
+  a.scale = 1.0f / std::sqrt(float(sh.head_dim));
+  a.embed = m.embed; a.embed_tiled = m.embed_tiled;
+  a.gain_ffn0 = m.ffn_gain0; a.gain_final = m.final_gain;
+  a.rope_cos = m.rope_cos; a.rope_sin = m.rope_sin;
+  a.kv = m.mk_kv;
+  a.x = m.x; a.sumsq = m.mk_sumsq; a.ld_sumsq = m.maxM;
+  a.qkv = m.qkv; a.attn = m.attn; a.act = m.act; a.logits = logits;
+  a.ws = m.ws; a.counters = m.counters;
+  a.aws = AttnWs{m.attn_part, m.attn_cnt};
+  a.nch = attn_chunks(m);
+  a.bar = m.mk_bar;
+  a.trace = E.mk_trace;
+  a.xb = m.xb;
+  a.pf_units = E.mk_pf_units;
+  a.utrace = E.mk_utrace;
+  for (int j = 0; j < 4; ++j) a.utrace_op[j] = E.mk_utrace_op[j];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(mk::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, mk::fwd_kernel<NP, G>, act_map(m, m.attn, m.qd, NP), act_map(m, m.act, sh.ffn, NP),
+                        act_map(m, m.xb, sh.d_model, NP), a));
+}
+
+template <int NP>
+static void mk_launch_g(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
+  switch (m.s.n_heads / m.s.n_kv_heads) {
+    case 1: mk_launch<NP, 1>(E, m, P, M, logits, s); break;
+    case 2: mk_launch<NP, 2>(E, m, P, M, logits, s); break;
+    case 4: mk_launch<NP, 4>(E, m, P, M, logits, s); break;
+    default: mk_launch<NP, 8>(E, m, P, M, logits, s); break;
+  }
+}
+
 // One forward step of `m` over the M tokens described by P. Logits of all M
 // rows go to `logits` ([M][V]) when non-null. Every kernel is launched with
 // PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
+  if (E.use_mk && M <= 64) {  // decode / verify / branch steps and prefill chunks: one persistent launch
+    if (M <= 16) mk_launch_g<16>(E, m, P, M, logits, s);
+    else if (M <= 32) mk_launch_g<32>(E, m, P, M, logits, s);
+    else mk_launch_g<64>(E, m, P, M, logits, s);
+    ++E.launches;
+    return;
+  }
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, H = sh.n_heads, KVH = sh.n_kv_heads, hd = sh.head_dim, F = sh.ffn;
   const int nqkv = m.qd + 2 * m.kvd;
-  launch_pdl(embed_kernel, dim3(M), dim3(256), 0, s, (const bf16*)m.embed, d, m.embed_tiled, P, m.x);
+  PfCursor pf(m, E.pf_ahead, logits != nullptr);
+  launch_pdl(embed_kernel, dim3(M), dim3(256), 0, s, (const bf16*)m.embed, d, m.embed_tiled, P, m.x, pf.upto(0));
   ++E.launches;
   const float scale = 1.0f / std::sqrt(float(hd));
   const int nch = attn_chunks(m);
@@ -494,26 +686,26 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
     // x += (previous layer's down projection); xb = norm(x)
     if (do_norm)
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
-                 (const float*)nullptr, sh.norm_eps, m.xb);
-    linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
+                 (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
+    linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
     if (do_attn) {
       auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
       launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
-                 (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws);
+                 (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws, pf.upto(4 * l + 1));
     }
-    linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
     // x += attention projection; xb = norm(x) * g
     if (do_norm)
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
-                 (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb);
-    linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
-    linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s);
+                 (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb, pf.upto(4 * l + 2));
+    linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s, pf.after(4 * l + 2));
+    linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
     E.launches += 3;
   }
   if (logits) {
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt2, d,
-               (const float*)m.final_gain, sh.norm_eps, m.xb);
-    linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s);
+               (const float*)m.final_gain, sh.norm_eps, m.xb, pf.upto(4 * sh.n_layers));
+    linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
     ++E.launches;
   }
 }
@@ -740,6 +932,25 @@ static void validate_cfg(Engine& E, const ssd_sim_config* c) {
 
 using namespace ssd;
 
+namespace ssd {
+// Watchdog record of the persistent forward kernel (fwd_mk.cuh): [0] set,
+// [1] code (1 weight producer empty, 2 MMA tmem-empty, 3 MMA full,
+// 4 B producer empty, 5 epilogue tmem-full, 9 grid barrier), [2] block,
+// [3] thread, [4..5] aux (op, counter). Host-mapped: valid after a trap.
+unsigned long long* g_diag_host = nullptr;
+static void mk_diag_init() {
+  if (g_diag_host) return;
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&g_diag_host), (8 + 8 * 256) * sizeof(unsigned long long),
+                   cudaHostAllocMapped));
+  std::memset(g_diag_host, 0, (8 + 8 * 256) * sizeof(unsigned long long));
+  unsigned long long* dptr = nullptr;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), g_diag_host, 0));
+  CK(cudaMemcpyToSymbol(mk::g_mk_diag, &dptr, sizeof(dptr)));
+  const int prog = std::getenv("SSD_B200_MK_PROGRESS") ? std::atoi(std::getenv("SSD_B200_MK_PROGRESS")) : 0;
+  CK(cudaMemcpyToSymbol(mk::g_mk_progress, &prog, sizeof(prog)));
+}
+}  // namespace ssd
+
 struct ssd_engine {
   Engine e;
 };
@@ -791,6 +1002,11 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
   E.V = target->vocab;
   E.role = role;
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
+  if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
+  if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
+  if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
+  if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
+  if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
   {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -807,6 +1023,7 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
     if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
       throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
   configure_kernels();
+  mk_diag_init();
   CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
@@ -1012,6 +1229,13 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
   // branch-row buffers (the next round's verifier reads this round's rows).
   E.launches = 0;
   GraphSet gs;
+  // verifier and speculator GEMMs on disjoint SM sets so both streams run at once
+  E.T.gemm_ctas = E.split_t;
+  E.D.gemm_ctas = E.split_d;
+  struct Uncap {
+    Engine& e;
+    ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; }
+  } uncap{E};
   for (int parity = 0; parity < 2; ++parity) {
     gs.g.push_back(capture_graph(sv, [&] {
       CK(cudaEventRecord(E.ev_fork, sv));
@@ -1429,14 +1653,15 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, F = sh.ffn, nqkv = m.qd + 2 * m.kvd;
   auto gemms = [&]() {
+    PfCursor pf(m, E.pf_ahead, true);
     for (int l = 0; l < sh.n_layers; ++l) {
       const DevLayer& L = m.layers[size_t(l)];
-      linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s);
-      linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s);
-      linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s);
-      linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s);
+      linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
+      linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
+      linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s, pf.after(4 * l + 2));
+      linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
     }
-    linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits, sh.vocab, nullptr, 0, s);
+    linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
   };
   forward(E, m, E.P_pre, M, m.logits, s);  // warm
   gemms();
@@ -1515,6 +1740,50 @@ extern "C" int ssd_debug_gemm_trace(unsigned long long* out /* 5 x 512 */) {
   return int(cudaMemcpyFromSymbol(out, tc::g_trace, sizeof(unsigned long long) * 5 * 512));
 }
 #endif
+
+// Debug timeline of one persistent forward of `which` over M tokens at
+// position pos: out[(op * grid + cta) * 4 + k] (ns, see fwd_mk.cuh mk_trace);
+// returns the op count; kinds[op] = op kind.
+int ssd_debug_mk_trace(ssd_engine* h, int which, int M, int pos, unsigned long long* out, int cap, int* kinds,
+                       const int* utrace_ops, unsigned long long* uout) {
+  try {
+    Engine& E = h->e;
+    CK(cudaSetDevice(E.dev));
+    Model& m = which == 0 ? E.T : E.D;
+    const int nops = m.mk_nops[1];
+    const size_t n = size_t(nops) * E_num_sms * 4;
+    if (size_t(cap) < n) return -2;
+    m.ctx_bound = pos + M + 1;
+    prep_prefill_kernel<<<1, kMaxM, 0, E.sv>>>(E.hist, E.P_pre, pos, M);
+    forward(E, m, E.P_pre, M, m.logits, E.sv);  // warm
+    CK(cudaMalloc(&E.mk_trace, n * 8));
+    CK(cudaMemset(E.mk_trace, 0, n * 8));
+    CK(cudaMalloc(&E.mk_utrace, 4 * 64 * 4 * 8));
+    CK(cudaMemset(E.mk_utrace, 0, 4 * 64 * 4 * 8));
+    for (int j = 0; j < 4; ++j) E.mk_utrace_op[j] = utrace_ops ? utrace_ops[j] : -1;
+    forward(E, m, E.P_pre, M, m.logits, E.sv);
+    CK(cudaStreamSynchronize(E.sv));
+    CK(cudaMemcpy(out, E.mk_trace, n * 8, cudaMemcpyDeviceToHost));
+    if (uout) CK(cudaMemcpy(uout, E.mk_utrace, 4 * 64 * 4 * 8, cudaMemcpyDeviceToHost));
+    cudaFree(E.mk_trace);
+    cudaFree(E.mk_utrace);
+    E.mk_trace = nullptr;
+    E.mk_utrace = nullptr;
+    std::vector<mk::Op> ops(static_cast<size_t>(nops));
+    CK(cudaMemcpy(ops.data(), m.mk_ops[1], size_t(nops) * sizeof(mk::Op), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nops; ++i) kinds[i] = ops[size_t(i)].kind;
+    return nops;
+  } catch (const std::exception& x) {
+    g_last_error = x.what();
+    return -1;
+  }
+}
+
+int ssd_debug_mk_diag(unsigned long long* out /* 8 + 8 * 256 */) {
+  if (!g_diag_host) return -1;
+  std::memcpy(out, g_diag_host, (8 + 8 * 256) * sizeof(unsigned long long));
+  return 0;
+}
 
 ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {
   API_BEGIN

@@ -77,6 +77,7 @@ constexpr int kKPS = SSD_GEMM_KPS;          // k-blocks per pipeline stage
 constexpr int kABlock = kBM * kBK * 2;      // 16 KB
 constexpr int kABytes = kABlock * kKPS;
 constexpr int kThreads = 192;   // 6 warps
+static_assert(kABytes == kPfUnitBytes, "prefetch windows assume 32 KB units");
 // Stage budget per CTA; the host launches enough CTAs per SM to fill it.
 constexpr int kSmemBudget = SSD_GEMM_SMEM_KB * 1024;
 
@@ -204,12 +205,10 @@ struct GemmArgs {
   int ldyb;
   float* ws;      // partials [2 * gridDim][M][128]
   int* counters;  // per-tile arrival counters (zeroed, self-resetting)
-  // The next GEMM of the forward (nullptr = none): once this CTA's weight
-  // stream is issued, it prefetches into L2 the first units that the same
-  // CTA index will stream in the next GEMM, hiding that kernel's cold start.
-  const bf16* nextW;
-  long long nextU;  // next GEMM's units
-  int nextP;        // next GEMM's grid size
+  // L2 prefetch window of the weight stream ahead of this GEMM (kernels.cuh
+  // prefetch_window), issued once this CTA's own weight stream is issued:
+  // it covers the drain / epilogue / next-launch gap.
+  Prefetch pf;
 };
 
 template <int EPI>
@@ -237,22 +236,30 @@ __device__ __forceinline__ int cta_of(int u, long long U, long long P) {
   return int(i);
 }
 
-template <int NP>
+// BUDGET_KB: shared-memory stage budget. The full budget (one CTA per SM,
+// ~190 KB in flight) streams large GEMMs at HBM speed; the small budget
+// (kSmallBudgetKB) lets the next GEMM's CTA be resident beside the current
+// one, so under PDL it launches, allocates and starts its weight stream
+// while the current one drains (what the small per-layer GEMMs of a 1B
+// draft step are bound by).
+constexpr int kSmallBudgetKB = 108;
+template <int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 struct Cfg {
+  static constexpr int kBudget = BUDGET_KB * 1024;
   static constexpr int kBBlock = NP * kBK * 2;
   static constexpr int kBBytes = kBBlock * kKPS;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (kSmemBudget / kStageBytes) < 2 ? 2
-                                 : ((kSmemBudget / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
-                                                                                      : kSmemBudget / kStageBytes);
+  static constexpr int kStages = (kBudget / kStageBytes) < 2 ? 2
+                                 : ((kBudget / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
+                                                                                  : kBudget / kStageBytes);
   static constexpr int kAccCols = NP < 32 ? 32 : NP;
   static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + 256;
 };
 
-template <int EPI, int NP>
+template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
-  using C = Cfg<NP>;
+  using C = Cfg<NP, BUDGET_KB>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -324,15 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #endif
       TRACE(0, i);
     }
-    if (g.nextW != nullptr && blockIdx.x < g.nextP) {
-      const long long b0 = (long long)blockIdx.x * g.nextU / g.nextP;
-      const long long b1 = (long long)(blockIdx.x + 1) * g.nextU / g.nextP;
-      const long long k = (b1 - b0) < S ? (b1 - b0) : S;
-      if (k > 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.nextW + size_t(b0) * (kABytes / 2)),
-                     "r"(uint32_t(k * kABytes))
-                     : "memory");
-    }
+    prefetch_window(g.pf, kABytes);
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
@@ -411,19 +410,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           __threadfence();
           // only the first contributing CTA can start before the tile
           const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KU ? 0 : 1);
-          for (int t0 = 0; t0 < g.M; t0 += 8) {
-            float acc[8];
+          // All partial loads of a (16 contributors x 4 tokens) block are in
+          // flight together (one L2 round trip instead of one per
+          // contributor), then summed in CTA order: the same order, hence the
+          // same bits, as a sequential reduction.
+          constexpr int kC = 16, kT = 4;
+          for (int t0 = 0; t0 < g.M; t0 += kT) {
+            float acc[kT];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-            for (int c2 = cf; c2 <= cl; ++c2) {
-              const int slot = c2 == cf ? first_slot : 2 * c2;
-              const float* src = g.ws + (size_t(slot) * g.M) * kBM + rl;
+            for (int j = 0; j < kT; ++j) acc[j] = 0.f;
+            for (int cb = cf; cb <= cl; cb += kC) {
+              float v[kC][kT];
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (t0 + j < g.M) acc[j] += __ldcg(src + size_t(t0 + j) * kBM);
+              for (int i = 0; i < kC; ++i) {
+                const int c2 = cb + i;
+                const int slot = c2 == cf ? first_slot : 2 * c2;
+                const float* src = g.ws + (size_t(slot) * g.M) * kBM + rl;
+#pragma unroll
+                for (int j = 0; j < kT; ++j)
+                  v[i][j] = (c2 <= cl && t0 + j < g.M) ? __ldcg(src + size_t(t0 + j) * kBM) : 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < kC; ++i)
+#pragma unroll
+                for (int j = 0; j < kT; ++j)
+                  if (cb + i <= cl) acc[j] += v[i][j];
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) apply_epi<EPI>(g, r, t0 + j, acc[j]);
+            for (int j = 0; j < kT; ++j) apply_epi<EPI>(g, r, t0 + j, acc[j]);
           }
           if (threadIdx.x == 64) g.counters[t] = 0;
         }

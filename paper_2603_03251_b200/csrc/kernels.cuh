@@ -139,10 +139,53 @@ __global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int
 
 __device__ __forceinline__ void pdl_wait_all() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// L2 prefetch window of the weight stream: the weight bytes
+// that upcoming GEMMs will stream next, pulled into L2 by the kernel that
+// runs before them, so HBM keeps streaming through latency-bound kernels
+// (attention, norms, GEMM ramps / drains). A persistent stream-K GEMM reads
+// its P unit ranges in parallel, so "the next bytes" of a GEMM are the
+// fraction [f0, f1) of EVERY range: a segment names a GEMM (pre-tiled
+// weights, U units of unit_bytes, P ranges) and that fraction. The issuing
+// kernel's CTAs share the ranges round-robin; thread 0 issues bulk L2
+// prefetches of <= 64 KB.
+struct PfSeg {
+  const char* w;
+  int U, P;
+  float f0, f1;
+};
+constexpr int kPfSegs = 4;
+struct Prefetch {
+  PfSeg seg[kPfSegs];
+  int n;
+};
+
+__device__ __forceinline__ void prefetch_window(const Prefetch& w, int unit_bytes) {
+  if (w.n <= 0 || threadIdx.x != 0 || threadIdx.y != 0 || threadIdx.z != 0) return;
+  const int nct = int(gridDim.x * gridDim.y * gridDim.z);
+  const int cta = int(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+  for (int k = 0; k < w.n && k < kPfSegs; ++k) {
+    const PfSeg& sg = w.seg[k];
+    for (int j = cta; j < sg.P; j += nct) {
+      const long long u0 = (long long)j * sg.U / sg.P, u1 = (long long)(j + 1) * sg.U / sg.P;
+      const long long len = (u1 - u0) * unit_bytes;
+      long long b0 = u0 * unit_bytes + ((long long)(sg.f0 * float(len)) & ~1023LL);
+      long long b1 = u0 * unit_bytes + (sg.f1 >= 1.0f ? len : ((long long)(sg.f1 * float(len)) & ~1023LL));
+      for (long long b = b0; b < b1; b += 65536) {
+        const long long n = (b1 - b) < 65536 ? (b1 - b) : 65536;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sg.w + b), "r"(uint32_t(n & ~15LL))
+                     : "memory");
+      }
+    }
+  }
+}
+
+constexpr int kPfUnitBytes = 32768;  // GEMM unit = 2 k-blocks of 128 x 64 bf16 (gemm_tc.cuh kABytes)
+
 // ------------------------------------------------------------------ forward
 // x[m][:] = E[token_m][:] (fp32 residual stream); E row-major or pre-tiled.
 __global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const FwdParams* __restrict__ P,
-                             float* __restrict__ x) {
+                             float* __restrict__ x, Prefetch pf) {
+  prefetch_window(pf, kPfUnitBytes);
   asm volatile("griddepcontrol.launch_dependents;");
   pdl_wait_all();
   const int m = blockIdx.x;
@@ -162,8 +205,9 @@ constexpr int kNormThreads = 256;
 
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                                                int d, const float* __restrict__ g, float eps,
-                                                               bf16* __restrict__ out) {
+                                                               bf16* __restrict__ out, Prefetch pf) {
   __shared__ float sh[32];
+  prefetch_window(pf, kPfUnitBytes);
   // let the next kernel (a GEMM) launch now and prefetch its weights; it
   // still waits for this grid, which waits for its own predecessor
   asm volatile("griddepcontrol.launch_dependents;");
@@ -226,23 +270,46 @@ struct AttnWs {
   int* counter;  // [M][KVH]
 };
 
-template <int G>
-__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __restrict__ qkv, const FwdParams* __restrict__ P,
-                                                                 int M, const float* __restrict__ cos_t,
-                                                                 const float* __restrict__ sin_t, bf16* __restrict__ kc,
-                                                                 bf16* __restrict__ vc, int S, int H, int KVH, int hd,
-                                                                 float scale, bf16* __restrict__ out, AttnWs ws) {
-  __shared__ float qs[kMaxGroup * 128];
-  __shared__ float sc[kMaxGroup * kAttnChunk];
-  __shared__ float stat[kMaxGroup][2];
-  __shared__ float pv_red[8192];  // [key groups][G][hd]: ngrp * hd = 1024, G <= 8
-  __shared__ int s_last;
-  // let the next kernel (a GEMM) launch now and prefetch its weights; it
-  // still waits for this grid, which waits for its own predecessor
-  asm volatile("griddepcontrol.launch_dependents;");
-  pdl_wait_all();
-  const int chunk = blockIdx.x, kvh = blockIdx.y, m = blockIdx.z, tid = threadIdx.x;
-  const int nchunks = gridDim.x;
+// Shared-memory scratch of one attention work item (kAttnSmemFloats(G, hd)
+// floats + one int); static in attention_kernel, carved from the dynamic
+// shared memory in the persistent forward kernel (fwd_mk.cuh).
+struct AttnSmem {
+  float* qs;      // [G][hd]
+  float* sc;      // [G][kAttnChunk]
+  float* stat;    // [G][2]
+  float* pv_red;  // [key groups][G][hd]
+  int* s_last;
+};
+__host__ __device__ constexpr int attn_pv_floats(int G, int hd) { return (kAttnThreads / (hd / 8)) * G * hd; }
+__host__ __device__ constexpr int attn_smem_floats(int G, int hd) {
+  return G * 128 + G * kAttnChunk + 2 * kMaxGroup + attn_pv_floats(G, hd) + 4;
+}
+__device__ __forceinline__ AttnSmem attn_smem_carve(float* base, int G, int hd) {
+  AttnSmem a;
+  a.qs = base;
+  a.sc = a.qs + G * 128;
+  a.stat = a.sc + G * kAttnChunk;
+  a.pv_red = a.stat + 2 * kMaxGroup;
+  a.s_last = reinterpret_cast<int*>(a.pv_red + attn_pv_floats(G, hd));
+  return a;
+}
+
+struct BlockSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// One work item (key chunk, kv head, query token) of the split attention,
+// executed by kAttnThreads threads (tid) that synchronise with sync().
+template <int G, class Sync>
+__device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __restrict__ P, int M,
+                          const float* __restrict__ cos_t, const float* __restrict__ sin_t, bf16* __restrict__ kc,
+                          bf16* __restrict__ vc, int S, int H, int KVH, int hd, float scale, bf16* __restrict__ out,
+                          AttnWs ws, int chunk, int kvh, int m, int nchunks, int tid, AttnSmem sm, Sync sync) {
+  float* qs = sm.qs;
+  float* sc = sm.sc;
+  float* stat = sm.stat;
+  float* pv_red = sm.pv_red;
+  int* s_last = sm.s_last;
   const int lane = tid & 31, warp = tid >> 5;
   const int half = hd >> 1;
   const size_t row_len = size_t(H + 2 * KVH) * hd;
@@ -263,13 +330,13 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
       const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
       const float* ks = qkv + size_t(t) * row_len + size_t(H + kvh) * hd;
       const float* vs = qkv + size_t(t) * row_len + size_t(H + KVH + kvh) * hd;
-      const float a = ks[i], b = ks[i + half];
+      const float a = __ldcg(ks + i), b = __ldcg(ks + i + half);
       bf16* kd = kc + (size_t(kvh) * S + slot) * hd;
       bf16* vd = vc + (size_t(kvh) * S + slot) * hd;
       kd[i] = __float2bfloat16_rn(a * c - b * sn);
       kd[i + half] = __float2bfloat16_rn(b * c + a * sn);
-      vd[i] = __float2bfloat16_rn(vs[i]);
-      vd[i + half] = __float2bfloat16_rn(vs[i + half]);
+      vd[i] = __float2bfloat16_rn(__ldcg(vs + i));
+      vd[i + half] = __float2bfloat16_rn(__ldcg(vs + i + half));
     }
     // 2) rotated queries of the group
     {
@@ -278,12 +345,12 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
         const int gg = e / half, i = e % half;
         const float* src = qkv + size_t(m) * row_len + size_t(kvh * G + gg) * hd;
         const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
-        const float a = src[i], b = src[i + half];
+        const float a = __ldcg(src + i), b = __ldcg(src + i + half);
         qs[gg * hd + i] = a * c - b * sn;
         qs[gg * hd + i + half] = b * c + a * sn;
       }
     }
-    __syncthreads();
+    sync();
     // 3) scores: one key per thread; the whole K row is loaded up front
     //    (hd/8 independent 16-byte loads in flight per thread)
     const bf16* kbase = kc + size_t(kvh) * S * hd;
@@ -321,7 +388,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
         for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + tid] = dot[gg] * scale;
       }
     }
-    __syncthreads();
+    sync();
     // 4) chunk softmax statistics (warp gg -> head gg)
     const int n = j1 - j0;
     for (int gg = warp; gg < G; gg += kAttnThreads / 32) {
@@ -335,9 +402,9 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
         den += e;
       }
       den = warp_sum(den);
-      if (lane == 0) { stat[gg][0] = mx; stat[gg][1] = den; }
+      if (lane == 0) { stat[2 * gg] = mx; stat[2 * gg + 1] = den; }
     }
-    __syncthreads();
+    sync();
     // 5) unnormalised P.V of the chunk. Thread = (key group, 8-dim chunk);
     //    its <= 16 V vectors are loaded up front; partial sums are reduced
     //    over key groups through shared memory.
@@ -382,7 +449,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
         for (int gg = 0; gg < G; ++gg)
 #pragma unroll
         for (int i = 0; i < 8; ++i) red[(kg * G + gg) * hd + dc * 8 + i] = acc[gg][i];
-      __syncthreads();
+      sync();
       for (int e = tid; e < G * hd; e += kAttnThreads) {
         const int gg = e / hd, dd = e % hd;
         float o = 0.f;
@@ -391,17 +458,17 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
       }
     }
     if (tid < G) {
-      part[(size_t(chunk) * G + tid) * (hd + 2) + hd] = stat[tid][0];
-      part[(size_t(chunk) * G + tid) * (hd + 2) + hd + 1] = stat[tid][1];
+      part[(size_t(chunk) * G + tid) * (hd + 2) + hd] = stat[2 * tid];
+      part[(size_t(chunk) * G + tid) * (hd + 2) + hd + 1] = stat[2 * tid + 1];
     }
   }
   // 6) the last of this query's chunks merges them in chunk order
   if (chunk >= used) return;
   __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&ws.counter[m * KVH + kvh], 1) == used - 1;
-  __syncthreads();
-  if (!s_last) return;
+  sync();
+  if (tid == 0) *s_last = atomicAdd(&ws.counter[m * KVH + kvh], 1) == used - 1;
+  sync();
+  if (!*s_last) return;
   __threadfence();
   for (int e = tid; e < G * hd; e += kAttnThreads) {
     const int gg = e / hd, dd = e % hd;
@@ -417,6 +484,23 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __
     out[size_t(m) * H * hd + size_t(kvh * G + gg) * hd + dd] = __float2bfloat16_rn(o / den);
   }
   if (tid == 0) ws.counter[m * KVH + kvh] = 0;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const float* __restrict__ qkv, const FwdParams* __restrict__ P,
+                                                                 int M, const float* __restrict__ cos_t,
+                                                                 const float* __restrict__ sin_t, bf16* __restrict__ kc,
+                                                                 bf16* __restrict__ vc, int S, int H, int KVH, int hd,
+                                                                 float scale, bf16* __restrict__ out, AttnWs ws,
+                                                                 Prefetch pf) {
+  __shared__ float smem[attn_smem_floats(kMaxGroup, 128)];
+  prefetch_window(pf, kPfUnitBytes);
+  // let the next kernel (a GEMM) launch now and prefetch its weights; it
+  // still waits for this grid, which waits for its own predecessor
+  asm volatile("griddepcontrol.launch_dependents;");
+  pdl_wait_all();
+  attn_item<G>(qkv, P, M, cos_t, sin_t, kc, vc, S, H, KVH, hd, scale, out, ws, blockIdx.x, blockIdx.y, blockIdx.z,
+               gridDim.x, threadIdx.x, attn_smem_carve(smem, G, hd), BlockSync());
 }
 
 // ------------------------------------------------------------------ top-k
