@@ -21,6 +21,7 @@
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
 #include "fwd_mk.cuh"
+#include "attn_cl.cuh"
 #include "kernels.cuh"
 #include "probe.cuh"
 #include "rowops.cuh"
@@ -197,6 +198,7 @@ struct Engine {
   // than HBM, so the phase barriers / attention latency it exposes are never
   // caught up).
   int use_mk = 0;
+  int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
@@ -491,6 +493,12 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
   configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
   configure_gemm<EPI_STORE, 32, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 32, tc::kSmallBudgetKB>();
+  for (auto f : {attention_cl_kernel<1>, attention_cl_kernel<2>, attention_cl_kernel<4>, attention_cl_kernel<8>})
+    carveout_max(f);
+  CK(cudaFuncSetAttribute(attention_cl_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(1, 128))));
+  CK(cudaFuncSetAttribute(attention_cl_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(2, 128))));
+  CK(cudaFuncSetAttribute(attention_cl_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(4, 128))));
+  CK(cudaFuncSetAttribute(attention_cl_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(8, 128))));
   mk_configure<16, 1>(); mk_configure<16, 2>(); mk_configure<16, 4>(); mk_configure<16, 8>();
   mk_configure<32, 1>(); mk_configure<32, 2>(); mk_configure<32, 4>(); mk_configure<32, 8>();
   mk_configure<64, 1>(); mk_configure<64, 2>(); mk_configure<64, 4>(); mk_configure<64, 8>();
@@ -600,6 +608,41 @@ static int attn_chunks(const Model& m) {
   return std::max(1, (nk + kAttnChunk - 1) / kAttnChunk);
 }
 
+// Cluster attention (attn_cl.cuh): the nch key chunks of a (kv head, token)
+// form one thread-block cluster; PDL as the other kernels of the step.
+template <int G>
+static void attn_cl_launch_g(Model& m, int nch, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale,
+                             cudaStream_t s, Prefetch pf) {
+  const ssd_model_shape& sh = m.s;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nch, sh.n_kv_heads, M);
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = attn_cl_smem(G, sh.head_dim);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = nch;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  CK(cudaLaunchKernelEx(&cfg, attention_cl_kernel<G>, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
+                        (const float*)m.rope_sin, kc, vc, m.S, sh.n_heads, sh.n_kv_heads, sh.head_dim, scale, m.attn,
+                        std::min(m.ctx_bound, m.S), pf));
+}
+
+static void attn_cl_launch(Model& m, int nch, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale,
+                           cudaStream_t s, Prefetch pf) {
+  switch (m.s.n_heads / m.s.n_kv_heads) {
+    case 1: attn_cl_launch_g<1>(m, nch, M, P, kc, vc, scale, s, pf); break;
+    case 2: attn_cl_launch_g<2>(m, nch, M, P, kc, vc, scale, s, pf); break;
+    case 4: attn_cl_launch_g<4>(m, nch, M, P, kc, vc, scale, s, pf); break;
+    default: attn_cl_launch_g<8>(m, nch, M, P, kc, vc, scale, s, pf); break;
+  }
+}
+
 // Persistent forward kernel launch (fwd_mk.cuh): the whole step in one
 // cooperative launch (all CTAs co-resident: grid barriers).
 template <int NP, int G>
@@ -688,7 +731,9 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
                  (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
-    if (do_attn) {
+    if (do_attn && nch <= kAttnClMaxChunks && E.attn_cluster) {
+      attn_cl_launch(m, nch, M, P, kc, vc, scale, s, pf.upto(4 * l + 1));
+    } else if (do_attn) {
       auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
       launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
                  (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws, pf.upto(4 * l + 1));
@@ -1004,6 +1049,7 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
   if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
+  if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
@@ -1024,8 +1070,17 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
       throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
   configure_kernels();
   mk_diag_init();
-  CK(cudaStreamCreateWithFlags(&E.sv, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&E.ss, cudaStreamNonBlocking));
+  {
+    // colocated SSD: optionally give the speculator (the longer chain of
+    // dependent steps per round) the higher stream priority
+    // (SSD_B200_SPEC_PRIO=1; measured neutral, profiles/r01_summary.md)
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* sp = std::getenv("SSD_B200_SPEC_PRIO");
+    const bool prio = sp && std::atoi(sp) != 0;
+    CK(cudaStreamCreateWithPriority(&E.sv, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&E.ss, cudaStreamNonBlocking, prio ? hi : lo));
+  }
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_verified, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming));
