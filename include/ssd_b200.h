@@ -152,6 +152,14 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
 ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model_shape* draft,
                                   const ssd_pair_params* pair, int32_t device, int32_t role, int32_t max_branches,
                                   int32_t max_lookahead, ssd_engine** out);
+/* Same, for rank tp_rank of a tensor-parallel verifier of tp_size ranks
+ * (role SSD_ROLE_VERIFIER; Megatron sharding: column-parallel QKV / gate-up,
+ * row-parallel O / down, vocabulary-parallel head, replicated embedding).
+ * Connect the ranks with ssd_tp_export / ssd_tp_connect; every rank then
+ * makes the same calls and computes identical results. */
+ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
+                                int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out);
 ssd_status ssd_engine_destroy(ssd_engine* e);
 /* Bytes of weights streamed per forward step of model `which` (0 target,
  * 1 draft): the algorithmic bytes of one decode step. */
@@ -190,6 +198,14 @@ ssd_status ssd_mailbox_export(ssd_engine* e, uint8_t* handle);
 /* Map the peers' mailboxes: handles[i * SSD_MAILBOX_HANDLE_BYTES ..] for
  * i in [0, n_peers); entry `self` is this engine's own. */
 ssd_status ssd_mailbox_connect(ssd_engine* e, int32_t n_peers, const uint8_t* handles, int32_t self);
+
+/* Tensor-parallel verifier: export this rank's collective region (CUDA IPC,
+ * SSD_MAILBOX_HANDLE_BYTES bytes) and map all ranks' regions
+ * (handles[r * SSD_MAILBOX_HANDLE_BYTES ..] for r in [0, tp_size)). The two
+ * all-reduces per layer and the logits all-gather then run as peer-memory
+ * kernels inside every forward. */
+ssd_status ssd_tp_export(ssd_engine* e, uint8_t* handle);
+ssd_status ssd_tp_connect(ssd_engine* e, const uint8_t* handles);
 
 /* VerifierProcess side of run_protocol_harness (sim.cpp:321-351, 502-601):
  * per round wait for the speculation, verify (M = K+1 target forward +

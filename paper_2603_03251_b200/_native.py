@@ -66,7 +66,11 @@ SIGNATURES = {
                                     P(EngineP)]),
     "ssd_engine_create_role": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32,
                                          C.c_int32, C.c_int32, P(EngineP)]),
+    "ssd_engine_create_tp": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_int32, C.c_int32, C.c_int32, P(EngineP)]),
     "ssd_engine_destroy": (C.c_int, [EngineP]),
+    "ssd_tp_export": (C.c_int, [EngineP, P(C.c_uint8)]),
+    "ssd_tp_connect": (C.c_int, [EngineP, P(C.c_uint8)]),
     "ssd_mailbox_export": (C.c_int, [EngineP, P(C.c_uint8)]),
     "ssd_mailbox_connect": (C.c_int, [EngineP, C.c_int32, P(C.c_uint8), C.c_int32]),
     "ssd_run_ssd_verifier": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, i32p, C.c_int64, i64p,

@@ -271,17 +271,34 @@ class Engine:
     """A (target, draft) pair resident on one B200 plus its decode loops."""
 
     def __init__(self, target: N.ModelShape, draft: N.ModelShape, pair: Pair = Pair(), device: int = 0,
-                 max_branches: int = 64, max_lookahead: int = 8, role: int = N.ROLE_COLOCATED):
+                 max_branches: int = 64, max_lookahead: int = 8, role: int = N.ROLE_COLOCATED, tp_rank: int = 0,
+                 tp_size: int = 1):
         """role: ROLE_COLOCATED (both models), ROLE_VERIFIER (target only) or
-        ROLE_SPECULATOR (draft only) — the processes of a split run."""
+        ROLE_SPECULATOR (draft only) — the processes of a split run. A
+        verifier may be tensor-parallel: rank tp_rank of tp_size (connect the
+        ranks with tp_handle / tp_connect)."""
         self.lib = N.load()
         self.target, self.draft, self.pair = target, draft, pair
         self.vocab = target.vocab
         self.role = role
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         h = C.c_void_p()
-        _check(self.lib.ssd_engine_create_role(C.byref(target), C.byref(draft), C.byref(pair.c()), device, role,
-                                               max_branches, max_lookahead, C.byref(h)))
+        _check(self.lib.ssd_engine_create_tp(C.byref(target), C.byref(draft), C.byref(pair.c()), device, role, tp_rank,
+                                             tp_size, max_branches, max_lookahead, C.byref(h)))
         self.h = h
+
+    def tp_handle(self) -> bytes:
+        buf = (C.c_uint8 * N.MAILBOX_HANDLE_BYTES)()
+        _check(self.lib.ssd_tp_export(self.h, buf))
+        return bytes(buf)
+
+    def tp_connect(self, handles: Sequence[bytes]):
+        """Map the TP ranks' collective regions (handles ordered by TP rank)."""
+        blob = b"".join(handles)
+        if len(handles) != self.tp_size or len(blob) != N.MAILBOX_HANDLE_BYTES * self.tp_size:
+            raise ConfigError("tensor parallel: one 64-byte handle per rank")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(self.lib.ssd_tp_connect(self.h, buf))
 
     def close(self):
         if getattr(self, "h", None):

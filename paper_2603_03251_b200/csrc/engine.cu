@@ -22,6 +22,7 @@
 #include "gemm_tc.cuh"
 #include "fwd_mk.cuh"
 #include "attn_cl.cuh"
+#include "tp.cuh"
 #include "kernels.cuh"
 #include "probe.cuh"
 #include "rowops.cuh"
@@ -143,6 +144,7 @@ struct Model {
   int* attn_cnt = nullptr;
   float *x = nullptr, *qkv = nullptr, *q = nullptr, *logits = nullptr;
   float *dlt1 = nullptr, *dlt2 = nullptr;  // attention / MLP projections (residual deltas)
+  float* logits_shard = nullptr;           // TP: this rank's vocabulary shard of the logits
   bf16 *xb = nullptr, *attn = nullptr, *act = nullptr;
   int64_t weight_bytes = 0;
   const char* arena = nullptr;  // every GEMM weight, contiguous in forward order (L2 prefetch stream)
@@ -160,6 +162,9 @@ struct Model {
   unsigned* mk_bar = nullptr;
   int mk_ctas = 0;                          // CTAs (SMs) of its launches; 0 = all
   int gemm_ctas = 0;                        // cap on a GEMM's CTAs (0 = every SM)
+  // tensor parallelism
+  int tp_rank = 0, tp_size = 1;
+  int V_full = 0;                           // unsharded vocabulary
 
   size_t kv_layer_elems() const { return size_t(s.n_kv_heads) * size_t(S) * size_t(s.head_dim); }
 };
@@ -216,6 +221,12 @@ struct Engine {
   Inbox** peers_dev = nullptr;       // device copy of `peers`
   int* send_counter = nullptr;
   int seq_base = 0;                  // advances by rounds + 2 per split run
+  // tensor-parallel verifier (tp.cuh)
+  char* tp_region = nullptr;         // this rank's IPC-exported region
+  TpLayout tp_L{};
+  TpPeers tp_peers{};
+  TpCtl* tp_ctl = nullptr;
+  std::vector<void*> tp_opened;
 };
 
 // ----------------------------------------------------------------- helpers
@@ -242,15 +253,36 @@ static float sign_h(uint64_t key, size_t i) { return unit_value_h(key, i) < 0.f 
 static GenShape gshape(const ssd_model_shape& s) { return GenShape{s.d_model, s.n_heads, s.n_kv_heads, s.head_dim, s.ffn}; }
 
 static void gen_launch(bf16* dst, int rows, int cols, int stride, int off, const ssd_model_shape& self,
-                       const ssd_model_shape& dr, const GenPair& gp, int role, int layer, int kind) {
-  gen_layer_kernel<<<148 * 8, 256>>>(dst, rows, cols, stride, off, gshape(self), gshape(dr), gp, role, layer, kind);
+                       const ssd_model_shape& dr, const GenPair& gp, int role, int layer, int kind, int lr0 = 0,
+                       int lc0 = 0) {
+  gen_layer_kernel<<<148 * 8, 256>>>(dst, rows, cols, stride, off, gshape(self), gshape(dr), gp, role, layer, kind, lr0,
+                                     lc0);
   KCHECK();
 }
 
-static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shape& dr, const ssd_pair_params& pp,
-                        int role, int branch_slots, int maxM) {
+// Tensor-parallel shard shape (Megatron): heads, kv heads, FFN
+// and vocabulary split over tp ranks; d_model replicated.
+static ssd_model_shape tp_local(const ssd_model_shape& s, int tp) {
+  ssd_model_shape l = s;
+  l.n_heads /= tp;
+  l.n_kv_heads /= tp;
+  l.ffn /= tp;
+  l.vocab /= tp;
+  return l;
+}
+
+// sfull: the model's full shape; with tp_size > 1 this engine holds shard
+// tp_rank (column-parallel QKV / gate-up, row-parallel O / down,
+// vocabulary-parallel head, replicated embedding), generated as the exact
+// blocks of the unsharded synthetic tensors.
+static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_shape& dr, const ssd_pair_params& pp,
+                        int role, int branch_slots, int maxM, int tp_rank = 0, int tp_size = 1) {
+  const ssd_model_shape s = tp_local(sfull, tp_size);
   m.s = s;
   m.role = role;
+  m.tp_rank = tp_rank;
+  m.tp_size = tp_size;
+  m.V_full = sfull.vocab;
   const int d = s.d_model, hd = s.head_dim;
   m.qd = s.n_heads * hd;
   m.kvd = s.n_kv_heads * hd;
@@ -290,14 +322,15 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
     m.head.w = reinterpret_cast<bf16*>(base + m.head.off);
   }
   // tables: the LM head is pre-tiled for the GEMM; a tied table is both
-  gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, s.tied ? 0 : 1, 1);
+  if (s.tied && tp_size > 1) throw Fail(SSD_CONFIG, "engine: tensor parallelism needs an untied LM head");
+  gen_table_kernel<<<148 * 8, 256>>>(m.head.w, s.vocab, d, dr.d_model, gp, s.tied ? 0 : 1, 1, tp_rank * s.vocab);
   KCHECK();
   if (s.tied) {
     m.embed = m.head.w;
     m.embed_tiled = 1;
   } else {
-    m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(s.vocab) * d)));
-    gen_table_kernel<<<148 * 8, 256>>>(m.embed, s.vocab, d, dr.d_model, gp, 0, 0);
+    m.embed = static_cast<bf16*>(own(dalloc<bf16>(size_t(sfull.vocab) * d)));
+    gen_table_kernel<<<148 * 8, 256>>>(m.embed, sfull.vocab, d, dr.d_model, gp, 0, 0, 0);
     KCHECK();
     m.embed_tiled = 0;
   }
@@ -324,13 +357,14 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   int64_t wb = 0;
   for (int l = 0; l < s.n_layers; ++l) {
     DevLayer& L = m.layers[size_t(l)];
-    gen_launch(L.qkv.w, m.qd, d, 1, 0, s, dr, gp, role, l, 0);
-    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd, s, dr, gp, role, l, 1);
-    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd + m.kvd, s, dr, gp, role, l, 2);
-    gen_launch(L.o.w, d, m.qd, 1, 0, s, dr, gp, role, l, 3);
-    gen_launch(L.gu.w, s.ffn, d, 2, 0, s, dr, gp, role, l, 4);
-    gen_launch(L.gu.w, s.ffn, d, 2, 1, s, dr, gp, role, l, 5);
-    gen_launch(L.dn.w, d, s.ffn, 1, 0, s, dr, gp, role, l, 6);
+    const int r = tp_rank;
+    gen_launch(L.qkv.w, m.qd, d, 1, 0, sfull, dr, gp, role, l, 0, r * m.qd);
+    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd, sfull, dr, gp, role, l, 1, r * m.kvd);
+    gen_launch(L.qkv.w, m.kvd, d, 1, m.qd + m.kvd, sfull, dr, gp, role, l, 2, r * m.kvd);
+    gen_launch(L.o.w, d, m.qd, 1, 0, sfull, dr, gp, role, l, 3, 0, r * m.qd);
+    gen_launch(L.gu.w, s.ffn, d, 2, 0, sfull, dr, gp, role, l, 4, r * s.ffn);
+    gen_launch(L.gu.w, s.ffn, d, 2, 1, sfull, dr, gp, role, l, 5, r * s.ffn);
+    gen_launch(L.dn.w, d, s.ffn, 1, 0, sfull, dr, gp, role, l, 6, 0, r * s.ffn);
     wb += int64_t(m.qd + 2 * m.kvd) * d + int64_t(d) * m.qd + int64_t(2 * s.ffn) * d + int64_t(d) * s.ffn;
   }
   wb += int64_t(s.vocab) * d;  // LM head
@@ -340,7 +374,7 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   m.kc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   m.vc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   std::vector<float> cs, sn;
-  rope_tables(s, cs, sn);
+  rope_tables(s, cs, sn);  // head_dim / max_ctx are not sharded
   m.rope_cos = static_cast<float*>(own(dalloc<float>(cs.size())));
   m.rope_sin = static_cast<float*>(own(dalloc<float>(sn.size())));
   CK(cudaMemcpy(m.rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
@@ -356,7 +390,8 @@ static void build_model(Model& m, const ssd_model_shape& s, const ssd_model_shap
   m.q = static_cast<float*>(own(dalloc<float>(size_t(maxM) * m.qd)));
   m.attn = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * m.qd)));
   m.act = static_cast<bf16*>(own(dalloc<bf16>(size_t(maxM) * s.ffn)));
-  m.logits = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.vocab)));
+  m.logits = static_cast<float*>(own(dalloc<float>(size_t(maxM) * sfull.vocab)));
+  if (tp_size > 1) m.logits_shard = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.vocab)));
   m.ws_floats = size_t(16) << 20;  // 64 MB of split-K partials
   m.ws = static_cast<float*>(own(dalloc<float>(m.ws_floats)));
   m.counters = static_cast<int*>(own(dalloc<int>(8192)));
@@ -699,12 +734,20 @@ static void mk_launch_g(Engine& E, Model& m, const FwdParams* P, int M, float* l
   }
 }
 
+// Row-parallel projection sum over the TP ranks (tp.cuh), in place.
+static void tp_allreduce(Engine& E, Model& m, float* buf, int M, cudaStream_t s) {
+  if (!E.tp_peers.region[0]) throw Fail(SSD_CONFIG, "tensor parallel: peers not connected (ssd_tp_connect)");
+  tp_allreduce_kernel<<<64, 256, 0, s>>>(buf, M, E.tp_L, E.tp_peers, m.tp_rank, E.tp_ctl, E.st);
+  KCHECK();
+  ++E.launches;
+}
+
 // One forward step of `m` over the M tokens described by P. Logits of all M
 // rows go to `logits` ([M][V]) when non-null. Every kernel is launched with
 // PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
-  if (E.use_mk && M <= 64) {  // decode / verify / branch steps and prefill chunks: one persistent launch
+  if (E.use_mk && M <= 64 && m.tp_size == 1) {  // decode / verify / branch steps and prefill chunks: one persistent launch
     if (M <= 16) mk_launch_g<16>(E, m, P, M, logits, s);
     else if (M <= 32) mk_launch_g<32>(E, m, P, M, logits, s);
     else mk_launch_g<64>(E, m, P, M, logits, s);
@@ -739,19 +782,29 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
                  (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws, pf.upto(4 * l + 1));
     }
     linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
+    if (m.tp_size > 1) tp_allreduce(E, m, m.dlt1, M, s);  // row-parallel O: sum the shards
     // x += attention projection; xb = norm(x) * g
     if (do_norm)
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
                  (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb, pf.upto(4 * l + 2));
     linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s, pf.after(4 * l + 2));
     linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
+    if (m.tp_size > 1) tp_allreduce(E, m, m.dlt2, M, s);  // row-parallel down projection
     E.launches += 3;
   }
   if (logits) {
     launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt2, d,
                (const float*)m.final_gain, sh.norm_eps, m.xb, pf.upto(4 * sh.n_layers));
-    linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
-    ++E.launches;
+    if (m.tp_size > 1) {  // vocabulary-parallel head: local shard, then all-gather the rows
+      linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits_shard, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
+      tp_gather_logits_kernel<<<64, 256, 0, s>>>(m.logits_shard, M, sh.vocab, logits, E.tp_L, E.tp_peers, m.tp_rank,
+                                                 E.tp_ctl, E.st);
+      KCHECK();
+      E.launches += 2;
+    } else {
+      linear<EPI_STORE>(E, m, m.head, m.xb, M, logits, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
+      ++E.launches;
+    }
   }
 }
 
@@ -766,7 +819,7 @@ static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t
     const bool last = lo + M >= n;
     forward(E, m, E.P_pre, M, (last && last_logits) ? m.logits : nullptr, s);
     if (last && last_logits)
-      CK(cudaMemcpyAsync(last_logits, m.logits + size_t(M - 1) * m.s.vocab, size_t(m.s.vocab) * 4,
+      CK(cudaMemcpyAsync(last_logits, m.logits + size_t(M - 1) * m.V_full, size_t(m.V_full) * 4,
                          cudaMemcpyDeviceToDevice, s));
   }
 }
@@ -1026,9 +1079,23 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
 ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model_shape* draft,
                                   const ssd_pair_params* pair, int32_t device, int32_t role, int32_t max_branches,
                                   int32_t max_lookahead, ssd_engine** out) {
+  return ssd_engine_create_tp(target, draft, pair, device, role, 0, 1, max_branches, max_lookahead, out);
+}
+
+ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
+                                int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out) {
   API_BEGIN
   if (!target || !draft || !pair || !out) throw Fail(SSD_CONFIG, "engine: null argument");
   if (role < SSD_ROLE_COLOCATED || role > SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "engine: unknown role");
+  if (tp_size < 1 || tp_size > kTpMax || tp_rank < 0 || tp_rank >= tp_size) throw Fail(SSD_CONFIG, "engine: bad TP rank");
+  if (tp_size > 1) {
+    if (role != SSD_ROLE_VERIFIER) throw Fail(SSD_CONFIG, "engine: tensor parallelism is for the verifier role");
+    const int T = tp_size;
+    if (target->n_kv_heads % T || target->n_heads % T || target->ffn % T || target->vocab % T ||
+        (target->ffn / T) % 128 || (target->n_heads / T * target->head_dim) % 128 || target->tied)
+      throw Fail(SSD_CONFIG, "engine: target shape does not shard over this TP size");
+  }
   if (target->vocab != draft->vocab) throw Fail(SSD_ERROR, "sim: target and draft shapes differ");
   if (draft->d_model > target->d_model || draft->ffn > target->ffn || !draft->tied)
     throw Fail(SSD_CONFIG, "engine: the draft must be tied and no wider than the target");
@@ -1060,7 +1127,8 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
   }
   const int maxM = std::max(max_branches, max_lookahead + 1);
   // a split process materialises only its own model
-  if (role != SSD_ROLE_SPECULATOR) build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64));
+  if (role != SSD_ROLE_SPECULATOR)
+    build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64), tp_rank, tp_size);
   else E.T.s = *target;
   if (role != SSD_ROLE_VERIFIER)
     build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
@@ -1130,6 +1198,14 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
     E.inbox = static_cast<Inbox*>(p);
     E.send_counter = static_cast<int*>(own(dalloc<int>(1)));
   }
+  if (tp_size > 1) {  // TP collective region (own allocation: exported alone)
+    E.tp_L = TpLayout{tp_size, E.T.maxM, target->d_model, target->vocab};
+    void* p = nullptr;
+    CK(cudaMalloc(&p, E.tp_L.bytes()));
+    CK(cudaMemset(p, 0, E.tp_L.bytes()));
+    E.tp_region = static_cast<char*>(p);
+    E.tp_ctl = static_cast<TpCtl*>(own(dalloc<TpCtl>(1)));
+  }
   CK(cudaDeviceSynchronize());
   *out = h;
   API_END
@@ -1144,6 +1220,8 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   free_model(E.T);
   free_model(E.D);
   for (void* p : E.ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : E.tp_opened) cudaIpcCloseMemHandle(p);
+  if (E.tp_region) cudaFree(E.tp_region);
   if (E.inbox) cudaFree(E.inbox);
   if (E.peers_dev) cudaFree(E.peers_dev);
   for (void* p : E.owned) cudaFree(p);
@@ -1379,6 +1457,43 @@ ssd_status ssd_mailbox_connect(ssd_engine* h, int32_t n_peers, const uint8_t* ha
   // a fresh connection starts from a clean inbox and sequence 0
   CK(cudaMemset(E.inbox, 0, kInboxRows));
   E.seq_base = 0;
+  CK(cudaDeviceSynchronize());
+  API_END
+}
+
+ssd_status ssd_tp_export(ssd_engine* h, uint8_t* handle64) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!E.tp_region) throw Fail(SSD_CONFIG, "tensor parallel: engine created with tp_size 1");
+  if (!handle64) throw Fail(SSD_CONFIG, "tensor parallel: null handle buffer");
+  cudaIpcMemHandle_t mh;
+  CK(cudaIpcGetMemHandle(&mh, E.tp_region));
+  std::memcpy(handle64, &mh, sizeof(mh));
+  API_END
+}
+
+ssd_status ssd_tp_connect(ssd_engine* h, const uint8_t* handles) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!E.tp_region || !handles) throw Fail(SSD_CONFIG, "tensor parallel: not a TP engine");
+  for (void* p : E.tp_opened) cudaIpcCloseMemHandle(p);
+  E.tp_opened.clear();
+  for (int r = 0; r < E.tp_L.T; ++r) {
+    if (r == E.T.tp_rank) {
+      E.tp_peers.region[r] = E.tp_region;
+      continue;
+    }
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, handles + size_t(r) * SSD_MAILBOX_HANDLE_BYTES, sizeof(mh));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+    E.tp_opened.push_back(p);
+    E.tp_peers.region[r] = static_cast<char*>(p);
+  }
+  CK(cudaMemset(E.tp_region, 0, 4096));
+  CK(cudaMemset(E.tp_ctl, 0, sizeof(TpCtl)));
   CK(cudaDeviceSynchronize());
   API_END
 }

@@ -107,25 +107,32 @@ __host__ __device__ __forceinline__ size_t tiled_at(size_t r, size_t c, size_t K
 }
 
 // Fill rows [row_off + row_stride * r] of the pre-tiled matrix dst (row
-// length cols) with logical tensor (role, layer, kind) rows [0, rows).
+// length cols) with logical tensor (role, layer, kind) rows [lr0, lr0 + rows),
+// columns [lc0, lc0 + cols): the tensor-parallel shard of the full logical
+// tensor (lr0 = lc0 = 0 without TP), so every shard is bit-identical to the
+// matching block of the unsharded model.
 __global__ void gen_layer_kernel(bf16* dst, int rows, int cols, int row_stride, int row_off, GenShape self,
-                                 GenShape dr, GenPair p, int role, int layer, int kind) {
+                                 GenShape dr, GenPair p, int role, int layer, int kind, int lr0, int lc0) {
   const size_t total = size_t(rows) * size_t(cols), KB = size_t(cols) / 64;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     const size_t r = e / size_t(cols), c = e % size_t(cols);
-    dst[tiled_at(size_t(row_off) + size_t(row_stride) * r, c, KB)] = layer_elem(self, dr, p, role, layer, kind, r, c);
+    dst[tiled_at(size_t(row_off) + size_t(row_stride) * r, c, KB)] =
+        layer_elem(self, dr, p, role, layer, kind, size_t(lr0) + r, size_t(lc0) + c);
   }
 }
 
 // Embedding / LM head [V][d]: shared table S in dims [0, ds), target-private
 // tables beyond (oracle transformer_lm.cpp constructor). `tiled` stores it in
 // the GEMM layout (LM heads, and the tied draft table that is both).
-__global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int which /*0 embed 1 head*/, int tiled) {
+// Rows [v0, v0 + V) of the table (vocabulary-parallel LM-head shard; v0 = 0
+// for the whole table).
+__global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int which /*0 embed 1 head*/, int tiled,
+                                 int v0) {
   const uint64_t kS = derive_seed(p.seed, 0xE0000001u), kPE = derive_seed(p.seed, 0xE0000002u),
                  kPH = derive_seed(p.seed, 0xE0000003u);
   const size_t total = size_t(V) * size_t(d), dp = size_t(d - ds);
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const size_t v = e / size_t(d), i = e % size_t(d);
+    const size_t vl = e / size_t(d), i = e % size_t(d), v = size_t(v0) + vl;
     float val;
     if (i < size_t(ds)) {
       val = unit_value(kS, v * size_t(ds) + i) * p.embed_scale;
@@ -133,7 +140,7 @@ __global__ void gen_table_kernel(bf16* dst, int V, int d, int ds, GenPair p, int
       const size_t j = v * dp + (i - size_t(ds));
       val = which == 0 ? unit_value(kPE, j) * p.priv_embed : unit_value(kPH, j) * p.priv_head;
     }
-    dst[tiled ? tiled_at(v, i, size_t(d) / 64) : e] = __float2bfloat16_rn(val);
+    dst[tiled ? tiled_at(vl, i, size_t(d) / 64) : e] = __float2bfloat16_rn(val);
   }
 }
 
