@@ -183,7 +183,8 @@ def run_split(args):
         dist.init_process_group("gloo")
     P, ts, ds, cfg, prompt, fan, temp = workload(args)
     B = sum(fan)
-    se = SplitEngine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+    tp = max(1, min(args.tp, ws - 1))
+    se = SplitEngine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead, tp=tp)
     for _ in range(args.warmup):
         se.run(prompt, cfg)
     torch.cuda.synchronize()
@@ -224,10 +225,10 @@ def run_split(args):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (random-init correlated pair, random prompt)",
                 "config": {"workload": f"{args.config} ssd greedy K={cfg.lookahead} F={args.fanout} batch1 "
-                                       f"split 1 verifier + {ws - 1} speculators (branch-sharded)",
+                                       f"split verifier TP{tp} + {ws - tp} speculators (branch-sharded)",
                            "prompt_len": args.prompt_len, "rounds_per_step": args.rounds, "branches": B,
                            "l2": "no flush: weights streamed per round >> 126 MB L2",
-                           "parallelism": f"verifier x1 + speculator x{ws - 1}, NVLink mailboxes",
+                           "parallelism": f"verifier TP{tp} + speculator x{ws - tp}, NVLink mailboxes",
                            "gpus_visible": ndev},
                 "e2e": {"value": tokens / wall, "unit": "tokens/s", "h2d_bytes_per_step": 4 * len(prompt),
                         "d2h_bytes_per_step": 4 * (tokens // len(runs))},
@@ -380,6 +381,7 @@ def main():
     # pair divergence knob calibrated on this workload to alpha ~ 0.8 (
     # scripts/bench_alpha.py, profiles/r01_summary.md); alpha is reported
     ap.add_argument("--block-out-scale", type=float, default=0.07)
+    ap.add_argument("--tp", type=int, default=1, help="N>1 split mode: tensor-parallel verifier ranks")
     ap.add_argument("--multi", default="split", choices=["split", "replicas"],
                     help="N>1: split verifier/speculator processes (default) or independent replicas")
     ap.set_defaults(greedy=True)

@@ -191,7 +191,8 @@ ssd_status ssd_run_ssd(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
  * The reference's Channel between VerifierProcess and DraftProcess becomes
  * device mailboxes in HBM, mapped across processes/GPUs by CUDA IPC (NVLink
  * peer memory); messages are written by the sender's kernels inside the
- * round graph. Peer table order: [0] verifier, [1..G] speculators. */
+ * round graph. Peer table order: [0..T) verifier ranks (T = tensor-parallel
+ * size, 1 without TP), [T..T+G) speculators. */
 
 /* Export this engine's mailbox (SSD_MAILBOX_HANDLE_BYTES bytes). */
 ssd_status ssd_mailbox_export(ssd_engine* e, uint8_t* handle);
@@ -209,8 +210,9 @@ ssd_status ssd_tp_connect(ssd_engine* e, const uint8_t* handles);
 
 /* VerifierProcess side of run_protocol_harness (sim.cpp:321-351, 502-601):
  * per round wait for the speculation, verify (M = K+1 target forward +
- * fused verification), send (k*, t*) to the n_spec speculators. Writes the
- * emitted tokens and per-round outcomes. */
+ * fused verification), send (k*, t*) to the n_spec speculators (TP rank 0
+ * of a tensor-parallel verifier; every rank verifies identically). Writes
+ * the emitted tokens and per-round outcomes. */
 ssd_status ssd_run_ssd_verifier(ssd_engine* e, const int32_t* prompt, int32_t prompt_len, const ssd_sim_config* cfg,
                                 int32_t n_spec, int32_t* out_tokens, int64_t out_capacity, int64_t* out_len,
                                 int32_t* out_outcomes, ssd_run_stats* stats);
@@ -221,7 +223,8 @@ ssd_status ssd_run_ssd_verifier(ssd_engine* e, const int32_t* prompt, int32_t pr
  * speculation when it owns the hit (or, rank 0, for a backup). Stats hold
  * the full RunStats counters (identical on every speculator). */
 ssd_status ssd_run_ssd_speculator(ssd_engine* e, const int32_t* prompt, int32_t prompt_len, const ssd_sim_config* cfg,
-                                  int32_t rank, int32_t n_spec, int32_t* out_hits, ssd_run_stats* stats);
+                                  int32_t rank, int32_t n_spec, int32_t n_verifiers, int32_t* out_hits,
+                                  ssd_run_stats* stats);
 
 /* ------------------------------------------ single operations (specdec.hpp,
  * cache.hpp). Each starts from `context` (prefilled into the model's KV). */

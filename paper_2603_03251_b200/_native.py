@@ -75,8 +75,8 @@ SIGNATURES = {
     "ssd_mailbox_connect": (C.c_int, [EngineP, C.c_int32, P(C.c_uint8), C.c_int32]),
     "ssd_run_ssd_verifier": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, i32p, C.c_int64, i64p,
                                        i32p, P(RunStatsC)]),
-    "ssd_run_ssd_speculator": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, C.c_int32, i32p,
-                                         P(RunStatsC)]),
+    "ssd_run_ssd_speculator": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, C.c_int32, C.c_int32,
+                                         i32p, P(RunStatsC)]),
     "ssd_engine_weight_bytes": (C.c_int64, [EngineP, C.c_int32]),
     "ssd_run_ar": (C.c_int, [EngineP, i32p, C.c_int32, P(Scheme), C.c_int64, C.c_uint64, i32p, C.c_int64,
                              P(RunStatsC)]),

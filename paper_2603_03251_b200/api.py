@@ -378,13 +378,15 @@ class Engine:
         r.outcomes = oc.reshape(-1, 2)
         return r
 
-    def run_ssd_speculator(self, prompt: Sequence[int], cfg: SimConfig, rank: int, n_spec: int) -> RunStats:
-        """DraftProcess side (sim.cpp:376-485) for speculator `rank` of n_spec."""
+    def run_ssd_speculator(self, prompt: Sequence[int], cfg: SimConfig, rank: int, n_spec: int,
+                           n_verifiers: int = 1) -> RunStats:
+        """DraftProcess side (sim.cpp:376-485) for speculator `rank` of n_spec;
+        n_verifiers = ranks of a tensor-parallel verifier."""
         p = _i32(prompt)
         hits = np.zeros(cfg.rounds, dtype=np.int32)
         st = N.RunStatsC()
         _check(self.lib.ssd_run_ssd_speculator(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), rank, n_spec,
-                                               _ptr(hits, C.c_int32), C.byref(st)))
+                                               n_verifiers, _ptr(hits, C.c_int32), C.byref(st)))
         r = RunStats._from_c(st)
         r.hits = hits
         return r

@@ -1193,8 +1193,8 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   // mailbox (own allocation so it can be exported alone by CUDA IPC)
   {
     void* p = nullptr;
-    CK(cudaMalloc(&p, kInboxRows + size_t(K) * V * 4));
-    CK(cudaMemset(p, 0, kInboxRows + size_t(K) * V * 4));
+    CK(cudaMalloc(&p, kInboxRows + size_t(2) * K * V * 4));
+    CK(cudaMemset(p, 0, kInboxRows + size_t(2) * K * V * 4));
     E.inbox = static_cast<Inbox*>(p);
     E.send_counter = static_cast<int*>(own(dalloc<int>(1)));
   }
@@ -1504,10 +1504,12 @@ static void branch_block(int B, int rank, int G, int& lo, int& Bl) {
   Bl = int((long long)B * (rank + 1) / G) - lo;
 }
 
-static void split_common_checks(Engine& E, const ssd_sim_config* c, int G) {
+static void split_common_checks(Engine& E, const ssd_sim_config* c, int T, int G) {
   validate_cfg(E, c);
   if (G < 1) throw Fail(SSD_CONFIG, "split: at least one speculator");
-  if (int(E.peers.size()) != G + 1) throw Fail(SSD_CONFIG, "split: mailbox not connected to 1 verifier + G speculators");
+  if (T < 1 || T > kTpMax) throw Fail(SSD_CONFIG, "split: verifier ranks");
+  if (int(E.peers.size()) != T + G)
+    throw Fail(SSD_CONFIG, "split: mailbox not connected to T verifier ranks + G speculators");
   if (E.V % 4) throw Fail(SSD_CONFIG, "split: vocabulary must be a multiple of 4");
 }
 
@@ -1519,7 +1521,8 @@ ssd_status ssd_run_ssd_verifier(ssd_engine* h, const int32_t* prompt, int32_t n0
   CK(cudaSetDevice(E.dev));
   if (E.role != SSD_ROLE_VERIFIER) throw Fail(SSD_CONFIG, "run_ssd_verifier: engine role is not verifier");
   need(E.T, "run_ssd_verifier");
-  split_common_checks(E, c, n_spec);
+  const int T = E.T.tp_size;  // a tensor-parallel verifier: every rank verifies, rank 0 answers
+  split_common_checks(E, c, T, n_spec);
   const int K = c->lookahead;
   const int64_t R = c->rounds;
   set_history(E, prompt, n0, int(n0 + R * (K + 1) + 2 * K + 2));
@@ -1535,7 +1538,7 @@ ssd_status ssd_run_ssd_verifier(ssd_engine* h, const int32_t* prompt, int32_t n0
   gs.g.push_back(capture_graph(s, [&] {
     recv_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, rows, E.V);
     verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, s);
-    send_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.peers_dev + 1, n_spec, d_out);
+    send_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.peers_dev + T, E.T.tp_rank == 0 ? n_spec : 0, d_out);
     commit_kernel<<<1, 32, 0, s>>>(E.st);
     KCHECK();
     E.launches += 3;
@@ -1566,13 +1569,15 @@ ssd_status ssd_run_ssd_verifier(ssd_engine* h, const int32_t* prompt, int32_t n0
 }
 
 ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c,
-                                  int32_t rank, int32_t n_spec, int32_t* out_hits, ssd_run_stats* stats) {
+                                  int32_t rank, int32_t n_spec, int32_t n_verifiers, int32_t* out_hits,
+                                  ssd_run_stats* stats) {
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   if (E.role != SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "run_ssd_speculator: engine role is not speculator");
   need(E.D, "run_ssd_speculator");
-  split_common_checks(E, c, n_spec);
+  const int T = n_verifiers;
+  split_common_checks(E, c, T, n_spec);
   if (rank < 0 || rank >= n_spec) throw Fail(SSD_CONFIG, "run_ssd_speculator: rank out of range");
   const int K = c->lookahead;
   int B = 0, max_f = 0;
@@ -1592,7 +1597,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
   }
   E.seq_base += int(R) + 2;
   if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
-  Inbox** vpeers = E.peers_dev;  // [0] verifier, [1..G] speculators
+  Inbox** vpeers = E.peers_dev;  // [0..T) verifier ranks, [T..T+G) speculators
   const int send_blocks = 2 * E_num_sms;
   // initial synchronous draft, clock starts at T_p (sim.cpp:524-526)
   draft_steps(E, K, c->scheme, 0, 0, s);
@@ -1602,7 +1607,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, clock), &tmp.clock, sizeof(double),
                        cudaMemcpyHostToDevice, s));
   }
-  send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 1, E.send_counter);
+  send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter);
   KCHECK();
   const bool jit = c->backup_kind == 0;
   E.launches = 0;
@@ -1613,7 +1618,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
       recv_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, E.hist);
       lookup_kernel<<<1, 32, 0, s>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, E.V, E.cum, nullptr,
                                      d_hit);
-      send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 0, E.send_counter);
+      send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 0, E.send_counter);
       recv_peer_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox);
       KCHECK();
       E.launches += 4;
@@ -1632,7 +1637,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
       if (!hit) {  // SamePrimaryJIT re-draft (sim.cpp:229-232), identical on every speculator; rank 0 sends
         const long long before = E.launches;
         draft_steps(E, K, c->scheme, 1, 2, s);
-        send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, n_spec, rank, E.V, 1, E.send_counter);
+        send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter);
         KCHECK();
         jit_launches += E.launches - before + 1;
       }

@@ -33,7 +33,9 @@ struct alignas(128) MsgD2V {
 };
 
 // Header of every process's inbox; the verifier's draft-row payload
-// [K][V] fp32 follows at kInboxRows bytes.
+// [2][K][V] fp32 (double-buffered by sequence parity: the ranks of a
+// tensor-parallel verifier may still read round r's rows while round r + 1's
+// arrive) follows at kInboxRows bytes.
 // Speculator slots are double-buffered by sequence parity, with credit flow
 // control: a speculator publishes `done` (the sequence number of its last
 // finished round) and a sender overwrites a slot only once the message that
@@ -86,10 +88,12 @@ __device__ bool wait_seq(const int* seq, int want, LoopState* st) {
 
 // Verifier: wait for the speculation of round st->round and install it
 // (the verifier-side half of Channel::send_speculations, sim.cpp:275-288).
-__global__ void recv_spec_kernel(LoopState* st, const Inbox* in, const float* rows, int V) {
+__global__ void recv_spec_kernel(LoopState* st, const Inbox* in, const float* rows2, int V) {
   if (threadIdx.x != 0 || st->error) return;
-  if (!wait_seq(&in->d2v.seq, st->seq_base + st->round + 1, st)) return;
+  const int seq = st->seq_base + st->round + 1;
+  if (!wait_seq(&in->d2v.seq, seq, st)) return;
   const int K = st->K;
+  const float* rows = rows2 + size_t(seq & 1) * K * V;
   st->spec_origin = in->d2v.origin;
   st->spec_src = in->d2v.src;
   st->spec_uniform = in->d2v.uniform;
@@ -148,11 +152,13 @@ __global__ void recv_outcome_kernel(LoopState* st, const Inbox* in, int* hist) {
 // backup (every speculator computes the identical backup) or the initial /
 // JIT draft (force). Rows [K][V] are copied by all CTAs; the last CTA to
 // finish publishes the header (release) so the rows are visible first.
-// peers[0] = verifier inbox, peers[1..G] = speculator inboxes.
-__global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* const* peers, int G, int rank, int V,
-                                                        int force, int* counter) {
+// peers[0..T) = verifier inboxes (the ranks of a tensor-parallel verifier
+// all verify the same speculation), peers[T..T+G) = speculator inboxes.
+__global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* const* peers, int T, int G, int rank,
+                                                        int V, int force, int* counter) {
   __shared__ int s_send, s_last;
   const int K = st->K;
+  const int rslot = (st->seq_base + st->round + 1) & 1;  // rows slot of this message
   if (threadIdx.x == 0) {
     int send = 0;
     if (!st->error && st->round < st->rounds) {
@@ -164,15 +170,15 @@ __global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* co
   }
   __syncthreads();
   if (!s_send) return;
-  Inbox* vin = peers[0];
-  float* dst = reinterpret_cast<float*>(reinterpret_cast<char*>(vin) + kInboxRows);
   if (!st->spec_uniform) {
     const size_t n4 = size_t(V) / 4;  // V % 4 == 0 (checked on the host)
     for (int i = 0; i < K; ++i) {
       const float4* src = reinterpret_cast<const float4*>(st->spec_rows[i]);
-      float4* d = reinterpret_cast<float4*>(dst + size_t(i) * V);
-      for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < n4; j += size_t(gridDim.x) * blockDim.x)
-        d[j] = src[j];
+      for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < n4; j += size_t(gridDim.x) * blockDim.x) {
+        const float4 v = src[j];
+        for (int vr = 0; vr < T; ++vr)
+          reinterpret_cast<float4*>(reinterpret_cast<char*>(peers[vr]) + kInboxRows)[(size_t(rslot) * K + i) * (V / 4) + j] = v;
+      }
     }
   }
   __threadfence_system();
@@ -188,27 +194,30 @@ __global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* co
   m.src = st->spec_src;
   m.uniform = st->spec_uniform;
   for (int i = 0; i < K; ++i) m.tokens[i] = st->spec[i];
-  vin->d2v.origin = m.origin;
-  vin->d2v.src = m.src;
-  vin->d2v.uniform = m.uniform;
-  for (int i = 0; i < K; ++i) vin->d2v.tokens[i] = m.tokens[i];
+  for (int vr = 0; vr < T; ++vr) {
+    Inbox* vin = peers[vr];
+    vin->d2v.origin = m.origin;
+    vin->d2v.src = m.src;
+    vin->d2v.uniform = m.uniform;
+    for (int i = 0; i < K; ++i) vin->d2v.tokens[i] = m.tokens[i];
+  }
   const bool bcast = !force && st->hit;  // others lack this branch's tokens
   if (bcast)
     for (int g = 0; g < G; ++g) {
       if (g == rank) continue;
       // slot seq & 1 last carried seq - 2, read in speculator g's round done = seq - 3
-      if (!wait_seq(&peers[1 + g]->credit.done, seq - 3, st)) return;
-      MsgD2V& p = peers[1 + g]->peer[seq & 1];
+      if (!wait_seq(&peers[T + g]->credit.done, seq - 3, st)) return;
+      MsgD2V& p = peers[T + g]->peer[seq & 1];
       p.origin = m.origin;
       p.src = m.src;
       p.uniform = m.uniform;
       for (int i = 0; i < K; ++i) p.tokens[i] = m.tokens[i];
     }
   __threadfence_system();
-  st_release_sys(&vin->d2v.seq, seq);
+  for (int vr = 0; vr < T; ++vr) st_release_sys(&peers[vr]->d2v.seq, seq);
   if (bcast)
     for (int g = 0; g < G; ++g)
-      if (g != rank) st_release_sys(&peers[1 + g]->peer[seq & 1].seq, seq);
+      if (g != rank) st_release_sys(&peers[T + g]->peer[seq & 1].seq, seq);
 }
 
 // Speculator that does not own the hit slot: take the next speculation's

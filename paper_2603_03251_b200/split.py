@@ -20,13 +20,14 @@ from .api import ConfigError, Engine, Pair, RunStats, SimConfig
 VERIFIER_RANK = 0
 
 
-def role_of(rank: int, world_size: int) -> int:
-    """Rank 0 verifies; every other rank speculates."""
-    if world_size < 2:
-        raise ConfigError("split: needs at least 2 processes (1 verifier + >= 1 speculator)")
+def role_of(rank: int, world_size: int, tp: int = 1) -> int:
+    """Ranks [0, tp) verify (a tensor-parallel verifier when tp > 1); every
+    other rank speculates."""
+    if tp < 1 or world_size < tp + 1:
+        raise ConfigError("split: needs the verifier ranks + at least one speculator")
     if not 0 <= rank < world_size:
         raise ConfigError("split: rank out of range")
-    return N.ROLE_VERIFIER if rank == VERIFIER_RANK else N.ROLE_SPECULATOR
+    return N.ROLE_VERIFIER if rank < tp else N.ROLE_SPECULATOR
 
 
 def branch_block(B: int, rank: int, G: int) -> tuple[int, int]:
@@ -60,16 +61,21 @@ COUNTERS = ("rounds", "tokens", "virtual_time", "primary_origin_lookups", "prima
             "hit_round_tokens", "miss_round_tokens", "accepted_sum")
 
 
-def merge_stats(per_rank: Sequence[dict]) -> dict:
-    """RunStats of a split run from every rank's own counters ([verifier,
-    speculator 0, ...]). The verifier knows tokens / accepted; each
-    speculator rebuilds the same history from (k*, t*) and keeps the lookup /
-    hit / clock counters, so every counter must agree across speculators and
+def merge_stats(per_rank: Sequence[dict], tp: int = 1) -> dict:
+    """RunStats of a split run from every rank's own counters ([verifier
+    ranks 0..tp-1, speculator 0, ...]). The verifier knows tokens / accepted;
+    each speculator rebuilds the same history from (k*, t*) and keeps the
+    lookup / hit / clock counters, so every counter must agree across
+    speculators (and across the ranks of a tensor-parallel verifier), and
     tokens / accepted with the verifier. Device time = the slowest rank."""
-    if len(per_rank) < 2:
+    if len(per_rank) < tp + 1:
         raise ConfigError("split: need the verifier and at least one speculator")
-    v, s0 = per_rank[0], per_rank[1]
-    for s in per_rank[2:]:
+    v, s0 = per_rank[0], per_rank[tp]
+    for vr in per_rank[1:tp]:
+        for k in ("tokens", "accepted_sum", "rounds"):
+            if vr[k] != v[k]:
+                raise ConfigError(f"split: tensor-parallel verifier ranks disagree on {k}")
+    for s in per_rank[tp + 1:]:
         for k in COUNTERS:
             if s[k] != s0[k]:
                 raise ConfigError(f"split: speculators disagree on {k}")
@@ -97,33 +103,42 @@ class SplitEngine:
     rounds of the protocol."""
 
     def __init__(self, target, draft, pair: Pair = Pair(), device: int = 0, max_branches: int = 64,
-                 max_lookahead: int = 8, group=None):
+                 max_lookahead: int = 8, group=None, tp: int = 1):
+        """tp > 1: ranks [0, tp) form a tensor-parallel verifier (tp.cuh)."""
         import torch.distributed as dist
         self.group = group
+        self.tp = tp
         self.rank = dist.get_rank(group)
         self.world_size = dist.get_world_size(group)
-        self.role = role_of(self.rank, self.world_size)
+        self.role = role_of(self.rank, self.world_size, tp)
+        vrank = self.rank if self.role == N.ROLE_VERIFIER else 0
         self.engine = Engine(target, draft, pair, device=device, max_branches=max_branches,
-                             max_lookahead=max_lookahead, role=self.role)
+                             max_lookahead=max_lookahead, role=self.role, tp_rank=vrank,
+                             tp_size=tp if self.role == N.ROLE_VERIFIER else 1)
+        if tp > 1:  # map the verifier ranks' collective regions
+            mine = self.engine.tp_handle() if self.role == N.ROLE_VERIFIER else bytes(N.MAILBOX_HANDLE_BYTES)
+            tph = exchange_handles(mine, group)
+            if self.role == N.ROLE_VERIFIER:
+                self.engine.tp_connect(tph[:tp])
         handles = exchange_handles(self.engine.mailbox_handle(), group)
         self.engine.connect(handles, self.rank)
         dist.barrier(group)  # every inbox is mapped and clean before anyone sends
 
     @property
     def n_spec(self) -> int:
-        return self.world_size - 1
+        return self.world_size - self.tp
 
     def run(self, prompt: Sequence[int], cfg: SimConfig) -> SplitRun:
         import torch.distributed as dist
         if self.role == N.ROLE_VERIFIER:
             r = self.engine.run_ssd_verifier(prompt, cfg, self.n_spec)
         else:
-            r = self.engine.run_ssd_speculator(prompt, cfg, self.rank - 1, self.n_spec)
+            r = self.engine.run_ssd_speculator(prompt, cfg, self.rank - self.tp, self.n_spec, self.tp)
         fields = [f for f, _ in N.RunStatsC._fields_]
         mine = {f: getattr(r, f) for f in fields}
         allst: list = [None] * self.world_size
         dist.all_gather_object(allst, mine, group=self.group)
-        merged = merge_stats(allst) if self.rank == VERIFIER_RANK else None
+        merged = merge_stats(allst, self.tp) if self.rank == VERIFIER_RANK else None
         return SplitRun(self.rank, self.world_size, r, merged, r.streams[0] if r.streams else None)
 
     def close(self):

@@ -34,7 +34,7 @@ def _prompt():
     return np.random.default_rng(11).integers(0, 32000, 10).tolist()
 
 
-def _worker(rank, world, port, temperature, backup, runs, q):
+def _worker(rank, world, port, temperature, backup, runs, q, tp=1):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -44,7 +44,7 @@ def _worker(rank, world, port, temperature, backup, runs, q):
         from paper_2603_03251_b200.configs import shapes
         from paper_2603_03251_b200.split import SplitEngine
         ts, ds = shapes("tiny", max_ctx=512)
-        se = SplitEngine(ts, ds, P.Pair(), device=0, max_branches=16, max_lookahead=4)
+        se = SplitEngine(ts, ds, P.Pair(), device=0, max_branches=16, max_lookahead=4, tp=tp)
         out = []
         for _ in range(runs):  # repeated runs reuse the mapped mailboxes (monotonic sequence numbers)
             r = se.run(_prompt(), _cfg(P, temperature, backup))
@@ -52,16 +52,19 @@ def _worker(rank, world, port, temperature, backup, runs, q):
         se.close()
         q.put((rank, "ok", out))
     except Exception as e:  # surface the failure in the parent
+        import sys
+        import traceback
+        traceback.print_exc(file=sys.stderr)
         q.put((rank, f"{type(e).__name__}: {e}", None))
     finally:
         dist.destroy_process_group()
 
 
-def _split(world, temperature, backup, runs=1):
+def _split(world, temperature, backup, runs=1, tp=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, temperature, backup, runs, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, temperature, backup, runs, q, tp)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -109,3 +112,19 @@ def test_split_run_matches_colocated_harness(colocated, world, temperature, back
         assert res[rank][1][0][2] == ref.hits.tolist()
     # a second run over the same mapped mailboxes is identical
     assert res[0][1][1][0] == tokens
+
+
+@pytest.mark.parametrize("world,tp,temperature", [(3, 2, 0.0), (4, 2, 1.0)])
+def test_split_run_with_tensor_parallel_verifier(colocated, world, tp, temperature):
+    """TP=2 verifier + (world - 2) speculators: the greedy stream equals the
+    colocated harness; in sampled mode the TP logits differ from the
+    unsharded ones by fp32 summation order only, so only self-consistency
+    and sanity are required."""
+    res = _split(world, temperature, "fast_random", runs=1, tp=tp)
+    tokens, merged, _ = res[0][1][0]
+    assert res[1][1][0][0] == tokens  # both verifier ranks emit the same stream
+    assert merged["tokens"] == len(tokens) and merged["rounds"] == ROUNDS
+    if temperature == 0.0:
+        ref = colocated(temperature, "fast_random")
+        assert tokens == ref.streams[0]
+        assert merged["primary_origin_hits"] + merged["backup_origin_hits"] == ref.hits_total()

@@ -13,6 +13,9 @@ from paper_2603_03251_b200.api import ConfigError
 
 
 def test_roles():
+    assert [split.role_of(r, 5, tp=2) for r in range(5)] == [N.ROLE_VERIFIER] * 2 + [N.ROLE_SPECULATOR] * 3
+    with pytest.raises(ConfigError):
+        split.role_of(0, 2, tp=2)
     assert split.role_of(0, 2) == N.ROLE_VERIFIER
     assert [split.role_of(r, 4) for r in range(1, 4)] == [N.ROLE_SPECULATOR] * 3
     with pytest.raises(ConfigError):
@@ -54,6 +57,10 @@ def test_merge_stats():
         split.merge_stats([v, s, _stats(tokens=30, accepted_sum=20.0, rounds=10, primary_origin_hits=6)])
     with pytest.raises(ConfigError):
         split.merge_stats([_stats(tokens=31, accepted_sum=20.0, rounds=10), s])
+    # tensor-parallel verifier ranks must agree
+    assert split.merge_stats([v, dict(v), s], tp=2)["primary_origin_hits"] == 7
+    with pytest.raises(ConfigError):
+        split.merge_stats([v, _stats(tokens=29, accepted_sum=20.0, rounds=10), s], tp=2)
 
 
 def _free_port():
