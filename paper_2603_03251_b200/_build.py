@@ -11,7 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libssd_b200.so")
 SOURCES = ["engine.cu", "plans.cpp"]
-DEPS = SOURCES + ["common.cuh", "kernels.cuh", "gemm_tc.cuh"]
+DEPS = SOURCES + ["common.cuh", "kernels.cuh", "gemm_tc.cuh", "rowops.cuh", "probe.cuh", "split.cuh", "tp.cuh",
+                  "attn_cl.cuh", "fwd_mk.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
@@ -34,6 +35,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
     return LIB
+
+
+def build_variant(name: str, defines: list[str], verbose: bool = False) -> str:
+    """A profiling variant of the library (e.g. -DSSD_KTL=1 kernel timeline),
+    loaded with SSD_B200_LIB=<path>; never the product build."""
+    out = os.path.join(HERE, f"libssd_b200_{name}.so")
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    return out
 
 
 if __name__ == "__main__":

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
   uint64_t* bar = reinterpret_cast<uint64_t*>(res + G * (hd + 2) + 2);
   bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bar) + 15) & ~uintptr_t(15));
 
+  KTL_ENTER(3);
   const int chunk = blockIdx.x, kvh = blockIdx.y, m = blockIdx.z, tid = threadIdx.x;
   const int nch = gridDim.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -74,12 +75,15 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
   }
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  KTL_READY();
+  KTL_SUB(0);
 
   const size_t row_len = size_t(H + 2 * KVH) * hd;
   const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
   const int nk = main_len + blen;
   const int j1 = min(nk, j0 + kAttnChunk);
   tc::mbar_wait(bar, 0);
+  KTL_SUB(1);
   if (j0 < j1) {
     // 1) branch-local keys of this chunk (j >= main_len) from their slots
     for (int e = tid; e < (j1 - max(j0, main_len)) * (hd >> 3); e += kAttnThreads) {
@@ -123,27 +127,13 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
       }
     }
     __syncthreads();
-    // 4) scores: one key per thread, K row from shared memory
+    KTL_SUB(2);
+    // 4) scores from the staged K rows (lane-cooperative, conflict-free)
     const int n = j1 - j0;
-    if (tid < n) {
-      const uint4* kr = reinterpret_cast<const uint4*>(Ks + size_t(tid) * hd);
-      float dot[G];
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) dot[gg] = 0.f;
-      for (int u = 0; u < (hd >> 3); ++u) {
-        float f[8];
-        bf16x8_to_f32(kr[u], f);
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          const float* qq = qs + gg * hd + u * 8;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dot[gg] += qq[i] * f[i];
-        }
-      }
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + tid] = dot[gg] * scale;
-    }
+    attn_scores<G>(qs, sc, n, hd, scale, warp, lane,
+                   [&](int jj) { return reinterpret_cast<const uint4*>(Ks + size_t(jj) * hd); });
     __syncthreads();
+    KTL_SUB(3);
     // 5) chunk softmax statistics (warp gg -> head gg)
     for (int gg = warp; gg < G; gg += kAttnThreads / 32) {
       float mx = -INFINITY;
@@ -193,8 +183,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
     res[tid * (hd + 2) + hd] = -INFINITY;
     res[tid * (hd + 2) + hd + 1] = 0.f;
   }
+  KTL_SUB(4);
   // 7) merge the cluster's chunks in chunk order (rank 0, over DSMEM)
   cluster.sync();
+  KTL_SUB(5);
   if (chunk == 0) {
     for (int e = tid; e < G * hd; e += kAttnThreads) {
       const int gg = e / hd, dd = e % hd;
@@ -215,7 +207,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
       out[size_t(m) * H * hd + size_t(kvh * G + gg) * hd + dd] = __float2bfloat16_rn(o / den);
     }
   }
+  KTL_SUB(6);
   cluster.sync();  // keep every rank's shared memory alive until rank 0 has read it
+  KTL_SUB(7);
+  KTL_EXIT();
 }
 
 }  // namespace ssd

@@ -80,6 +80,46 @@ __device__ inline VI block_best(VI a, VI* sh) {
   return warp_best(r);
 }
 
+// ----------------------------------------------------------- kernel timeline
+// Profiling build only (-DSSD_KTL=1, scripts/ktl.py): block 0 of every
+// decode-step kernel records (kind, entry, after-PDL-wait, exit) globaltimer
+// stamps, to see the real (PDL-overlapped, graph-launched) step timeline.
+#ifndef SSD_KTL
+#define SSD_KTL 0
+#endif
+#if SSD_KTL
+__device__ unsigned long long g_ktl[16384][4];
+__device__ unsigned g_ktl_n;
+__device__ __forceinline__ unsigned long long ktl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool ktl_lead() {
+  return blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0;
+}
+#define KTL_ENTER(kind)                                   \
+  unsigned ktl_slot_ = 0xffffffffu;                       \
+  if (ktl_lead()) {                                       \
+    ktl_slot_ = atomicAdd(&g_ktl_n, 1u) & 16383u;         \
+    g_ktl[ktl_slot_][0] = (kind);                         \
+    g_ktl[ktl_slot_][1] = ktl_now();                      \
+  }
+#define KTL_READY() \
+  if (ktl_slot_ != 0xffffffffu) g_ktl[ktl_slot_][2] = ktl_now();
+#define KTL_EXIT() \
+  if (ktl_slot_ != 0xffffffffu) g_ktl[ktl_slot_][3] = ktl_now();
+// sub-phase stamps of the last launch of an instrumented kernel (block 0)
+__device__ unsigned long long g_ktl_sub[16];
+#define KTL_SUB(i) \
+  if (ktl_lead()) g_ktl_sub[i] = ktl_now();
+#else
+#define KTL_SUB(i)
+#define KTL_ENTER(kind)
+#define KTL_READY()
+#define KTL_EXIT()
+#endif
+
 // ----------------------------------------------------------- mt19937_64
 // std::mt19937_64 (fully specified by the C++ standard); the device copy of
 // the reference's rng::Stream (rng.hpp:32-48).

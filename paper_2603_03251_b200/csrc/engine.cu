@@ -1100,7 +1100,8 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   if (draft->d_model > target->d_model || draft->ffn > target->ffn || !draft->tied)
     throw Fail(SSD_CONFIG, "engine: the draft must be tied and no wider than the target");
   for (const ssd_model_shape* s : {target, draft}) {
-    if (s->head_dim % 16 || s->head_dim > 128 || s->n_heads % s->n_kv_heads || s->d_model % 8 || s->ffn % 8)
+    if (s->head_dim < 16 || s->head_dim > 128 || (s->head_dim & (s->head_dim - 1)) || s->n_heads % s->n_kv_heads ||
+        s->d_model % 8 || s->ffn % 8)
       throw Fail(SSD_CONFIG, "engine: unsupported shape");
   }
   if (max_lookahead < 1 || max_lookahead > kMaxK) throw Fail(SSD_TOO_LARGE, "engine: lookahead capacity");
@@ -1952,6 +1953,26 @@ int ssd_debug_mk_trace(ssd_engine* h, int which, int M, int pos, unsigned long l
     g_last_error = x.what();
     return -1;
   }
+}
+
+// Kernel timeline (profiling build -DSSD_KTL=1): copies up to n records
+// (kind, entry, ready, exit) and resets the ring; returns the count.
+int ssd_debug_ktl(unsigned long long* out, int n) {
+#if SSD_KTL
+  unsigned cnt = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  cudaMemcpyFromSymbol(&cnt, g_ktl_n, sizeof(cnt));
+  const int m = std::min<int>(n, std::min<unsigned>(cnt, 16384u));
+  cudaMemcpyFromSymbol(out, g_ktl, size_t(m) * 4 * sizeof(unsigned long long));
+  const unsigned zero = 0;
+  cudaMemcpyToSymbol(g_ktl_n, &zero, sizeof(zero));
+  if (n >= m + 4) cudaMemcpyFromSymbol(out + size_t(m) * 4, g_ktl_sub, 16 * sizeof(unsigned long long));
+  return m;
+#else
+  (void)out;
+  (void)n;
+  return -1;
+#endif
 }
 
 int ssd_debug_mk_diag(unsigned long long* out /* 8 + 8 * 256 */) {

@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int s_last;
 
+  KTL_ENTER(10 + EPI);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (g.N + kBM - 1) / kBM;
   const long long U = (long long)tiles * g.KU, P = gridDim.x;
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       TRACE(0, i);
     }
     pdl_wait();  // activations are produced by the previous kernel
+    KTL_READY();
     for (int i = 0; i < pre; ++i) {
       const int kb = ((u0 + i) % g.KU) * kKPS;
 #pragma unroll
@@ -449,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
   if (threadIdx.x == 0) TRACE(4, 1);
+  KTL_EXIT();
 }
 
 }  // namespace tc

@@ -192,15 +192,18 @@ constexpr int kPfUnitBytes = 32768;  // GEMM unit = 2 k-blocks of 128 x 64 bf16 
 // x[m][:] = E[token_m][:] (fp32 residual stream); E row-major or pre-tiled.
 __global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const FwdParams* __restrict__ P,
                              float* __restrict__ x, Prefetch pf) {
+  KTL_ENTER(1);
   prefetch_window(pf, kPfUnitBytes);
   asm volatile("griddepcontrol.launch_dependents;");
   pdl_wait_all();
+  KTL_READY();
   const int m = blockIdx.x;
   const size_t tok = size_t(P->tokens[m]);
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const size_t at = tiled ? tiled_at(tok, size_t(i), size_t(d) / 64) : tok * size_t(d) + size_t(i);
     x[size_t(m) * d + i] = __bfloat162float(E[at]);
   }
+  KTL_EXIT();
 }
 
 // Residual add + RMSNorm (gain optional) with bf16 rounding of the output:
@@ -214,11 +217,13 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
                                                                int d, const float* __restrict__ g, float eps,
                                                                bf16* __restrict__ out, Prefetch pf) {
   __shared__ float sh[32];
+  KTL_ENTER(2);
   prefetch_window(pf, kPfUnitBytes);
   // let the next kernel (a GEMM) launch now and prefetch its weights; it
   // still waits for this grid, which waits for its own predecessor
   asm volatile("griddepcontrol.launch_dependents;");
   pdl_wait_all();
+  KTL_READY();
   const int m = blockIdx.x;
   float4* xr = reinterpret_cast<float4*>(x + size_t(m) * d);
   const float4* dr = delta ? reinterpret_cast<const float4*>(delta + size_t(m) * d) : nullptr;
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
     o2[2 * i] = __floats2bfloat162_rn(a, b);
     o2[2 * i + 1] = __floats2bfloat162_rn(c, e);
   }
+  KTL_EXIT();
 }
 
 enum Epi { EPI_STORE = 0, EPI_RESID = 1, EPI_SWIGLU = 2 };
@@ -276,6 +282,45 @@ struct AttnWs {
   float* part;   // [M][KVH][chunks][G][hd + 2]
   int* counter;  // [M][KVH]
 };
+
+// Scores of one key chunk for the G query heads of a KV group: the hd/8
+// 16-byte chunks of a K row are spread over hd/8 lanes (a warp covers
+// 32/(hd/8) keys per step, its reads one contiguous run — conflict-free in
+// shared memory, coalesced in global), partial dot products reduced with
+// xor shuffles. rowp(jj) -> the K row of key jj of the chunk. hd: 16..128,
+// a power of two.
+template <int G, class RowPtr>
+__device__ __forceinline__ void attn_scores(const float* qs, float* sc, int n, int hd, float scale, int warp, int lane,
+                                            RowPtr rowp) {
+  const int cpr = hd >> 3;
+  const int kpi = 32 / cpr;
+  const int sub = lane / cpr, ch = lane % cpr;
+  float qv[G][8];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[gg][i] = qs[gg * hd + ch * 8 + i];
+  for (int jb = warp * kpi; jb < n; jb += (kAttnThreads / 32) * kpi) {
+    const int jj = jb + sub;
+    float part[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) part[gg] = 0.f;
+    if (jj < n) {
+      float f[8];
+      bf16x8_to_f32(rowp(jj)[ch], f);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part[gg] += qv[gg][i] * f[i];
+    }
+    for (int o = cpr >> 1; o > 0; o >>= 1)
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) part[gg] += __shfl_xor_sync(0xffffffffu, part[gg], o);
+    if (ch == 0 && jj < n)
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + jj] = part[gg] * scale;
+  }
+}
 
 // Shared-memory scratch of one attention work item (kAttnSmemFloats(G, hd)
 // floats + one int); static in attention_kernel, carved from the dynamic
@@ -358,43 +403,14 @@ __device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __rest
       }
     }
     sync();
-    // 3) scores: one key per thread; the whole K row is loaded up front
-    //    (hd/8 independent 16-byte loads in flight per thread)
+    // 3) scores, lane-cooperative (attn_scores): coalesced K row reads
     const bf16* kbase = kc + size_t(kvh) * S * hd;
     const bf16* vbase = vc + size_t(kvh) * S * hd;
-    {
-      const int j = j0 + tid;
-      if (j < j1) {
-        const int slot = j < main_len ? j : bbase + (j - main_len);
-        const uint4* kr = reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
-        uint4 kv[16];
-        const int nv = hd >> 3;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (u < nv) kv[u] = kr[u];
-        float dot[kMaxGroup];
-        
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) dot[gg] = 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          if (u < nv) {
-            float f[8];
-            bf16x8_to_f32(kv[u], f);
-            
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-              const float* qq = qs + gg * hd + u * 8;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) dot[gg] += qq[i] * f[i];
-            }
-          }
-        }
-        
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) sc[gg * kAttnChunk + tid] = dot[gg] * scale;
-      }
-    }
+    attn_scores<G>(qs, sc, j1 - j0, hd, scale, warp, lane, [&](int jj) {
+      const int j = j0 + jj;
+      const int slot = j < main_len ? j : bbase + (j - main_len);
+      return reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
+    });
     sync();
     // 4) chunk softmax statistics (warp gg -> head gg)
     const int n = j1 - j0;

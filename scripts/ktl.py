@@ -1,0 +1,67 @@
+"""Real (PDL-overlapped) timeline of decode-step kernels from the profiling
+build (-DSSD_KTL=1): block 0 of each kernel stamps entry / after-PDL-wait /
+exit. Usage: python scripts/ktl.py [t1|d1|d20 ...] (builds the variant)."""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["SSD_B200_LIB"] = os.path.join(ROOT, "paper_2603_03251_b200", "libssd_b200_ktl.so")  # before the import
+from paper_2603_03251_b200 import _build  # noqa: E402
+
+if not os.path.exists(os.environ["SSD_B200_LIB"]):
+    _build.build_variant("ktl", ["SSD_KTL=1"])
+import numpy as np  # noqa: E402
+
+import paper_2603_03251_b200 as P  # noqa: E402
+from paper_2603_03251_b200.configs import shapes  # noqa: E402
+
+KIND = {1: "embed", 2: "rmsnorm", 3: "attention", 10: "gemm", 12: "gemm_swiglu"}
+ts, ds = shapes("llama8b_1b", max_ctx=1024)
+eng = P.Engine(ts, ds, P.Pair(), max_branches=20, max_lookahead=4)
+lib = P._native.load()
+lib.ssd_debug_ktl.restype = ctypes.c_int
+buf = (ctypes.c_ulonglong * (16384 * 4))()
+for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
+    which, M = (0 if w[0] == "t" else 1), int(w[1:])
+    eng.profile_forward(which, M, 128, 2)
+    lib.ssd_debug_ktl(buf, 16384)  # reset
+    eng.profile_forward(which, M, 128, 1)  # warm forward + gemms + forward + gemms
+    n = lib.ssd_debug_ktl(buf, 16384)
+    assert n > 0, f"no timeline records ({n}): not the SSD_KTL build?"
+    sub = np.array(buf[n * 4: n * 4 + 16], dtype=np.float64)
+    t = np.array(buf[: n * 4], dtype=np.float64).reshape(n, 4)
+    t = t[np.argsort(t[:, 1])]
+    # the last full forward: from the last embed to the next embed / end, cut at the GEMM-only pass
+    emb = np.nonzero(t[:, 0] == 1)[0]
+    f = t[emb[-1]:]
+    n_gemm = 4 * (ts.n_layers if which == 0 else ds.n_layers) + 1
+    k, g = 0, 0
+    while k < len(f) and g < n_gemm:
+        g += f[k, 0] >= 10
+        k += 1
+    f = f[:k]
+    t0 = f[0, 1]
+    print(f"== {w}: {len(f)} kernels, block-0 span {(f[-1, 3] - t0) / 1e3:.1f} us")
+    agg = {}
+    prev_exit = None
+    for r in f:
+        kind = KIND.get(int(r[0]), str(int(r[0])))
+        wait = (r[2] - r[1]) / 1e3
+        work = (r[3] - r[2]) / 1e3
+        gap = (r[1] - prev_exit) / 1e3 if prev_exit is not None else 0.0
+        a = agg.setdefault(kind, [0, 0.0, 0.0, 0.0])
+        a[0] += 1; a[1] += wait; a[2] += work; a[3] += gap
+        prev_exit = r[3]
+    for kind, a in agg.items():
+        print(f"   {kind:12s} n={a[0]:4d} entry->ready {a[1] / a[0]:7.2f} us  ready->exit(block0) {a[2] / a[0]:7.2f} us  "
+              f"prev-exit->entry {a[3] / a[0]:7.2f} us")
+    print("   last attention sub-phases (us from ready): mbar %.2f append+rope %.2f scores %.2f softmax+PV %.2f "
+          "cluster.sync %.2f merge %.2f final sync %.2f" % tuple((sub[i] - sub[0]) / 1e3 for i in range(1, 8)))
+    for r in f[:14]:
+        print(f"      {KIND.get(int(r[0]), int(r[0])):12s} entry {(r[1] - t0) / 1e3:8.2f} ready {(r[2] - t0) / 1e3:8.2f} "
+              f"exit {(r[3] - t0) / 1e3:8.2f}")
+eng.close()
+
+    # (printed per workload above) -- attention sub-phases of the last launch
