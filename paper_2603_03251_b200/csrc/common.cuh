@@ -111,6 +111,8 @@ __device__ __forceinline__ bool ktl_lead() {
   if (ktl_slot_ != 0xffffffffu) g_ktl[ktl_slot_][3] = ktl_now();
 // sub-phase stamps of the last launch of an instrumented kernel (block 0)
 __device__ unsigned long long g_ktl_sub[16];
+// per-CTA (ready, MMA done, exit) stamps of the last 64 GEMM launches
+__device__ unsigned long long g_ktl_cta[64][160][8];
 #define KTL_SUB(i) \
   if (ktl_lead()) g_ktl_sub[i] = ktl_now();
 #else

@@ -468,7 +468,8 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
   const int cap = m.gemm_ctas > 0 ? std::min(m.gemm_ctas, E_num_sms) : E_num_sms * SSD_GEMM_CTAS_PER_SM;
   const int grid = std::min(units, cap);
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
-  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf};
+  static int dbg_seq = 0;
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++};
   launch_pdl(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP),
              g);
 }
@@ -1967,6 +1968,8 @@ int ssd_debug_ktl(unsigned long long* out, int n) {
   const unsigned zero = 0;
   cudaMemcpyToSymbol(g_ktl_n, &zero, sizeof(zero));
   if (n >= m + 4) cudaMemcpyFromSymbol(out + size_t(m) * 4, g_ktl_sub, 16 * sizeof(unsigned long long));
+  if (n >= m + 4 + 64 * 160 * 8)
+    cudaMemcpyFromSymbol(out + size_t(m) * 4 + 16, g_ktl_cta, size_t(64) * 160 * 8 * sizeof(unsigned long long));
   return m;
 #else
   (void)out;
@@ -1979,6 +1982,31 @@ int ssd_debug_mk_diag(unsigned long long* out /* 8 + 8 * 256 */) {
   if (!g_diag_host) return -1;
   std::memcpy(out, g_diag_host, (8 + 8 * 256) * sizeof(unsigned long long));
   return 0;
+}
+
+// tcgen05 rate probe (profiling): cycles for `iters` units of 8 MMAs at N = np.
+int ssd_debug_mma_rate(int np, int iters, unsigned long long* out) {
+  try {
+    unsigned long long* d = dalloc<unsigned long long>(2);
+    auto run = [&](auto kern, size_t smem) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      kern<<<1, 64, smem>>>(iters, d);
+      KCHECK();
+    };
+    const size_t extra = 1024 + tc::kABytes + 64;
+    if (np == 16) run(mma_rate_probe<16>, extra + tc::Cfg<16>::kBBytes);
+    else if (np == 32) run(mma_rate_probe<32>, extra + tc::Cfg<32>::kBBytes);
+    else if (np == 64) run(mma_rate_probe<64>, extra + tc::Cfg<64>::kBBytes);
+    else if (np == 128) run(mma_rate_probe<128>, extra + tc::Cfg<128>::kBBytes);
+    else run(mma_rate_probe<256>, extra + tc::Cfg<256>::kBBytes);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, d, 16, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return 0;
+  } catch (const std::exception& x) {
+    g_last_error = x.what();
+    return -1;
+  }
 }
 
 ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {

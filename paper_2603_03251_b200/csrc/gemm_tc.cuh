@@ -209,6 +209,7 @@ struct GemmArgs {
   // prefetch_window), issued once this CTA's own weight stream is issued:
   // it covers the drain / epilogue / next-launch gap.
   Prefetch pf;
+  int dbg_seq;  // profiling build: launch sequence number (per-CTA timeline)
 };
 
 template <int EPI>
@@ -309,6 +310,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
     pdl_wait();  // activations are produced by the previous kernel
     KTL_READY();
+#if SSD_KTL
+    if (blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][0] = ktl_now();
+#endif
     for (int i = 0; i < pre; ++i) {
       const int kb = ((u0 + i) % g.KU) * kKPS;
 #pragma unroll
@@ -360,8 +364,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       }
       mma_commit(&empty[s]);
       TRACE(2, i);
+#if SSD_KTL
+      if (i + 1 == u1 - u0 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][1] = ktl_now();
+#endif
       const bool last = (u + 1 == u1) || ((u + 1) / g.KU != t);
       if (last) mma_commit(&tfull[seg & 1]);
+#if SSD_KTL
+      if (last && u + 1 == u1 && blockIdx.x < 160) {  // profiling: when the accumulator is complete
+        mbar_wait(&tfull[seg & 1], (seg >> 1) & 1);
+        g_ktl_cta[g.dbg_seq & 63][blockIdx.x][7] = ktl_now();
+      }
+#endif
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: TMEM lanes (warp % 4) * 32 + lane
@@ -379,6 +392,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       if (lane == 0) mbar_sleep_wait(&tfull[b], (seg >> 1) & 1);
       __syncwarp();
       mbar_wait(&tfull[b], (seg >> 1) & 1);
+#if SSD_KTL
+      if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][3] = ktl_now();
+#endif
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(b * C::kAccCols);
       const int r = t * kBM + rl;
@@ -401,15 +417,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           else if (c + j < g.M) part[size_t(c + j) * kBM + rl] = f;
         }
       }
+#if SSD_KTL
+      if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][4] = ktl_now();
+#endif
       if (!whole) {
         // last-arriving segment of tile t reduces the partials in CTA order
         const int cf = cta_of(t * g.KU, U, P), cl = cta_of((t + 1) * g.KU - 1, U, P);
-        __threadfence();
+        // The CTA barrier orders the 128 threads' partial stores before the
+        // arrival; one acq_rel atomic (cumulative release of those stores,
+        // acquire of the other contributors') replaces two full fences.
+        // (Deferring the ticket past the next segment's drain was measured
+        // slower: profiles/r01_summary.md.)
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) s_last = atomicAdd(&g.counters[t], 1) == (cl - cf);
+        if (threadIdx.x == 64) {
+          int old;
+          asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&g.counters[t]) : "memory");
+          s_last = old == (cl - cf);
+        }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+#if SSD_KTL
+        if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][5] = ktl_now();
+#endif
         if (s_last) {
-          __threadfence();
           // only the first contributing CTA can start before the tile
           const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KU ? 0 : 1);
           // All partial loads of a (16 contributors x 4 tokens) block are in
@@ -424,24 +453,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             for (int cb = cf; cb <= cl; cb += kC) {
               float v[kC][kT];
 #pragma unroll
-              for (int i = 0; i < kC; ++i) {
-                const int c2 = cb + i;
+              for (int k = 0; k < kC; ++k) {
+                const int c2 = cb + k;
                 const int slot = c2 == cf ? first_slot : 2 * c2;
                 const float* src = g.ws + (size_t(slot) * g.M) * kBM + rl;
 #pragma unroll
                 for (int j = 0; j < kT; ++j)
-                  v[i][j] = (c2 <= cl && t0 + j < g.M) ? __ldcg(src + size_t(t0 + j) * kBM) : 0.f;
+                  v[k][j] = (c2 <= cl && t0 + j < g.M) ? __ldcg(src + size_t(t0 + j) * kBM) : 0.f;
               }
 #pragma unroll
-              for (int i = 0; i < kC; ++i)
+              for (int k = 0; k < kC; ++k)
 #pragma unroll
                 for (int j = 0; j < kT; ++j)
-                  if (cb + i <= cl) acc[j] += v[i][j];
+                  if (cb + k <= cl) acc[j] += v[k][j];
             }
 #pragma unroll
             for (int j = 0; j < kT; ++j) apply_epi<EPI>(g, r, t0 + j, acc[j]);
           }
           if (threadIdx.x == 64) g.counters[t] = 0;
+#if SSD_KTL
+          if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][6] = ktl_now();
+#endif
         }
       }
       u = seg_end;
@@ -451,6 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
   if (threadIdx.x == 0) TRACE(4, 1);
+#if SSD_KTL
+  if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][2] = ktl_now();
+#endif
   KTL_EXIT();
 }
 

@@ -22,15 +22,17 @@ ts, ds = shapes("llama8b_1b", max_ctx=1024)
 eng = P.Engine(ts, ds, P.Pair(), max_branches=20, max_lookahead=4)
 lib = P._native.load()
 lib.ssd_debug_ktl.restype = ctypes.c_int
-buf = (ctypes.c_ulonglong * (16384 * 4))()
+NBUF = 16384 * 4 + 16 + 64 * 160 * 8
+buf = (ctypes.c_ulonglong * NBUF)()
 for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
     which, M = (0 if w[0] == "t" else 1), int(w[1:])
     eng.profile_forward(which, M, 128, 2)
-    lib.ssd_debug_ktl(buf, 16384)  # reset
+    lib.ssd_debug_ktl(buf, NBUF)  # reset
     eng.profile_forward(which, M, 128, 1)  # warm forward + gemms + forward + gemms
-    n = lib.ssd_debug_ktl(buf, 16384)
+    n = lib.ssd_debug_ktl(buf, NBUF)
     assert n > 0, f"no timeline records ({n}): not the SSD_KTL build?"
     sub = np.array(buf[n * 4: n * 4 + 16], dtype=np.float64)
+    cta = np.array(buf[n * 4 + 16: n * 4 + 16 + 64 * 160 * 8], dtype=np.float64).reshape(64, 160, 8)
     t = np.array(buf[: n * 4], dtype=np.float64).reshape(n, 4)
     t = t[np.argsort(t[:, 1])]
     # the last full forward: from the last embed to the next embed / end, cut at the GEMM-only pass
@@ -59,9 +61,22 @@ for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
               f"prev-exit->entry {a[3] / a[0]:7.2f} us")
     print("   last attention sub-phases (us from ready): mbar %.2f append+rope %.2f scores %.2f softmax+PV %.2f "
           "cluster.sync %.2f merge %.2f final sync %.2f" % tuple((sub[i] - sub[0]) / 1e3 for i in range(1, 8)))
+    # per-CTA spread of the last GEMM launches of this workload (ready / MMA done / exit), us rel. to min ready
+    print("   per-CTA GEMM spreads (last launches): [ready span, last MMA-done - first ready, exit span, last exit - max MMA done]")
+    for j in range(64):
+        c = cta[j]
+        ok = c[:, 0] > 0
+        if ok.sum() < 8:
+            continue
+        r0 = c[ok, 0].min()
+        last = int(np.argmax(np.where(ok, c[:, 2], 0)))  # the CTA that exits last
+        rel = lambda v: (v - c[last, 1]) / 1e3 if v > 0 else float("nan")  # noqa: E731
+        print("     launch %2d mma-done %6.2f tail %6.2f | last CTA %3d: mma-complete %+.2f tfull %+.2f drained %+.2f arrived %+.2f reduced %+.2f exit %+.2f" % (
+            j, (c[ok, 1].max() - r0) / 1e3, (c[ok, 2].max() - c[ok, 1].max()) / 1e3, last, rel(c[last, 7]),
+            rel(c[last, 3]), rel(c[last, 4]), rel(c[last, 5]), rel(c[last, 6]), rel(c[last, 2])))
     for r in f[:14]:
         print(f"      {KIND.get(int(r[0]), int(r[0])):12s} entry {(r[1] - t0) / 1e3:8.2f} ready {(r[2] - t0) / 1e3:8.2f} "
               f"exit {(r[3] - t0) / 1e3:8.2f}")
 eng.close()
 
-    # (printed per workload above) -- attention sub-phases of the last launch
+
