@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libssd_b200.so")
 SOURCES = ["engine.cu", "plans.cpp"]
 DEPS = SOURCES + ["common.cuh", "kernels.cuh", "gemm_tc.cuh", "rowops.cuh", "probe.cuh", "split.cuh", "tp.cuh",
-                  "attn_cl.cuh", "fwd_mk.cuh"]
+                  "attn_cl.cuh", "fwd_mk.cuh", "gemm_cl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]

@@ -20,6 +20,7 @@
 
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
+#include "gemm_cl.cuh"
 #include "fwd_mk.cuh"
 #include "attn_cl.cuh"
 #include "tp.cuh"
@@ -204,6 +205,7 @@ struct Engine {
   // caught up).
   int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
+  long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
@@ -474,6 +476,62 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
              g);
 }
 
+// Cluster split-K GEMM (gemm_cl.cuh): NC clusters of CS CTAs.
+template <int EPI, int NP, int CS>
+static void gemm_cl_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                           cudaStream_t s, Prefetch pf) {
+  using C = tc::ClCfg<NP>;
+  const int NC = E_num_sms / CS;
+  const int KU = W.K / (tc::kBK * tc::kKPS);
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, 0};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(NC * CS);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CS;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  CK(cudaLaunchKernelEx(&cfg, tc::gemm_cl_kernel<EPI, NP, CS>, act_map(m, X, W.K, NP), g));
+}
+
+// Cluster size minimising the units on a CTA's critical path (whole tiles
+// per cluster x k-slice), ties to the smaller cluster.
+static int pick_cluster(const WMat& W) {
+  const int T = (W.N + tc::kBM - 1) / tc::kBM, KU = W.K / (tc::kBK * tc::kKPS);
+  int best = 0, best_units = 1 << 30;
+  for (int cs : {2, 4, 8}) {
+    const int nc = E_num_sms / cs;
+    const int units = ((T + nc - 1) / nc) * ((KU + cs - 1) / cs);
+    if (units < best_units) { best_units = units; best = cs; }
+  }
+  return best;
+}
+
+template <int EPI, int NP>
+static void gemm_cl_dispatch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                             cudaStream_t s, Prefetch pf) {
+  switch (pick_cluster(W)) {
+    case 2: gemm_cl_launch<EPI, NP, 2>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
+    case 4: gemm_cl_launch<EPI, NP, 4>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
+    default: gemm_cl_launch<EPI, NP, 8>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
+  }
+}
+
+template <int EPI, int NP, int CS>
+static void configure_cl() {
+  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(tc::ClCfg<NP>::kSmem)));
+  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                          int(cudaSharedmemCarveoutMaxShared)));
+}
+
 template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 static void configure_gemm() {
   CK(cudaFuncSetAttribute(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -528,6 +586,8 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 192>(); configure_gemm<EPI_SWIGLU, 192>();
   configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
   configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
+  configure_cl<EPI_STORE, 32, 2>(); configure_cl<EPI_STORE, 32, 4>(); configure_cl<EPI_STORE, 32, 8>();
+  configure_cl<EPI_SWIGLU, 32, 2>(); configure_cl<EPI_SWIGLU, 32, 4>(); configure_cl<EPI_SWIGLU, 32, 8>();
   configure_gemm<EPI_STORE, 32, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 32, tc::kSmallBudgetKB>();
   for (auto f : {attention_cl_kernel<1>, attention_cl_kernel<2>, attention_cl_kernel<4>, attention_cl_kernel<8>})
     carveout_max(f);
@@ -575,6 +635,13 @@ template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                    cudaStream_t s, Prefetch pf) {
   ++E.launches;
+  // small weight matrices at branch widths (17..32 tokens): cluster split-K.
+  // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
+  // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
+  if (W.bytes <= E.cl_gemm_bytes && M > 16 && M <= 32 && m.gemm_ctas == 0) {
+    gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    return;
+  }
   // small weight matrices: the co-resident (small-budget) configuration
   if (W.bytes <= E.small_gemm_bytes && M <= 32) {
     if (M <= 16) gemm_tc_launch<EPI, 16, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
@@ -1120,6 +1187,7 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
+  if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
   {
