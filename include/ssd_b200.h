@@ -160,6 +160,11 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
 ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
                                 const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
                                 int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out);
+/* Same, colocated, with `max_batch` batch lanes (SimConfig::batch_size,
+ * sim.hpp:40): each lane has its own KV region, history and streams. */
+ssd_status ssd_engine_create_batch(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                   const ssd_pair_params* pair, int32_t device, int32_t max_batch,
+                                   int32_t max_branches, int32_t max_lookahead, ssd_engine** out);
 ssd_status ssd_engine_destroy(ssd_engine* e);
 /* Bytes of weights streamed per forward step of model `which` (0 target,
  * 1 draft): the algorithmic bytes of one decode step. */
@@ -187,6 +192,19 @@ ssd_status ssd_run_ssd(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
                        int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits,
                        ssd_run_stats* stats);
 
+/* run_protocol_harness with SimConfig::batch_size = `batch` (sim.cpp:502-601,
+ * sim.hpp:121-126): every sequence shares the prompt, sequence j drafts from
+ * Stream(derive_seed(seed, j)) and verifies from
+ * Stream(derive_seed(derive_seed(seed, 0x5EED), j)); the batch's forwards run
+ * batched on the GPU (verify M = batch (K+1), branch steps M = batch B), and a
+ * miss in any sequence stalls the round's virtual clock for the backup
+ * (whole-batch stall). Streams go to out_tokens[j * out_capacity ..] with
+ * lengths out_lens[j]; outcomes / hits are sequence 0's; stats sum over the
+ * batch (RunStats semantics). batch == 1 is ssd_run_ssd. */
+ssd_status ssd_run_ssd_batch(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
+                             const ssd_sim_config* cfg, int32_t batch, int32_t* out_tokens,
+                             int64_t out_capacity, int64_t* out_lens, int32_t* out_outcomes,
+                             int32_t* out_hits, ssd_run_stats* stats);
 /* ------------------------------------------ split processes (sim.cpp:258-601)
  * The reference's Channel between VerifierProcess and DraftProcess becomes
  * device mailboxes in HBM, mapped across processes/GPUs by CUDA IPC (NVLink

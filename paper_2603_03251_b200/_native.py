@@ -68,6 +68,8 @@ SIGNATURES = {
                                          C.c_int32, C.c_int32, P(EngineP)]),
     "ssd_engine_create_tp": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32, C.c_int32,
                                        C.c_int32, C.c_int32, C.c_int32, P(EngineP)]),
+    "ssd_engine_create_batch": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32,
+                                          C.c_int32, C.c_int32, P(EngineP)]),
     "ssd_engine_destroy": (C.c_int, [EngineP]),
     "ssd_tp_export": (C.c_int, [EngineP, P(C.c_uint8)]),
     "ssd_tp_connect": (C.c_int, [EngineP, P(C.c_uint8)]),
@@ -83,6 +85,8 @@ SIGNATURES = {
     "ssd_run_sd": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), i32p, C.c_int64, i64p, P(RunStatsC)]),
     "ssd_run_ssd": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), i32p, C.c_int64, i64p, i32p, i32p,
                               P(RunStatsC)]),
+    "ssd_run_ssd_batch": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, i32p, C.c_int64, i64p, i32p,
+                                    i32p, P(RunStatsC)]),
     "ssd_logits": (C.c_int, [EngineP, C.c_int32, i32p, C.c_int32, f32p]),
     "ssd_draft": (C.c_int, [EngineP, i32p, C.c_int32, C.c_int32, P(Scheme), C.c_uint64, i32p, f32p]),
     "ssd_build_cache": (C.c_int, [EngineP, i32p, C.c_int32, i32p, C.c_int32, P(Plan), P(Scheme), C.c_int32,

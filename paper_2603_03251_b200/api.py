@@ -140,6 +140,7 @@ class SimConfig:
     rounds: int = 1000
     seed: int = 0
     accept_scale: float = 1.0
+    batch_size: int = 1  # sim.hpp:40; run_ssd only (whole-batch stall semantics)
 
     def c(self) -> N.SimConfigC:
         ts = self.target_scheme or SamplingScheme.standard(self.scheme.temperature)
@@ -169,6 +170,7 @@ class RunStats:
     device_ms: float
     kernel_launches: int
     streams: list = field(default_factory=list)
+    batch: int = 1
     outcomes: Optional[np.ndarray] = None  # [rounds, 2] (accepted, bonus)
     hits: Optional[np.ndarray] = None      # [rounds] 1/0, -1 on the last round
 
@@ -272,7 +274,7 @@ class Engine:
 
     def __init__(self, target: N.ModelShape, draft: N.ModelShape, pair: Pair = Pair(), device: int = 0,
                  max_branches: int = 64, max_lookahead: int = 8, role: int = N.ROLE_COLOCATED, tp_rank: int = 0,
-                 tp_size: int = 1):
+                 tp_size: int = 1, max_batch: int = 1):
         """role: ROLE_COLOCATED (both models), ROLE_VERIFIER (target only) or
         ROLE_SPECULATOR (draft only) — the processes of a split run. A
         verifier may be tensor-parallel: rank tp_rank of tp_size (connect the
@@ -282,9 +284,14 @@ class Engine:
         self.vocab = target.vocab
         self.role = role
         self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.max_batch = max_batch
         h = C.c_void_p()
-        _check(self.lib.ssd_engine_create_tp(C.byref(target), C.byref(draft), C.byref(pair.c()), device, role, tp_rank,
-                                             tp_size, max_branches, max_lookahead, C.byref(h)))
+        if max_batch > 1:  # batch lanes (colocated engine)
+            _check(self.lib.ssd_engine_create_batch(C.byref(target), C.byref(draft), C.byref(pair.c()), device,
+                                                    max_batch, max_branches, max_lookahead, C.byref(h)))
+        else:
+            _check(self.lib.ssd_engine_create_tp(C.byref(target), C.byref(draft), C.byref(pair.c()), device, role,
+                                                 tp_rank, tp_size, max_branches, max_lookahead, C.byref(h)))
         self.h = h
 
     def tp_handle(self) -> bytes:
@@ -334,17 +341,24 @@ class Engine:
         return RunStats._from_c(st, out[: n.value].tolist())
 
     def run_ssd(self, prompt: Sequence[int], cfg: SimConfig) -> RunStats:
-        """sim::run_protocol_harness semantics (sim.cpp:502-601)."""
+        """sim::run_protocol_harness semantics (sim.cpp:502-601), with
+        cfg.batch_size sequences (whole-batch stall: any miss delays the
+        round for the backup). streams[j] is sequence j's output; outcomes /
+        hits are sequence 0's."""
         p = _i32(prompt)
+        b = int(cfg.batch_size)
         cap = cfg.rounds * (cfg.lookahead + 1)
-        out = np.zeros(cap, dtype=np.int32)
+        out = np.zeros(b * cap, dtype=np.int32)
         oc = np.zeros(2 * cfg.rounds, dtype=np.int32)
         hits = np.zeros(cfg.rounds, dtype=np.int32)
-        n = C.c_int64()
+        lens = np.zeros(b, dtype=np.int64)
         st = N.RunStatsC()
-        _check(self.lib.ssd_run_ssd(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), _ptr(out, C.c_int32), cap,
-                                    C.byref(n), _ptr(oc, C.c_int32), _ptr(hits, C.c_int32), C.byref(st)))
-        r = RunStats._from_c(st, out[: n.value].tolist())
+        _check(self.lib.ssd_run_ssd_batch(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), b,
+                                          _ptr(out, C.c_int32), cap, _ptr(lens, C.c_int64), _ptr(oc, C.c_int32),
+                                          _ptr(hits, C.c_int32), C.byref(st)))
+        r = RunStats._from_c(st, out[: int(lens[0])].tolist())
+        r.streams = [out[j * cap: j * cap + int(lens[j])].tolist() for j in range(b)]
+        r.batch = b
         r.outcomes = oc.reshape(-1, 2)
         r.hits = hits
         return r

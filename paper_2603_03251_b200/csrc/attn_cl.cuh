@@ -55,8 +55,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
   const bf16* kbase = kc + size_t(kvh) * S * hd;
   const bf16* vbase = vc + size_t(kvh) * S * hd;
   // 0) main-cache rows [j0, j0 + npre) of this head: written by earlier
-  //    forwards (or patched below), so they are fetched before the PDL wait
-  const int npre = max(0, min(kAttnChunk, ctx_bound - j0));
+  //    forwards (or patched below), so they are fetched before the PDL wait.
+  //    (P was written before this forward's first kernel started.)
+  const int mb = P->mbase[m];
+  const int npre = max(0, min(min(kAttnChunk, ctx_bound - j0), S - mb - j0));
   if (tid == 0) {
     tc::mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -69,8 +71,8 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
     if (bytes) {
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      tc::bulk_load(Ks, kbase + size_t(j0) * hd, bytes, bar, pol);
-      tc::bulk_load(Vs, vbase + size_t(j0) * hd, bytes, bar, pol);
+      tc::bulk_load(Ks, kbase + size_t(mb + j0) * hd, bytes, bar, pol);
+      tc::bulk_load(Vs, vbase + size_t(mb + j0) * hd, bytes, bar, pol);
     }
   }
   asm volatile("griddepcontrol.launch_dependents;");
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_cl_kernel(
     for (int e = tid; e < M * half; e += kAttnThreads) {
       const int t = e / half, i = e % half;
       const int slot = P->slot[t];
-      const int j = slot < main_len ? slot : (slot >= bbase && slot < bbase + blen ? main_len + slot - bbase : -1);
+      const int j = visible_key(slot, mb, main_len, bbase, blen);
       if (j < j0 || j >= j1) continue;
       const int pos = P->pos[t];
       const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];

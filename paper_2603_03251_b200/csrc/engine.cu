@@ -133,7 +133,8 @@ struct Model {
   float* final_gain = nullptr;
   float* ffn_gain0 = nullptr;
   std::vector<DevLayer> layers;
-  int S = 0;             // KV slots per kv-head (main + branch region)
+  int S = 0;             // KV slots per kv-head: batch lanes x (main + branch region)
+  int lane_S = 0;        // KV slots of one batch lane (lane l starts at l * lane_S)
   bf16* kc = nullptr;    // [L][KVH][S][hd]
   bf16* vc = nullptr;
   float* rope_cos = nullptr;
@@ -174,6 +175,9 @@ struct Engine {
   int dev = 0;
   Model T, D;
   int maxB = 0, maxK = 0;
+  int nbmax = 1;            // batch lanes (run_protocol_harness batch_size)
+  int hist_stride = 0;      // history capacity of one lane
+  int* d_lanes = nullptr;   // device list of the lanes a batched draft serves
   int V = 0;
   cudaStream_t sv = nullptr, ss = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_verified = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
@@ -182,8 +186,8 @@ struct Engine {
   FwdParams *P_t = nullptr, *P_x = nullptr, *P_b = nullptr, *P_s = nullptr, *P_pre = nullptr;
   float* tlogits = nullptr;   // [K+1][V]
   float* xrows = nullptr;     // extend rows [K+1][V]
-  float* dmain = nullptr;     // drafted rows [K][V]
-  float* brows[2] = {nullptr, nullptr};  // branch rows [K][B][V], double-buffered by round parity
+  float* dmain = nullptr;     // drafted rows [K][lanes][V]
+  float* brows[2] = {nullptr, nullptr};  // branch rows [K][lanes * B][V], double-buffered by round parity
   int *keys = nullptr, *bk = nullptr, *btok = nullptr, *bt = nullptr;
   double* bu = nullptr;
   double* ubuf = nullptr;
@@ -278,7 +282,7 @@ static ssd_model_shape tp_local(const ssd_model_shape& s, int tp) {
 // vocabulary-parallel head, replicated embedding), generated as the exact
 // blocks of the unsharded synthetic tensors.
 static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_shape& dr, const ssd_pair_params& pp,
-                        int role, int branch_slots, int maxM, int tp_rank = 0, int tp_size = 1) {
+                        int role, int branch_slots, int maxM, int tp_rank = 0, int tp_size = 1, int lanes = 1) {
   const ssd_model_shape s = tp_local(sfull, tp_size);
   m.s = s;
   m.role = role;
@@ -372,7 +376,8 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
   wb += int64_t(s.vocab) * d;  // LM head
   m.weight_bytes = wb * 2;
   // KV cache
-  m.S = s.max_ctx + branch_slots;
+  m.lane_S = s.max_ctx + branch_slots;
+  m.S = lanes * m.lane_S;
   m.kc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   m.vc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   std::vector<float> cs, sn;
@@ -878,11 +883,11 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
 
 // Prefill hist[0, n) into model m (chunks of maxM). Logits of the last
 // token to `last_logits` when non-null.
-static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t s) {
+static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t s, int lane = 0) {
   const int chunk = std::min(m.maxM, kMaxM);
   for (int lo = 0; lo < n; lo += chunk) {
     const int M = std::min(chunk, n - lo);
-    prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, lo, M);
+    prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist + size_t(lane) * E.hist_stride, E.P_pre, lo, M, lane * m.lane_S);
     KCHECK();
     const bool last = lo + M >= n;
     forward(E, m, E.P_pre, M, (last && last_logits) ? m.logits : nullptr, s);
@@ -912,7 +917,7 @@ static void check_scheme(const ssd_scheme& s, int V) {
 
 // ------------------------------------------------------------------ state
 static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed, uint64_t vseed, const ssd_sim_config* c,
-                        cudaStream_t s) {
+                        cudaStream_t s, int lane = 0) {
   LoopState h;
   std::memset(&h, 0, sizeof(h));
   h.n = n;
@@ -922,15 +927,15 @@ static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed,
   h.primary_time = c ? c->primary_time : 0.0;
   h.backup_time = c ? (c->backup_kind == 0 ? c->primary_time : c->backup_time) : 0.0;
   h.seq_base = E.seq_base;
-  CK(cudaMemcpyAsync(E.st, &h, offsetof(LoopState, vrng), cudaMemcpyHostToDevice, s));
-  mt_init_kernel<<<1, 32, 0, s>>>(&E.st->vrng, vseed);
-  mt_init_kernel<<<1, 32, 0, s>>>(&E.st->drng, dseed);
+  CK(cudaMemcpyAsync(E.st + lane, &h, offsetof(LoopState, vrng), cudaMemcpyHostToDevice, s));
+  mt_init_kernel<<<1, 32, 0, s>>>(&E.st[lane].vrng, vseed);
+  mt_init_kernel<<<1, 32, 0, s>>>(&E.st[lane].drng, dseed);
   KCHECK();
 }
 
-static LoopState read_state(Engine& E) {
+static LoopState read_state(Engine& E, int lane = 0) {
   LoopState h;
-  CK(cudaMemcpy(&h, E.st, offsetof(LoopState, vrng), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&h, E.st + lane, offsetof(LoopState, vrng), cudaMemcpyDeviceToHost));
   return h;
 }
 
@@ -954,12 +959,13 @@ static void row_pick(Engine& E, const float* base, size_t stride, int rows, int 
 }
 
 // Cache keys from K+1 contiguous logit rows (cache.cpp:249-270).
+// Batch lanes: nl lanes of nrows rows each; lane l's branches at l * bper.
 static void row_keys(Engine& E, const float* rows, int nrows, int V, int max_f, const LoopState* st, const int* excl,
-                     int n_excl, cudaStream_t s) {
+                     int n_excl, cudaStream_t s, int nl = 1, int bper = 0) {
   const int T = std::min(max_f + 1, kMaxTopF + 1);
-  row_phase1_kernel<<<dim3(E.nch, nrows), kRowThreads, 0, s>>>(rows, size_t(V), V, T, 0.0, E.cand, E.rstat2);
-  row_keys_kernel<<<nrows, kRowThreads, 0, s>>>(E.nch, T, E.cand, E.plans, E.offs, st, excl, n_excl, max_f, E.keys, E.bk,
-                                                E.btok);
+  row_phase1_kernel<<<dim3(E.nch, nrows * nl), kRowThreads, 0, s>>>(rows, size_t(V), V, T, 0.0, E.cand, E.rstat2);
+  row_keys_kernel<<<nrows * nl, kRowThreads, 0, s>>>(E.nch, T, E.cand, E.plans, E.offs, st, excl, n_excl, max_f, E.keys,
+                                                     E.bk, E.btok, nrows, bper);
   KCHECK();
   E.launches += 2;
 }
@@ -969,7 +975,7 @@ static void row_keys(Engine& E, const float* rows, int nrows, int V, int max_f, 
 static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int src, cudaStream_t s) {
   const DScheme ds = dscheme(sc);
   for (int i = 0; i < K; ++i) {
-    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i);
+    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, nullptr, 1, 0, 0);
     forward(E, E.D, E.P_s, 1, E.dmain + size_t(i) * E.V, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
     row_pick(E, E.dmain + size_t(i) * E.V, size_t(E.V), 1, E.V, ds, E.ubuf, 1, &E.st->spec[i], 1, s);
@@ -981,16 +987,38 @@ static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int 
   ++E.launches;
 }
 
+// specdec::draft for the nl batch lanes listed in E.d_lanes, batched: one
+// M = nl draft forward per step, each lane drawing from its own stream
+// (the initial drafts and the JIT backups of run_protocol_harness at batch
+// size > 1, sim.cpp:524-526, 565-570). Rows: dmain[(i * nbmax + m) * V].
+static void draft_lanes(Engine& E, int K, const ssd_scheme& sc, int origin, int src, int nl, cudaStream_t s) {
+  const DScheme ds = dscheme(sc);
+  for (int i = 0; i < K; ++i) {
+    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, E.d_lanes, nl, E.hist_stride, E.D.lane_S);
+    float* rows = E.dmain + size_t(i) * E.nbmax * E.V;
+    forward(E, E.D, E.P_s, nl, rows, s);
+    draw_lane_uniforms_kernel<<<1, 32, 0, s>>>(E.st, E.d_lanes, nl, E.ubuf);
+    row_pick(E, rows, size_t(E.V), nl, E.V, ds, E.ubuf, 1, E.tok_scratch, 1, s);
+    scatter_spec_kernel<<<1, 32, 0, s>>>(E.st, E.d_lanes, nl, i, E.tok_scratch);
+    KCHECK();
+    E.launches += 3;
+  }
+  set_lane_spec_rows_kernel<<<1, 32, 0, s>>>(E.st, E.d_lanes, nl, E.dmain, E.nbmax, E.V, origin, src);
+  KCHECK();
+  ++E.launches;
+}
+
 // Verification of st->spec against the target (verify forward M = K+1,
 // then the decision kernels).
 static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_scheme& ds, double scale, int use_draft_stream,
-                         cudaStream_t s) {
-  prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1);
+                         cudaStream_t s, int nl = 1) {
+  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1, E.hist_stride, E.T.lane_S);
   KCHECK();
-  forward(E, E.T, E.P_t, K + 1, E.tlogits, s);
-  verify_stats_kernel<<<2 * K + 1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.V, dscheme(ts), dscheme(ds), E.rstat);
-  verify_decide_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, E.V, dscheme(ts), dscheme(ds), scale, E.rstat,
-                                                    use_draft_stream);
+  forward(E, E.T, E.P_t, nl * (K + 1), E.tlogits, s);
+  verify_stats_kernel<<<dim3(2 * K + 1, nl), kSampleThreads, 0, s>>>(E.tlogits, E.st, E.V, dscheme(ts), dscheme(ds),
+                                                                       E.rstat);
+  verify_decide_kernel<<<nl, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, E.V, dscheme(ts), dscheme(ds), scale, E.rstat,
+                                                     use_draft_stream, E.hist_stride);
   KCHECK();
   E.launches += 3;
 }
@@ -1000,22 +1028,26 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 // per-branch streams, K branch decode steps at M = B.
 // Branch sharding: every speculator computes the full key
 // table and the per-branch streams, and decodes branches [lo, lo + Bl).
+// Batch lanes (nl > 1, no sharding: lo = 0, Bl = B): every lane's extend
+// rides one M = nl (K+1) forward, its B branches are rows [l B, (l+1) B) of
+// one M = nl B branch step.
 static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
-                         cudaStream_t s) {
-  prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1);
+                         cudaStream_t s, int nl = 1) {
+  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S);
   KCHECK();
-  forward(E, E.D, E.P_x, K + 1, E.xrows, s);
-  row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s);
+  forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
+  row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s, nl, B);
   const bool sampled = sc.temperature > 0.0;
-  branch_streams_kernel<<<1, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
+  branch_streams_kernel<<<nl, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
   E.launches += 2;
+  if (nl > 1) Bl = nl * B;
   if (Bl <= 0) return;
   const DScheme ds = dscheme(sc);
   float* rows = E.brows[parity];
   for (int j = 0; j < K; ++j) {
     prep_branch_kernel<<<(Bl + 127) / 128, 128, 0, s>>>(E.st, E.bk + lo, E.btok + lo, E.bt, E.P_b, Bl, j,
-                                                         E.D.s.max_ctx);
+                                                         E.D.s.max_ctx, nl > 1 ? B : 0, E.D.lane_S);
     float* out = rows + size_t(j) * Bl * E.V;
     forward(E, E.D, E.P_b, Bl, out, s);
     row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * K + j : nullptr, K, E.bt + j, K, s);
@@ -1050,14 +1082,30 @@ static void upload_plans(Engine& E, const ssd_plan& p, const ssd_plan& b, int K,
   CK(cudaMemcpy(E.offs, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
 }
 
-static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_needed) {
+static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_needed, int lanes = 1) {
   if (n < 1) throw Fail(SSD_ERROR, "prompt must hold at least one token");
   const int cap = std::min(E.T.s.max_ctx, E.D.s.max_ctx);
   if (max_ctx_needed > cap) throw Fail(SSD_TOO_LARGE, "context exceeds max_ctx");
   E.T.ctx_bound = E.D.ctx_bound = max_ctx_needed + 2 * E.maxK + 2;
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= E.V) throw Fail(SSD_ERROR, "context_index: token out of range");
-  CK(cudaMemcpy(E.hist, prompt, size_t(n) * 4, cudaMemcpyHostToDevice));
+  for (int l = 0; l < lanes; ++l)
+    CK(cudaMemcpy(E.hist + size_t(l) * E.hist_stride, prompt, size_t(n) * 4, cudaMemcpyHostToDevice));
+}
+
+// RunStats counters summed over batch lanes (sim.cpp:548-586 counts every
+// sequence); the virtual clock is shared.
+static LoopState sum_lanes(const std::vector<LoopState>& v) {
+  LoopState h = v[0];
+  for (size_t l = 1; l < v.size(); ++l) {
+    const LoopState& o = v[l];
+    h.tokens += o.tokens; h.p_lookups += o.p_lookups; h.p_hits += o.p_hits; h.b_lookups += o.b_lookups;
+    h.b_hits += o.b_hits; h.hit_rounds += o.hit_rounds; h.miss_rounds += o.miss_rounds;
+    h.initial_rounds += o.initial_rounds; h.hit_round_tokens += o.hit_round_tokens;
+    h.miss_round_tokens += o.miss_round_tokens; h.accepted_sum += o.accepted_sum;
+    if (o.error && !h.error) h.error = o.error;
+  }
+  return h;
 }
 
 static void fill_stats(const LoopState& h, int64_t rounds, float ms, long long launches, ssd_run_stats* out) {
@@ -1079,10 +1127,12 @@ static void fill_stats(const LoopState& h, int64_t rounds, float ms, long long l
   out->kernel_launches = launches;
 }
 
-static void copy_out(Engine& E, int n0, int n, int32_t* out, int64_t cap, int64_t* out_len) {
+static void copy_out(Engine& E, int n0, int n, int32_t* out, int64_t cap, int64_t* out_len, int lane = 0) {
   const int64_t len = n - n0;
   if (out_len) *out_len = len;
-  if (out && len > 0) CK(cudaMemcpy(out, E.hist + n0, size_t(std::min<int64_t>(len, cap)) * 4, cudaMemcpyDeviceToHost));
+  if (out && len > 0)
+    CK(cudaMemcpy(out, E.hist + size_t(lane) * E.hist_stride + n0, size_t(std::min<int64_t>(len, cap)) * 4,
+                  cudaMemcpyDeviceToHost));
 }
 
 static void validate_cfg(Engine& E, const ssd_sim_config* c) {
@@ -1150,10 +1200,14 @@ ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model
   return ssd_engine_create_tp(target, draft, pair, device, role, 0, 1, max_branches, max_lookahead, out);
 }
 
-ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
+static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_shape* draft,
                                 const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
-                                int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out) {
+                                int32_t tp_size, int32_t max_batch, int32_t max_branches, int32_t max_lookahead,
+                                ssd_engine** out) {
   API_BEGIN
+  if (max_batch < 1) throw Fail(SSD_ERROR, "sim: batch_size must be >= 1");
+  if (max_batch > 1 && (role != SSD_ROLE_COLOCATED || tp_size > 1))
+    throw Fail(SSD_CONFIG, "engine: batch lanes are for the colocated engine");
   if (!target || !draft || !pair || !out) throw Fail(SSD_CONFIG, "engine: null argument");
   if (role < SSD_ROLE_COLOCATED || role > SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "engine: unknown role");
   if (tp_size < 1 || tp_size > kTpMax || tp_rank < 0 || tp_rank >= tp_size) throw Fail(SSD_CONFIG, "engine: bad TP rank");
@@ -1178,6 +1232,7 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   auto* h = new ssd_engine();
   Engine& E = h->e;
   E.dev = device;
+  E.nbmax = max_batch;
   E.maxB = max_branches;
   E.maxK = max_lookahead;
   E.V = target->vocab;
@@ -1195,13 +1250,15 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     E_num_sms = sms;
   }
-  const int maxM = std::max(max_branches, max_lookahead + 1);
+  const int nb = max_batch;
+  const int maxM = nb * std::max(max_branches, max_lookahead + 1);
+  if (maxM > kMaxM) throw Fail(SSD_TOO_LARGE, "engine: batch x branches above the forward capacity");
   // a split process materialises only its own model
   if (role != SSD_ROLE_SPECULATOR)
-    build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64), tp_rank, tp_size);
+    build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64), tp_rank, tp_size, nb);
   else E.T.s = *target;
   if (role != SSD_ROLE_VERIFIER)
-    build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64));
+    build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64), 0, 1, nb);
   else E.D.s = *draft;
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
@@ -1226,31 +1283,33 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   CK(cudaEventCreate(&E.ev_t1));
   auto own = [&](void* p) { E.owned.push_back(p); return p; };
   const int K = max_lookahead, B = max_branches, V = E.V;
-  E.st = static_cast<LoopState*>(own(dalloc<LoopState>(1)));
-  E.hist = static_cast<int*>(own(dalloc<int>(size_t(std::max(target->max_ctx, draft->max_ctx)) + K + 2)));
+  E.st = static_cast<LoopState*>(own(dalloc<LoopState>(size_t(nb))));
+  E.hist_stride = std::max(target->max_ctx, draft->max_ctx) + K + 2;
+  E.hist = static_cast<int*>(own(dalloc<int>(size_t(nb) * E.hist_stride)));
+  E.d_lanes = static_cast<int*>(own(dalloc<int>(size_t(nb))));
   E.P_t = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_x = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_b = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_s = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_pre = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
-  E.tlogits = static_cast<float*>(own(dalloc<float>(size_t(K + 1) * V)));
-  E.xrows = static_cast<float*>(own(dalloc<float>(size_t(K + 1) * V)));
-  E.dmain = static_cast<float*>(own(dalloc<float>(size_t(K) * V)));
-  E.brows[0] = static_cast<float*>(own(dalloc<float>(size_t(K) * B * V)));
-  E.brows[1] = static_cast<float*>(own(dalloc<float>(size_t(K) * B * V)));
-  E.keys = static_cast<int*>(own(dalloc<int>(size_t(K + 1) * kMaxTopF)));
-  E.bk = static_cast<int*>(own(dalloc<int>(size_t(B))));
-  E.btok = static_cast<int*>(own(dalloc<int>(size_t(B))));
-  E.bt = static_cast<int*>(own(dalloc<int>(size_t(B) * K)));
-  E.bu = static_cast<double*>(own(dalloc<double>(size_t(B) * K)));
+  E.tlogits = static_cast<float*>(own(dalloc<float>(size_t(nb) * (K + 1) * V)));
+  E.xrows = static_cast<float*>(own(dalloc<float>(size_t(nb) * (K + 1) * V)));
+  E.dmain = static_cast<float*>(own(dalloc<float>(size_t(K) * nb * V)));
+  E.brows[0] = static_cast<float*>(own(dalloc<float>(size_t(K) * nb * B * V)));
+  E.brows[1] = static_cast<float*>(own(dalloc<float>(size_t(K) * nb * B * V)));
+  E.keys = static_cast<int*>(own(dalloc<int>(size_t(nb) * (K + 1) * kMaxTopF)));
+  E.bk = static_cast<int*>(own(dalloc<int>(size_t(nb) * B)));
+  E.btok = static_cast<int*>(own(dalloc<int>(size_t(nb) * B)));
+  E.bt = static_cast<int*>(own(dalloc<int>(size_t(nb) * B * K)));
+  E.bu = static_cast<double*>(own(dalloc<double>(size_t(nb) * B * K)));
   E.ubuf = static_cast<double*>(own(dalloc<double>(64)));
   E.plans = static_cast<int*>(own(dalloc<int>(size_t(2 * (K + 1)))));
   E.offs = static_cast<int*>(own(dalloc<int>(size_t(2 * (K + 1)))));
-  E.rstat = static_cast<RowStat*>(own(dalloc<RowStat>(size_t(2 * K + 1))));
+  E.rstat = static_cast<RowStat*>(own(dalloc<RowStat>(size_t(nb) * (2 * K + 1))));
   E.tok_scratch = static_cast<int*>(own(dalloc<int>(64)));
   E.nch = std::max(1, std::min(kMaxChunks, (V + 1023) / 1024));
   {
-    const int rows = std::max(B, K + 1);
+    const int rows = nb * std::max(B, K + 1);
     E.cand = static_cast<VI*>(own(dalloc<VI>(size_t(rows) * E.nch * (kMaxTopF + 1))));
     E.rstat2 = static_cast<RowChunk*>(own(dalloc<RowChunk>(size_t(rows) * E.nch)));
   }
@@ -1279,6 +1338,19 @@ ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_s
   CK(cudaDeviceSynchronize());
   *out = h;
   API_END
+}
+
+ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
+                                int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out) {
+  return engine_create(target, draft, pair, device, role, tp_rank, tp_size, 1, max_branches, max_lookahead, out);
+}
+
+ssd_status ssd_engine_create_batch(const ssd_model_shape* target, const ssd_model_shape* draft,
+                                   const ssd_pair_params* pair, int32_t device, int32_t max_batch, int32_t max_branches,
+                                   int32_t max_lookahead, ssd_engine** out) {
+  return engine_create(target, draft, pair, device, SSD_ROLE_COLOCATED, 0, 1, max_batch, max_branches, max_lookahead,
+                       out);
 }
 
 ssd_status ssd_engine_destroy(ssd_engine* h) {
@@ -1329,7 +1401,7 @@ ssd_status ssd_run_ar(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   E.launches = 0;
   GraphSet gs;
   gs.g.push_back(capture_graph(s, [&] {
-    prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1);
+    prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1, E.hist_stride, E.T.lane_S);
     forward(E, E.T, E.P_t, 1, E.tlogits, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
     row_pick(E, E.tlogits, size_t(E.V), 1, E.V, d, E.ubuf, 1, E.tok_scratch, 1, s);
@@ -1393,38 +1465,55 @@ ssd_status ssd_run_sd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   API_END
 }
 
-ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t* out,
-                       int64_t cap, int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats) {
-  API_BEGIN
-  Engine& E = h->e;
+}  // extern "C"
+
+namespace ssd {
+
+// run_protocol_harness (sim.cpp:502-601) over `nb` batch lanes: lane l is
+// sequence j = l with draft stream derive_seed(seed, l) and verifier stream
+// derive_seed(derive_seed(seed, 0x5EED), l) (sim.cpp:379-380, 516-518); all
+// lanes share the prompt, their forwards are batched (verify M = nb (K+1),
+// branch steps M = nb B), and a miss in any lane stalls the round's clock
+// for the backup (sim.cpp:570-577).
+static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int nb, int32_t* out,
+                         int64_t cap, int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats) {
   CK(cudaSetDevice(E.dev));
   validate_cfg(E, c);
   need(E.T, "run_ssd");
   need(E.D, "run_ssd");
+  if (nb < 1) throw Fail(SSD_ERROR, "sim: batch_size must be >= 1");
+  if (nb > E.nbmax) throw Fail(SSD_TOO_LARGE, "sim: batch_size exceeds the engine's batch capacity");
+  if (nb > 1 && (E.use_mk || E.T.tp_size > 1)) throw Fail(SSD_CONFIG, "sim: batch > 1 needs the per-op colocated engine");
   const int K = c->lookahead;
   int B = 0, max_f = 0;
   upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);
-  set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2));
+  if (nb * B > E.D.maxM || nb * (K + 1) > E.T.maxM) throw Fail(SSD_TOO_LARGE, "sim: batch x branches exceeds capacity");
+  set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2), nb);
   const int64_t R = c->rounds;
-  int* d_out = static_cast<int*>(nullptr);
-  int* d_hit = static_cast<int*>(nullptr);
-  d_out = dalloc<int>(size_t(2 * R));
-  d_hit = dalloc<int>(size_t(R));
+  struct DevBuf {
+    int* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+  } d_out, d_hit;
+  d_out.p = dalloc<int>(size_t(2 * R));
+  d_hit.p = dalloc<int>(size_t(R));
   cudaStream_t sv = E.sv, ss = E.ss;
-  // harness streams: draft j=0 derive_seed(seed, 0); verifier
-  // derive_seed(derive_seed(seed, 0x5EED), 0) (sim.cpp:379-380, 516-518)
-  reset_state(E, K, n0, R, derive_seed(c->seed, 0), derive_seed(derive_seed(c->seed, 0x5EED), 0), c, sv);
-  if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, sv);
-  if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, sv);
-  // initial synchronous draft; clock starts at T_p (sim.cpp:524-526)
-  draft_steps(E, K, c->scheme, 0, 0, sv);
-  {
-    LoopState tmp;
-    tmp.clock = c->primary_time;
-    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, clock), &tmp.clock, sizeof(double),
-                       cudaMemcpyHostToDevice, sv));
+  for (int l = 0; l < nb; ++l) {
+    reset_state(E, K, n0, R, derive_seed(c->seed, uint64_t(l)), derive_seed(derive_seed(c->seed, 0x5EED), uint64_t(l)),
+                c, sv, l);
+    if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, sv, l);
+    if (n0 > 1) prefill(E, E.T, n0 - 1, nullptr, sv, l);
   }
-  CK(cudaStreamSynchronize(sv));
+  // initial synchronous drafts; clock starts at T_p (sim.cpp:524-526)
+  std::vector<int> lanes(static_cast<size_t>(nb));
+  for (int l = 0; l < nb; ++l) lanes[size_t(l)] = l;
+  CK(cudaMemcpyAsync(E.d_lanes, lanes.data(), size_t(nb) * 4, cudaMemcpyHostToDevice, sv));
+  draft_lanes(E, K, c->scheme, 0, 0, nb, sv);
+  for (int l = 0; l < nb; ++l) {
+    const double clock0 = c->primary_time;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st + l) + offsetof(LoopState, clock), &clock0, sizeof(double),
+                       cudaMemcpyHostToDevice, sv));
+    CK(cudaStreamSynchronize(sv));
+  }
   const bool jit = c->backup_kind == 0;
   // One SSD round = one graph: the verifier branch (verify forward +
   // decision) and the speculator branch (extend, keys, K branch steps) fork
@@ -1443,12 +1532,12 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
     gs.g.push_back(capture_graph(sv, [&] {
       CK(cudaEventRecord(E.ev_fork, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
-      prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss);
-      verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv);
+      prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb);
+      verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
       CK(cudaEventRecord(E.ev_verified, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
-      lookup_kernel<<<1, 32, 0, ss>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, B, E.V, E.cum, d_out,
-                                      d_hit);
+      lookup_kernel<<<1, 32, 0, ss>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V, E.cum,
+                                      d_out.p, d_hit.p);
       KCHECK();
       ++E.launches;
       CK(cudaEventRecord(E.ev_join, ss));
@@ -1457,16 +1546,23 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
   }
   const long long per_round = E.launches / 2;
   long long jit_launches = 0;
+  std::vector<int> hits(static_cast<size_t>(nb));
   CK(cudaEventRecord(E.ev_t0, sv));
   for (int64_t r = 0; r < R; ++r) {
     CK(cudaGraphLaunch(gs.g[size_t(r & 1)], sv));
     if (jit && r + 1 < R) {
+      // SamePrimaryJIT: the lanes that missed re-draft from their new
+      // history, batched (the one host round trip of the JIT backup)
       CK(cudaStreamSynchronize(sv));
-      int hit = 0;
-      CK(cudaMemcpy(&hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int), cudaMemcpyDeviceToHost));
-      if (!hit) {
+      CK(cudaMemcpy2D(hits.data(), sizeof(int), reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit),
+                      sizeof(LoopState), sizeof(int), size_t(nb), cudaMemcpyDeviceToHost));
+      int nm = 0;
+      for (int l = 0; l < nb; ++l)
+        if (!hits[size_t(l)]) lanes[size_t(nm++)] = l;
+      if (nm > 0) {
         const long long before = E.launches;
-        draft_steps(E, K, c->scheme, 1, 2, sv);
+        CK(cudaMemcpyAsync(E.d_lanes, lanes.data(), size_t(nm) * 4, cudaMemcpyHostToDevice, sv));
+        draft_lanes(E, K, c->scheme, 1, 2, nm, sv);
         jit_launches += E.launches - before;
       }
     }
@@ -1476,14 +1572,35 @@ ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const s
   CK(cudaStreamSynchronize(sv));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
-  LoopState st = read_state(E);
-  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
-  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
-  cudaFree(d_out);
-  cudaFree(d_hit);
+  std::vector<LoopState> sts;
+  for (int l = 0; l < nb; ++l) sts.push_back(read_state(E, l));
+  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out.p, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
+  if (out_hits) CK(cudaMemcpy(out_hits, d_hit.p, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  const LoopState st = sum_lanes(sts);
   raise_device_error(st);
   fill_stats(st, R, ms, E.launches, stats);
-  copy_out(E, n0, st.n, out, cap, out_len);
+  for (int l = 0; l < nb; ++l)
+    copy_out(E, n0, sts[size_t(l)].n, out ? out + size_t(l) * cap : nullptr, cap, out_lens ? out_lens + l : nullptr, l);
+}
+
+}  // namespace ssd
+
+using namespace ssd;
+
+extern "C" {
+
+ssd_status ssd_run_ssd(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t* out,
+                       int64_t cap, int64_t* out_len, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats) {
+  API_BEGIN
+  run_ssd_impl(h->e, prompt, n0, c, 1, out, cap, out_len, out_outcomes, out_hits, stats);
+  API_END
+}
+
+ssd_status ssd_run_ssd_batch(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t batch,
+                             int32_t* out, int64_t cap, int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits,
+                             ssd_run_stats* stats) {
+  API_BEGIN
+  run_ssd_impl(h->e, prompt, n0, c, batch, out, cap, out_lens, out_outcomes, out_hits, stats);
   API_END
 }
 
@@ -1686,7 +1803,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
     gs.g.push_back(capture_graph(s, [&] {
       prespeculate(E, K, B, lo, Bl, max_f, c->scheme, parity, s);
       recv_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, E.hist);
-      lookup_kernel<<<1, 32, 0, s>>>(E.st, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, E.V, E.cum, nullptr,
+      lookup_kernel<<<1, 32, 0, s>>>(E.st, 1, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, 0, E.V, E.cum, nullptr,
                                      d_hit);
       send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 0, E.send_counter);
       recv_peer_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox);
@@ -1873,7 +1990,8 @@ ssd_status ssd_verify_rows(ssd_engine* h, const float* trows, const float* drows
                        cudaMemcpyHostToDevice, s));
   }
   verify_stats_kernel<<<2 * K + 1, kSampleThreads, 0, s>>>(E.tlogits, E.st, V, dscheme(*ts), dscheme(*ds), E.rstat);
-  verify_decide_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, V, dscheme(*ts), dscheme(*ds), scale, E.rstat, 0);
+  verify_decide_kernel<<<1, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, V, dscheme(*ts), dscheme(*ds), scale, E.rstat, 0,
+                                                    E.hist_stride);
   KCHECK();
   CK(cudaStreamSynchronize(s));
   LoopState st = read_state(E);
@@ -1893,7 +2011,7 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
   cudaStream_t s = E.sv;
   m.ctx_bound = pos + M + 1;
-  prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M);
+  prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M, 0);
   KCHECK();
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, F = sh.ffn, nqkv = m.qd + 2 * m.kvd;
@@ -1999,7 +2117,7 @@ int ssd_debug_mk_trace(ssd_engine* h, int which, int M, int pos, unsigned long l
     const size_t n = size_t(nops) * E_num_sms * 4;
     if (size_t(cap) < n) return -2;
     m.ctx_bound = pos + M + 1;
-    prep_prefill_kernel<<<1, kMaxM, 0, E.sv>>>(E.hist, E.P_pre, pos, M);
+    prep_prefill_kernel<<<1, kMaxM, 0, E.sv>>>(E.hist, E.P_pre, pos, M, 0);
     forward(E, m, E.P_pre, M, m.logits, E.sv);  // warm
     CK(cudaMalloc(&E.mk_trace, n * 8));
     CK(cudaMemset(E.mk_trace, 0, n * 8));

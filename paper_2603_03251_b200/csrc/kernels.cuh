@@ -18,9 +18,28 @@ struct FwdParams {
   int tokens[kMaxM];
   int pos[kMaxM];       // RoPE position
   int slot[kMaxM];      // KV slot written by this token
-  int main_len[kMaxM];  // visible main-cache slots [0, main_len)
+  int main_len[kMaxM];  // visible main-cache keys: slots [mbase, mbase + main_len)
   int bbase[kMaxM];     // visible branch slots [bbase, bbase + blen)
   int blen[kMaxM];
+  int mbase[kMaxM];     // first main slot of the token's sequence (batch lane; 0 at batch 1)
+};
+
+// Key index of `slot` among the keys query (mbase, main_len, bbase, blen)
+// sees, or -1: main keys [0, main_len) live in slots mbase + j, branch keys
+// main_len + i in slots bbase + i.
+__device__ __forceinline__ int visible_key(int slot, int mbase, int main_len, int bbase, int blen) {
+  if (slot >= mbase && slot < mbase + main_len) return slot - mbase;
+  if (slot >= bbase && slot < bbase + blen) return main_len + slot - bbase;
+  return -1;
+}
+
+// Batch lanes (run_protocol_harness with batch_size > 1, sim.cpp:502-601):
+// lane l's loop state is st[l], its history hist[l * hist_stride ..], its
+// main KV slots start at l * lane_slots of each model, and its pre-speculation
+// branches are the rows [l * bper, (l + 1) * bper) of the batched branch step.
+struct Lanes {
+  int hist_stride;
+  int bper;
 };
 
 // Device-resident loop state: the harness' two processes' bookkeeping
@@ -365,7 +384,7 @@ __device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __rest
   const int lane = tid & 31, warp = tid >> 5;
   const int half = hd >> 1;
   const size_t row_len = size_t(H + 2 * KVH) * hd;
-  const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m];
+  const int main_len = P->main_len[m], bbase = P->bbase[m], blen = P->blen[m], mbase = P->mbase[m];
   const int nk = main_len + blen;
   const int j0 = chunk * kAttnChunk, j1 = min(nk, j0 + kAttnChunk);
   const int used = (nk + kAttnChunk - 1) / kAttnChunk;  // chunks holding keys of this query
@@ -376,7 +395,7 @@ __device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __rest
     for (int e = tid; e < M * half; e += kAttnThreads) {
       const int t = e / half, i = e % half;
       const int slot = P->slot[t];
-      const int j = slot < main_len ? slot : (slot >= bbase && slot < bbase + blen ? main_len + slot - bbase : -1);
+      const int j = visible_key(slot, mbase, main_len, bbase, blen);
       if (j < j0 || j >= j1) continue;
       const int pos = P->pos[t];
       const float c = cos_t[size_t(pos) * half + i], sn = sin_t[size_t(pos) * half + i];
@@ -408,7 +427,7 @@ __device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __rest
     const bf16* vbase = vc + size_t(kvh) * S * hd;
     attn_scores<G>(qs, sc, j1 - j0, hd, scale, warp, lane, [&](int jj) {
       const int j = j0 + jj;
-      const int slot = j < main_len ? j : bbase + (j - main_len);
+      const int slot = j < main_len ? mbase + j : bbase + (j - main_len);
       return reinterpret_cast<const uint4*>(kbase + size_t(slot) * hd);
     });
     sync();
@@ -441,7 +460,7 @@ __device__ void attn_item(const float* __restrict__ qkv, const FwdParams* __rest
         const int jj = kg + u * ngrp;
         if (jj < n) {
           const int jabs = j0 + jj;
-          const int slot = jabs < main_len ? jabs : bbase + (jabs - main_len);
+          const int slot = jabs < main_len ? mbase + jabs : bbase + (jabs - main_len);
           vv[u] = reinterpret_cast<const uint4*>(vbase + size_t(slot) * hd)[dc];
         }
       }
@@ -729,7 +748,10 @@ __global__ void __launch_bounds__(kSampleThreads) verify_stats_kernel(const floa
   __shared__ VI shv[32];
   __shared__ VI top[kMaxTopF + 1];
   __shared__ VI wl[(kSampleThreads / 32) * (kMaxTopF + 1)];
+  st += blockIdx.y;  // batch lane
   const int K = st->K;
+  trows += size_t(blockIdx.y) * (K + 1) * V;
+  out += size_t(blockIdx.y) * (2 * K + 1);
   const int r = blockIdx.x;
   const bool target = r <= K;
   if (!target && st->spec_uniform) return;
@@ -774,13 +796,17 @@ __device__ __forceinline__ double row_prob(const float* z, int j, const DScheme&
 __global__ void __launch_bounds__(kSampleThreads) verify_decide_kernel(const float* __restrict__ trows, LoopState* st,
                                                                       int* __restrict__ hist, int V, DScheme ts, DScheme ds,
                                                                       double accept_scale, const RowStat* __restrict__ rs,
-                                                                      int use_draft_stream) {
+                                                                      int use_draft_stream, int hist_stride) {
   __shared__ int s_k;
   __shared__ double s_u;
   __shared__ int s_err;
   __shared__ double shd[32];
   __shared__ VI shv[32];
+  st += blockIdx.x;  // batch lane: its stream, rows and history
+  hist += size_t(blockIdx.x) * hist_stride;
   const int K = st->K;
+  trows += size_t(blockIdx.x) * (K + 1) * V;
+  rs += size_t(blockIdx.x) * (2 * K + 1);
   Mt64& rng = use_draft_stream ? st->drng : st->vrng;
   const bool uni = st->spec_uniform != 0;
   const double inv_v = 1.0 / double(V);
@@ -919,33 +945,46 @@ __global__ void __launch_bounds__(kSampleThreads) verify_decide_kernel(const flo
 
 // ------------------------------------------------------------------ prep
 // Chain inputs [hist[n-1], spec[0..M-2]] at positions n-1 .. (verify /
-// extend / AR step). Causal visibility over the main cache.
-__global__ void prep_chain_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int M) {
-  const int m = threadIdx.x;
+// extend / AR step). Causal visibility over the main cache. grid = batch
+// lanes: lane l fills rows [l*M, (l+1)*M) from st[l] and its history, its
+// main KV slots starting at l * lane_slots.
+__global__ void prep_chain_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int M,
+                                  int hist_stride, int lane_slots) {
+  const int l = blockIdx.x, m = threadIdx.x;
   if (m >= M) return;
+  st += l;
+  hist += size_t(l) * hist_stride;
   const int n = st->n;
   const int tok = m == 0 ? hist[n - 1] : st->spec[m - 1];
-  const int pos = n - 1 + m;
-  P->tokens[m] = tok; P->pos[m] = pos; P->slot[m] = pos;
-  P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+  const int pos = n - 1 + m, r = l * M + m, mb = l * lane_slots;
+  P->tokens[r] = tok; P->pos[r] = pos; P->slot[r] = mb + pos;
+  P->main_len[r] = pos + 1; P->bbase[r] = 0; P->blen[r] = 0; P->mbase[r] = mb;
 }
 
 // Draft step i of specdec::draft: input hist[n-1] (i == 0) or spec[i-1].
-__global__ void prep_draft_step_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int i) {
-  if (threadIdx.x != 0) return;
+// Row m drafts for lane lanes[m] (lanes == nullptr: lane 0, one row).
+__global__ void prep_draft_step_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int i,
+                                       const int* __restrict__ lanes, int nl, int hist_stride, int lane_slots) {
+  const int m = threadIdx.x;
+  if (m >= (lanes ? nl : 1)) return;
+  const int l = lanes ? lanes[m] : 0;
+  st += l;
+  hist += size_t(l) * hist_stride;
   const int n = st->n;
-  const int pos = n - 1 + i;
-  P->tokens[0] = i == 0 ? hist[n - 1] : st->spec[i - 1];
-  P->pos[0] = pos; P->slot[0] = pos; P->main_len[0] = pos + 1; P->bbase[0] = 0; P->blen[0] = 0;
+  const int pos = n - 1 + i, mb = l * lane_slots;
+  P->tokens[m] = i == 0 ? hist[n - 1] : st->spec[i - 1];
+  P->pos[m] = pos; P->slot[m] = mb + pos; P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+  P->mbase[m] = mb;
 }
 
-// Prefill of hist[lo, hi) (chunked by the caller, M <= kMaxM).
-__global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, int lo, int M) {
+// Prefill of hist[lo, hi) (chunked by the caller, M <= kMaxM) into the main
+// KV slots starting at mb.
+__global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, int lo, int M, int mb) {
   const int m = threadIdx.x;
   if (m >= M) return;
   const int pos = lo + m;
-  P->tokens[m] = hist[pos]; P->pos[m] = pos; P->slot[m] = pos;
-  P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+  P->tokens[m] = hist[pos]; P->pos[m] = pos; P->slot[m] = mb + pos;
+  P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0; P->mbase[m] = mb;
 }
 
 // Branch step j (cache.cpp:258-268 continuation drafts, batched): branch b
@@ -953,23 +992,33 @@ __global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, 
 // drafted tokens. KV of branch-local tokens lives in slots
 // kv_base + b*K + j; its attention sees main slots [0, n + k_b) plus its own
 // branch slots.
+// Batch lanes (bper > 0): branch b belongs to lane b / bper, whose KV slots
+// start at lane * lane_slots (main) and lane * lane_slots + kv_base (branches).
 __global__ void prep_branch_kernel(const LoopState* __restrict__ st, const int* __restrict__ bk, const int* __restrict__ btok,
-                                   const int* __restrict__ bt /* [B][K] */, FwdParams* P, int B, int j, int kv_base) {
+                                   const int* __restrict__ bt /* [B][K] */, FwdParams* P, int B, int j, int kv_base,
+                                   int bper, int lane_slots) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
+  const int l = bper > 0 ? b / bper : 0, lb = bper > 0 ? b - l * bper : b;
+  st += l;
   const int K = st->K, n = st->n, k = bk[b];
+  const int mb = l * lane_slots, bb = mb + kv_base + lb * K;
   P->tokens[b] = j == 0 ? btok[b] : bt[b * K + j - 1];
   P->pos[b] = n + k + j;
-  P->slot[b] = kv_base + b * K + j;
+  P->slot[b] = bb + j;
   P->main_len[b] = n + k;
-  P->bbase[b] = kv_base + b * K;
+  P->bbase[b] = bb;
   P->blen[b] = j + 1;
+  P->mbase[b] = mb;
 }
 
 // Per-branch streams: base = one next_u64 of the draft stream (cache.cpp:245),
 // branch b draws K uniforms from Stream(derive_seed(base, b)) (cache.cpp:264).
+// grid = batch lanes (lane l: st[l], bu rows [l*B, (l+1)*B)).
 __global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__ bu /* [B][K] */, int need) {
   __shared__ uint64_t base;
+  st += blockIdx.x;
+  bu += size_t(blockIdx.x) * B * st->K;
   if (threadIdx.x == 0) base = mt_next(st->drng);
   __syncthreads();
   if (!need) return;
@@ -987,63 +1036,76 @@ __global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__
 // :133-138 on a vector of 1/V), for the FastRandom tokens (sim.cpp:35-48).
 // Branch sharding: this engine decodes branches [lo, lo + Bl)
 // of the B keyed ones; bt / brows hold only those ([Bl][K], [K][Bl][V]).
-__global__ void lookup_kernel(LoopState* st, const int* __restrict__ keys, int max_f, const int* __restrict__ off,
-                              const int* __restrict__ bt, const float* __restrict__ brows, int lo, int Bl, int V,
-                              const double* __restrict__ cum, int* __restrict__ log_outcomes, int* __restrict__ log_hits) {
+__global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ keys, int max_f,
+                              const int* __restrict__ off2, const int* __restrict__ bt, const float* __restrict__ brows,
+                              int lo, int Bl, int bper, int V, const double* __restrict__ cum,
+                              int* __restrict__ log_outcomes, int* __restrict__ log_hits) {
   if (threadIdx.x != 0) return;
-  const int K = st->K;
-  const int k = st->out_k, t = st->out_t;
-  const int r = st->round;  // 0-based round being closed
-  // tokens attributed to the source of the verified speculation
-  const long long emitted = k + 1;
-  if (st->spec_src == 0) st->initial_rounds++;
-  else if (st->spec_src == 1) { st->hit_rounds++; st->hit_round_tokens += emitted; }
-  else { st->miss_rounds++; st->miss_round_tokens += emitted; }
-  if (log_outcomes) { log_outcomes[2 * r] = k; log_outcomes[2 * r + 1] = t; }
-  const double v0 = st->clock, v1 = v0 + 1.0, ready = v0 + st->primary_time;
-  st->n += k + 1;
-  st->round = r + 1;
-  if (r + 1 >= st->rounds) {  // last round: no lookup, no backup
-    st->clock = v1;
-    if (log_hits) log_hits[r] = -1;
-    return;
-  }
-  int b = -1;
-  for (int j = 0; j < max_f; ++j)
-    if (keys[k * max_f + j] == t) { b = off[k] + j; break; }
-  const bool hit = b >= 0;
-  const bool from_primary = st->spec_origin == 0;
-  if (from_primary) { st->p_lookups++; st->p_hits += hit; } else { st->b_lookups++; st->b_hits += hit; }
-  if (log_hits) log_hits[r] = hit ? 1 : 0;
-  st->hit = hit;
-  if (hit) {
-    const int lb = b - lo;
-    st->own = lb >= 0 && lb < Bl;
-    if (st->own) {  // otherwise the owning speculator broadcasts the tokens
-      for (int i = 0; i < K; ++i) {
-        st->spec[i] = bt[lb * K + i];
-        st->spec_rows[i] = brows + (size_t(i) * Bl + lb) * size_t(V);
-      }
+  // Batch lanes (sim.cpp:548-577): every lane looks up its own outcome; the
+  // round's virtual clock stalls the whole batch for the backup when any
+  // lane missed. Per-round logs follow lane 0 (the harness' outcomes0 /
+  // hits0).
+  const double v0 = st[0].clock, v1 = v0 + 1.0, ready = v0 + st[0].primary_time;
+  const int r = st[0].round;  // 0-based round being closed
+  const bool last = r + 1 >= st[0].rounds;  // last round: no lookup, no backup
+  bool all_hit = true;
+  for (int l = 0; l < nb; ++l) {
+    LoopState* s = st + l;
+    const int K = s->K;
+    const int k = s->out_k, t = s->out_t;
+    // tokens attributed to the source of the verified speculation
+    const long long emitted = k + 1;
+    if (s->spec_src == 0) s->initial_rounds++;
+    else if (s->spec_src == 1) { s->hit_rounds++; s->hit_round_tokens += emitted; }
+    else { s->miss_rounds++; s->miss_round_tokens += emitted; }
+    if (l == 0 && log_outcomes) { log_outcomes[2 * r] = k; log_outcomes[2 * r + 1] = t; }
+    s->n += k + 1;
+    s->round = r + 1;
+    if (last) {
+      if (l == 0 && log_hits) log_hits[r] = -1;
+      continue;
     }
-    st->spec_origin = 0; st->spec_src = 1; st->spec_uniform = 0;
-    st->clock = fmax(v1, ready);
-  } else {
-    st->own = 0;
-    st->spec_origin = 1; st->spec_src = 2;
-    st->clock = v1 + st->backup_time;
-    if (st->backup_kind == 1) {  // FastRandom: K uniform draws, exact CDF
-      for (int i = 0; i < K; ++i) {
-        const double u = mt_unit(st->drng);
-        int lo = 0, hi = V;  // first idx with u < cum[idx]
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (u < cum[mid]) hi = mid; else lo = mid + 1; }
-        st->spec[i] = lo < V ? lo : V - 1;
-        st->spec_rows[i] = nullptr;
+    // the key table was built under the in-flight speculation's plan
+    const int origin = s->spec_origin;
+    const int* kl = keys + size_t(l) * (K + 1) * max_f;
+    int b = -1;
+    for (int j = 0; j < max_f; ++j)
+      if (kl[k * max_f + j] == t) { b = l * bper + off2[origin * (K + 1) + k] + j; break; }
+    const bool hit = b >= 0;
+    const bool from_primary = origin == 0;
+    if (from_primary) { s->p_lookups++; s->p_hits += hit; } else { s->b_lookups++; s->b_hits += hit; }
+    if (l == 0 && log_hits) log_hits[r] = hit ? 1 : 0;
+    s->hit = hit;
+    if (hit) {
+      const int lb = b - lo;
+      s->own = lb >= 0 && lb < Bl;
+      if (s->own) {  // otherwise the owning speculator broadcasts the tokens
+        for (int i = 0; i < K; ++i) {
+          s->spec[i] = bt[lb * K + i];
+          s->spec_rows[i] = brows + (size_t(i) * Bl + lb) * size_t(V);
+        }
       }
-      st->spec_uniform = 1;
+      s->spec_origin = 0; s->spec_src = 1; s->spec_uniform = 0;
     } else {
-      st->spec_uniform = 0;  // the host runs the JIT re-draft
+      all_hit = false;
+      s->own = 0;
+      s->spec_origin = 1; s->spec_src = 2;
+      if (s->backup_kind == 1) {  // FastRandom: K uniform draws, exact CDF
+        for (int i = 0; i < K; ++i) {
+          const double u = mt_unit(s->drng);
+          int a = 0, z = V;  // first idx with u < cum[idx]
+          while (a < z) { const int mid = (a + z) >> 1; if (u < cum[mid]) z = mid; else a = mid + 1; }
+          s->spec[i] = a < V ? a : V - 1;
+          s->spec_rows[i] = nullptr;
+        }
+        s->spec_uniform = 1;
+      } else {
+        s->spec_uniform = 0;  // the host runs the JIT re-draft
+      }
     }
   }
+  const double clock = last ? v1 : (all_hit ? fmax(v1, ready) : v1 + st[0].backup_time);
+  for (int l = 0; l < nb; ++l) st[l].clock = clock;
 }
 
 // After a JIT / initial draft of spec[] from rows: origin bookkeeping.
@@ -1051,6 +1113,29 @@ __global__ void set_spec_rows_kernel(LoopState* st, const float* __restrict__ ro
   if (threadIdx.x != 0) return;
   for (int i = 0; i < st->K; ++i) st->spec_rows[i] = rows + size_t(i) * V;
   st->spec_origin = origin; st->spec_src = src; st->spec_uniform = 0;
+}
+
+// Batched draft (the initial drafts and the JIT backups of a batch): row m of
+// draft step i drafted lane lanes[m]; its row is rows[(i * row_step + m) * V].
+__global__ void set_lane_spec_rows_kernel(LoopState* st, const int* __restrict__ lanes, int nl, const float* __restrict__ rows,
+                                          int row_step, int V, int origin, int src) {
+  const int m = threadIdx.x;
+  if (m >= nl) return;
+  LoopState* s = st + lanes[m];
+  for (int i = 0; i < s->K; ++i) s->spec_rows[i] = rows + (size_t(i) * row_step + m) * V;
+  s->spec_origin = origin; s->spec_src = src; s->spec_uniform = 0;
+}
+
+// One uniform per row from its lane's draft stream (specdec.cpp:19).
+__global__ void draw_lane_uniforms_kernel(LoopState* st, const int* __restrict__ lanes, int nl, double* u) {
+  if (threadIdx.x == 0)
+    for (int m = 0; m < nl; ++m) u[m] = mt_unit(st[lanes[m]].drng);
+}
+
+// Scatter the tokens drawn for rows m into st[lanes[m]].spec[i].
+__global__ void scatter_spec_kernel(LoopState* st, const int* __restrict__ lanes, int nl, int i, const int* __restrict__ tok) {
+  const int m = threadIdx.x;
+  if (m < nl) st[lanes[m]].spec[i] = tok[m];
 }
 
 // SD / AR commit: n += k + 1 (history already appended by verify).

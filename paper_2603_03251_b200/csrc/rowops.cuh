@@ -227,10 +227,16 @@ __global__ void __launch_bounds__(kRowThreads) row_keys_kernel(int nch, int T, c
                                                                const LoopState* __restrict__ st,
                                                                const int* __restrict__ excl_explicit, int n_excl,
                                                                int max_f, int* __restrict__ keys, int* __restrict__ bk,
-                                                               int* __restrict__ btok) {
+                                                               int* __restrict__ btok, int nrows, int bper) {
+  // Batch lanes: grid = lanes x nrows; lane l's key table is
+  // keys[l][nrows][max_f], its branches bk/btok[l * bper ..].
   __shared__ VI top[kMaxTopF + 1];
   __shared__ VI wl[(kRowThreads / 32) * (kMaxTopF + 1)];
-  const int k = blockIdx.x, nrows = gridDim.x;
+  const int row = blockIdx.x, l = row / nrows, k = row % nrows;
+  if (st) st += l;
+  keys += size_t(l) * nrows * max_f;
+  bk += l * bper;
+  btok += l * bper;
   const int origin = st ? st->spec_origin : 0;
   const int F = fan2[origin * nrows + k];
   const int off = off2[origin * nrows + k];
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(kRowThreads) row_keys_kernel(int nch, int T, c
     for (int j = threadIdx.x; j < max_f; j += kRowThreads) keys[k * max_f + j] = -1;
     return;
   }
-  block_topk_pairs<kRowThreads>(cand + size_t(k) * nch * T, nch * T, min(F + 1, T), top, wl);
+  block_topk_pairs<kRowThreads>(cand + size_t(row) * nch * T, nch * T, min(F + 1, T), top, wl);
   if (threadIdx.x == 0) {
     int got = 0;
     for (int t = 0; t < min(F + 1, T) && got < F; ++t) {

@@ -75,7 +75,7 @@ for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
             j, (c[ok, 1].max() - r0) / 1e3, (c[ok, 2].max() - c[ok, 1].max()) / 1e3, last, rel(c[last, 7]),
             rel(c[last, 3]), rel(c[last, 4]), rel(c[last, 5]), rel(c[last, 6]), rel(c[last, 2])))
     for r in f[:14]:
-        print(f"      {KIND.get(int(r[0]), int(r[0])):12s} entry {(r[1] - t0) / 1e3:8.2f} ready {(r[2] - t0) / 1e3:8.2f} "
+        print(f"      {str(KIND.get(int(r[0]), int(r[0]))):12s} entry {(r[1] - t0) / 1e3:8.2f} ready {(r[2] - t0) / 1e3:8.2f} "
               f"exit {(r[3] - t0) / 1e3:8.2f}")
 eng.close()
 
