@@ -140,6 +140,17 @@ ssd_status ssd_uniform_fanout(int32_t lookahead, int32_t budget, int32_t role, s
 /* cache::conditional_hit_rate (cache.hpp:79-85, cache.cpp:150-169). */
 double ssd_conditional_hit_rate(const ssd_plan* plan, double acceptance, double exponent);
 
+/* perf::speedup_batch (perf.hpp:54-59, perf.cpp:44-55): per-sequence
+ * speedup of a batch whose rounds stall for the backup when any sequence
+ * misses (all-hit probability hit_rate^batch). Times in verify passes. */
+ssd_status ssd_speedup_batch(double hit_rate, double hit_tokens, double miss_tokens, double primary_time,
+                             double backup_time, double batch, double* out);
+/* perf::critical_batch (perf.hpp:61-72, perf.cpp:57-73): the batch size b*
+ * at which the free (FastRandom) backup overtakes the JIT re-draft; the
+ * Saguaro fallback policy uses JIT below b*. SSD_NO_CROSSOVER when one
+ * strategy dominates at every batch size. */
+ssd_status ssd_critical_batch(double hit_rate, double hit_tokens, double miss_tokens, double primary_time,
+                              double* out);
 /* --------------------------------------------------------------- engine */
 
 /* Materialise the (target, draft) pair on `device` with synthetic weights

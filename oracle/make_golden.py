@@ -154,6 +154,21 @@ def cases():
          "primary_plan": {"fan": [7, 7, 8]}, "backup_plan": {"fan": [7, 7, 8]}})
     add("harness jit batch 2", {**base_config(10, 1, 0.8, 3, 12, 123), "mode": "harness", "rounds": 80, "batch_size": 2,
                                 "backup": "same_primary_jit", "timing": {"primary_time": 0.4, "backup_time": 0.4}})
+    add("harness fast_random batch 4 backup 0.5", {**base_config(10, 1, 0.8, 3, 12, 124), "mode": "harness", "rounds": 80,
+                                                   "batch_size": 4, "timing": {"primary_time": 0.4, "backup_time": 0.5}})
+    add("harness batch 3 differing primary and backup plans",
+        {**base_config(12, 1, 0.75, 3, 10, 125), "mode": "harness", "rounds": 60, "batch_size": 3,
+         "primary_plan": {"fan": [4, 3, 2, 1]}, "backup_plan": {"fan": [1, 1, 4, 4]}})
+    # ---- perf model (perf.cpp:19-73): batch speedup and the backup crossover b*
+    for p_, eh, em, tp, tb, b in ((0.9, 3.2, 1.6, 0.8, 0.8, 4), (0.7, 2.5, 1.2, 0.5, 0.0, 16), (0.95, 3.5, 2.0, 1.0, 1.0, 2),
+                                  (0.6, 2.0, 1.5, 0.3, 0.3, 1), (0.8, 3.0, 1.0, 0.4, 0.4, 8)):
+        add(f"perf p={p_} Eh={eh} Em={em} tp={tp} tb={tb} b={b}",
+            {"op": "perf", "hit_rate": p_, "hit_tokens": eh, "miss_tokens": em, "primary_time": tp, "backup_time": tb,
+             "batch": b, "critical": True})
+    add("perf no crossover", {"op": "perf", "hit_rate": 0.5, "hit_tokens": 1.0, "miss_tokens": 3.0, "primary_time": 0.5,
+                              "critical": True})
+    add("perf hit rate out of range", {"op": "perf", "hit_rate": 1.5, "hit_tokens": 2.0, "miss_tokens": 1.0,
+                                       "primary_time": 0.5})
     add("harness synthetic rejected (test_sim.cpp:353-358)",
         {**base_config(8, 1, 0.8, 2, 8, 121), "mode": "harness", "rounds": 10, "synthetic_hit_rate": 0.5})
     # ---- shipped configs (proj/configs/simulate_*.json), shortened

@@ -187,6 +187,15 @@ json run(const json& req) {
     }
     return o;
   }
+  if (op == "perf") {  // perf.cpp:19-73
+    const Yields y{req.at("hit_tokens").get<double>(), req.at("miss_tokens").get<double>()};
+    const double p = req.at("hit_rate"), tp = req.at("primary_time"), tb = req.value("backup_time", 0.0);
+    json o;
+    o["speedup_ssd"] = speedup_ssd(p, y, tp, tb);
+    if (req.contains("batch")) o["speedup_batch"] = speedup_batch(p, y, tp, tb, req.at("batch").get<double>());
+    if (req.value("critical", false)) o["critical_batch"] = critical_batch(p, y, tp);
+    return o;
+  }
   if (op == "top_indices") {
     const auto z = req.at("z").get<std::vector<double>>();
     return json{{"idx", rank_tokens(z, req.at("count"))}};

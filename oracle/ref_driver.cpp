@@ -17,6 +17,7 @@
 #include "ssdlab/cache.hpp"
 #include "ssdlab/categorical.hpp"
 #include "ssdlab/errors.hpp"
+#include "ssdlab/perf.hpp"
 #include "ssdlab/lm.hpp"
 #include "ssdlab/rng.hpp"
 #include "ssdlab/sim.hpp"
@@ -113,6 +114,16 @@ json run(const json& req) {
       o["fan"] = cache::geometric_fanout(g.at(0), g.at(1), K, g.at(2)).fan_out;
       o["continuous"] = cache::geometric_fanout_continuous(g.at(0), g.at(1), K, g.at(2).get<double>()).fan_out;
     }
+    return o;
+  }
+  if (op == "perf") {
+    const perf::TokenYields y{req.at("hit_tokens").get<double>(), req.at("miss_tokens").get<double>(), 1.0, 0.0};
+    const perf::TimingParams t{req.at("primary_time").get<double>(), req.value("backup_time", 0.0)};
+    const double p = req.at("hit_rate");
+    json o;
+    o["speedup_ssd"] = perf::speedup_ssd(p, y, t);
+    if (req.contains("batch")) o["speedup_batch"] = perf::speedup_batch(p, y, t, req.at("batch").get<double>());
+    if (req.value("critical", false)) o["critical_batch"] = perf::critical_batch(p, y, t);
     return o;
   }
   if (op == "top_indices") {

@@ -668,6 +668,39 @@ HarnessOut sim_harness(const SimCfg& c) {
   return out;
 }
 
+// ============================================================== perf
+// perf.cpp:10-15
+static void check_p(double p) {
+  if (!(p >= 0.0) || !(p <= 1.0)) throw Error("perf: hit_rate must be in [0, 1]");
+}
+
+// perf.cpp:19-27: [p E_hit + (1-p) E_miss] / [p max(1, T_p) + (1-p)(1 + T_b)]
+double speedup_ssd(double p, const Yields& y, double tp, double tb) {
+  check_p(p);
+  const double tokens = p * y.hit + (1.0 - p) * y.miss;
+  const double latency = p * std::max(1.0, tp) + (1.0 - p) * (1.0 + tb);
+  return tokens / latency;
+}
+
+// perf.cpp:44-55: whole-batch stall, the all-hit probability is p^b
+double speedup_batch(double p, const Yields& y, double tp, double tb, double batch) {
+  check_p(p);
+  if (!(batch >= 1.0)) throw Error("speedup_batch: batch must be >= 1");
+  const double tokens = p * y.hit + (1.0 - p) * y.miss;
+  const double all = std::pow(p, batch);
+  return tokens / (all * std::max(1.0, tp) + (1.0 - all) * (1.0 + tb));
+}
+
+// perf.cpp:57-73: b* = log(1 + 1/T_p - E_hit / (T_p E)) / log(p)
+double critical_batch(double p, const Yields& y, double tp) {
+  if (!(p > 0.0) || !(p < 1.0)) throw Error("critical_batch: hit_rate must be in (0, 1)");
+  if (!(tp > 0.0)) throw Error("critical_batch: primary_time must be > 0");
+  const double mean = p * y.hit + (1.0 - p) * y.miss;
+  const double arg = 1.0 + 1.0 / tp - y.hit / (tp * mean);
+  if (!(arg > 0.0) || arg > 1.0) throw NoCrossoverError("critical_batch: one backup strategy dominates at every batch size");
+  return std::log(arg) / std::log(p);
+}
+
 // ============================================================== Markov LM
 // lm.cpp:49-63
 MarkovLM::MarkovLM(int V, int order, std::uint64_t seed, std::vector<Row> rows)

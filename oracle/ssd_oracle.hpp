@@ -141,6 +141,14 @@ Plan geometric_plan(double a, double r, int K, int budget, Origin role = Origin:
 Plan uniform_plan(int K, int budget, Origin role = Origin::Primary);
 double plan_hit_rate(std::span<const int> fan, double a, double r);
 
+// ---------------------------------------------------------------- perf
+// reference perf.hpp:7-80 / perf.cpp:19-73: the latency model of the loop
+// and the batch-size crossover of the two backup strategies.
+struct Yields { double hit = 1.0, miss = 1.0; };
+double speedup_ssd(double p, const Yields& y, double tp, double tb);
+double speedup_batch(double p, const Yields& y, double tp, double tb, double batch);
+double critical_batch(double p, const Yields& y, double tp);
+
 struct CacheEntry {
   Outcome key;
   Spec spec;

@@ -62,6 +62,9 @@ SIGNATURES = {
     "ssd_geometric_fanout": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_int32, P(Plan)]),
     "ssd_uniform_fanout": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, P(Plan)]),
     "ssd_conditional_hit_rate": (C.c_double, [P(Plan), C.c_double, C.c_double]),
+    "ssd_speedup_batch": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                    P(C.c_double)]),
+    "ssd_critical_batch": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, P(C.c_double)]),
     "ssd_engine_create": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32, C.c_int32,
                                     P(EngineP)]),
     "ssd_engine_create_role": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32,

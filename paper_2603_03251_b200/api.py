@@ -126,6 +126,40 @@ def conditional_hit_rate(plan: FanOutPlan, acceptance: float, exponent: float) -
 FAST_RANDOM, SAME_PRIMARY_JIT = "fast_random", "same_primary_jit"  # sim::BackupKind
 
 
+def speedup_batch(hit_rate: float, hit_tokens: float, miss_tokens: float, primary_time: float,
+                  backup_time: float, batch: float) -> float:
+    """perf::speedup_batch (perf.cpp:44-55): per-sequence speedup under
+    whole-batch stalls; times in units of one verification pass."""
+    out = C.c_double()
+    _check(N.load().ssd_speedup_batch(hit_rate, hit_tokens, miss_tokens, primary_time, backup_time, batch,
+                                      C.byref(out)))
+    return out.value
+
+
+def critical_batch(hit_rate: float, hit_tokens: float, miss_tokens: float, primary_time: float) -> float:
+    """perf::critical_batch (perf.cpp:57-73): the batch size b* where the
+    free backup overtakes the JIT re-draft (NoCrossoverError if none)."""
+    out = C.c_double()
+    _check(N.load().ssd_critical_batch(hit_rate, hit_tokens, miss_tokens, primary_time, C.byref(out)))
+    return out.value
+
+
+def saguaro_backup(batch: int, hit_rate: float, hit_tokens: float, miss_tokens: float, primary_time: float,
+                   jit_time: Optional[float] = None, fast_time: float = 0.0) -> str:
+    """The Saguaro fallback policy (PAPER §5): re-use the
+    primary speculator as a just-in-time backup below the crossover batch
+    b*, the free FastRandom backup at or above it. Without a crossover the
+    strategy with the larger speedup_batch at this batch size wins."""
+    jt = primary_time if jit_time is None else jit_time
+    try:
+        return SAME_PRIMARY_JIT if batch < critical_batch(hit_rate, hit_tokens, miss_tokens, primary_time) \
+            else FAST_RANDOM
+    except (NoCrossoverError, Error):
+        j = speedup_batch(hit_rate, hit_tokens, miss_tokens, primary_time, jt, batch)
+        f = speedup_batch(hit_rate, hit_tokens, miss_tokens, primary_time, fast_time, batch)
+        return SAME_PRIMARY_JIT if j > f else FAST_RANDOM
+
+
 @dataclass
 class SimConfig:
     """sim::SimConfig (sim.hpp:28-53); the models live in the Engine."""

@@ -121,4 +121,31 @@ double ssd_conditional_hit_rate(const ssd_plan* p, double a, double r) {
   return hit_rate(f, a, r);
 }
 
+// Latency model of the loop (perf.cpp:19-55) and the backup crossover b*
+// (perf.cpp:57-73) that drives the Saguaro fallback policy at batch > 1:
+// below b* re-using the primary as a JIT backup wins, at or above it the
+// free FastRandom backup does (PAPER §5, whole-batch stalls).
+ssd_status ssd_speedup_batch(double p, double hit_tokens, double miss_tokens, double primary_time, double backup_time,
+                             double batch, double* out) {
+  if (!(p >= 0.0) || !(p <= 1.0)) { ssd::g_last_error = "perf: hit_rate must be in [0, 1]"; return SSD_ERROR; }
+  if (!(batch >= 1.0)) { ssd::g_last_error = "speedup_batch: batch must be >= 1"; return SSD_ERROR; }
+  const double tokens = p * hit_tokens + (1.0 - p) * miss_tokens;
+  const double all = std::pow(p, batch);
+  *out = tokens / (all * std::max(1.0, primary_time) + (1.0 - all) * (1.0 + backup_time));
+  return SSD_OK;
+}
+
+ssd_status ssd_critical_batch(double p, double hit_tokens, double miss_tokens, double primary_time, double* out) {
+  if (!(p > 0.0) || !(p < 1.0)) { ssd::g_last_error = "critical_batch: hit_rate must be in (0, 1)"; return SSD_ERROR; }
+  if (!(primary_time > 0.0)) { ssd::g_last_error = "critical_batch: primary_time must be > 0"; return SSD_ERROR; }
+  const double mean = p * hit_tokens + (1.0 - p) * miss_tokens;
+  const double arg = 1.0 + 1.0 / primary_time - hit_tokens / (primary_time * mean);
+  if (!(arg > 0.0) || arg > 1.0) {
+    ssd::g_last_error = "critical_batch: one backup strategy dominates at every batch size";
+    return SSD_NO_CROSSOVER;
+  }
+  *out = std::log(arg) / std::log(p);
+  return SSD_OK;
+}
+
 }  // extern "C"

@@ -91,3 +91,51 @@ def test_engine_fails_loudly_without_gpu(lib):
     ts, ds = shapes("tiny", max_ctx=128)
     with pytest.raises(P.CudaError):
         P.Engine(ts, ds, P.Pair())
+
+
+def _perf_cases():
+    with open(os.path.join(ROOT, "tests", "golden", "ref_golden.json")) as f:
+        return [c for c in json.load(f) if c["req"]["op"] == "perf"]
+
+
+@pytest.mark.parametrize("case", _perf_cases(), ids=lambda c: c["name"])
+def test_perf_model_matches_reference_golden(lib, case):
+    """ssd_speedup_batch / ssd_critical_batch (the batch-size crossover that
+    drives the Saguaro fallback policy) against the compiled reference's
+    perf.cpp:19-73 on the same inputs."""
+    import paper_2603_03251_b200 as P
+    r, out = case["req"], case["out"]
+    args = (r["hit_rate"], r["hit_tokens"], r["miss_tokens"], r["primary_time"])
+    if "error" in out:
+        if out["code"] == 9:  # NoCrossoverError from critical_batch
+            with pytest.raises(P.NoCrossoverError):
+                P.critical_batch(*args)
+        else:
+            with pytest.raises(P.Error):
+                P.speedup_batch(*args, r.get("backup_time", 0.0), r.get("batch", 1))
+        return
+    if "batch" in r:
+        assert P.speedup_batch(*args, r.get("backup_time", 0.0), r["batch"]) == pytest.approx(out["speedup_batch"],
+                                                                                             rel=1e-14)
+    # batch 1 is speedup_ssd (perf.cpp:19-27)
+    assert P.speedup_batch(*args, r.get("backup_time", 0.0), 1) == pytest.approx(out["speedup_ssd"], rel=1e-14)
+    if r.get("critical"):
+        if "critical_batch" in out:
+            assert P.critical_batch(*args) == pytest.approx(out["critical_batch"], rel=1e-14)
+        else:
+            with pytest.raises(P.NoCrossoverError):
+                P.critical_batch(*args)
+
+
+def test_saguaro_fallback_policy(lib):
+    """JIT backup below b*, FastRandom at or above it; without a crossover the
+    strategy with the larger batch speedup."""
+    import paper_2603_03251_b200 as P
+    p, eh, em, tp = 0.8, 3.0, 1.0, 0.4
+    b = P.critical_batch(p, eh, em, tp)
+    assert 2.0 < b < 3.0
+    assert P.saguaro_backup(1, p, eh, em, tp) == P.SAME_PRIMARY_JIT
+    assert P.saguaro_backup(2, p, eh, em, tp) == P.SAME_PRIMARY_JIT
+    assert P.saguaro_backup(3, p, eh, em, tp) == P.FAST_RANDOM
+    assert P.saguaro_backup(8, p, eh, em, tp) == P.FAST_RANDOM
+    assert P.saguaro_backup(4, 0.5, 1.0, 3.0, 0.5) in (P.SAME_PRIMARY_JIT, P.FAST_RANDOM)
