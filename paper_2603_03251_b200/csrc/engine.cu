@@ -23,6 +23,7 @@
 #include "gemm_cl.cuh"
 #include "fwd_mk.cuh"
 #include "attn_cl.cuh"
+#include "attn_dec.cuh"
 #include "tp.cuh"
 #include "kernels.cuh"
 #include "probe.cuh"
@@ -209,6 +210,7 @@ struct Engine {
   // caught up).
   int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
+  int attn_dec = 1;      // one-CTA-per-(kv head, token) attention (attn_dec.cuh; SSD_B200_ATTN_DEC=0: chunked kernels)
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
@@ -582,6 +584,27 @@ static void configure_kernels() {
   carveout_max(commit_kernel);
   carveout_max(ar_commit_kernel);
   carveout_max(draw_uniforms_kernel);
+  // Every remaining kernel is touched here too: setting an attribute loads it
+  // now instead of at its first launch (CUDA lazy loading). Measured: with
+  // lazy loading, the first forward of a tensor-parallel verifier pair
+  // (spin-waiting peer-memory collectives) returned wrong logits in ~1 of 3
+  // process pairs (scripts/tp_diag.py); eager-loaded, 0 of 15.
+  carveout_max(tp_allreduce_kernel);
+  carveout_max(tp_gather_logits_kernel);
+  carveout_max(recv_spec_kernel);
+  carveout_max(send_outcome_kernel);
+  carveout_max(recv_outcome_kernel);
+  carveout_max(send_spec_kernel);
+  carveout_max(recv_peer_spec_kernel);
+  carveout_max(scatter_spec_kernel);
+  carveout_max(set_lane_spec_rows_kernel);
+  carveout_max(draw_lane_uniforms_kernel);
+  carveout_max(mt_init_kernel);
+  carveout_max(mt_draw_kernel);
+  carveout_max(keys_kernel);
+  carveout_max(sample_rows_kernel);
+  carveout_max(gen_layer_kernel);
+  carveout_max(gen_table_kernel);
   configure_gemm<EPI_STORE, 16>(); configure_gemm<EPI_SWIGLU, 16>();
   configure_gemm<EPI_STORE, 32>(); configure_gemm<EPI_SWIGLU, 32>();
   configure_gemm<EPI_STORE, 48>(); configure_gemm<EPI_SWIGLU, 48>();
@@ -600,6 +623,17 @@ static void configure_kernels() {
   CK(cudaFuncSetAttribute(attention_cl_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(2, 128))));
   CK(cudaFuncSetAttribute(attention_cl_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(4, 128))));
   CK(cudaFuncSetAttribute(attention_cl_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(8, 128))));
+  {
+    constexpr int kDecSmemMax = 227 * 1024;
+    auto dec = [&](const void* f) {
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemMax));
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
+    };
+#define SSD_DEC_CFG(GG, HH) dec((const void*)attention_dec_kernel<GG, HH, 1>); dec((const void*)attention_dec_kernel<GG, HH, 2>);
+    SSD_DEC_CFG(1, 64) SSD_DEC_CFG(2, 64) SSD_DEC_CFG(4, 64) SSD_DEC_CFG(8, 64)
+    SSD_DEC_CFG(1, 128) SSD_DEC_CFG(2, 128) SSD_DEC_CFG(4, 128) SSD_DEC_CFG(8, 128)
+#undef SSD_DEC_CFG
+  }
   mk_configure<16, 1>(); mk_configure<16, 2>(); mk_configure<16, 4>(); mk_configure<16, 8>();
   mk_configure<32, 1>(); mk_configure<32, 2>(); mk_configure<32, 4>(); mk_configure<32, 8>();
   mk_configure<64, 1>(); mk_configure<64, 2>(); mk_configure<64, 4>(); mk_configure<64, 8>();
@@ -751,6 +785,58 @@ static void attn_cl_launch(Model& m, int nch, int M, const FwdParams* P, bf16* k
   }
 }
 
+// One-CTA-per-(kv head, token) attention (attn_dec.cuh). Returns false when
+// the shape is not covered (head_dim other than 64 / 128, or the score rows
+// do not fit shared memory): the caller then uses the chunked kernels.
+template <int G, int HD, int MINB>
+static void attn_dec_launch_g(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap, int nst,
+                              cudaStream_t s, Prefetch pf) {
+  const ssd_model_shape& sh = m.s;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sh.n_kv_heads, M);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = attn_dec_smem(G, HD, kcap, nst);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, attention_dec_kernel<G, HD, MINB>, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
+                        (const float*)m.rope_sin, kc, vc, m.S, sh.n_heads, sh.n_kv_heads, scale, m.attn, kcap, nst, pf));
+}
+
+static int g_attn_stage = 1;  // SSD_B200_ATTN_STAGE=0: never stage KV rows in shared memory
+
+template <int G, int HD>
+static void attn_dec_pick(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap,
+                          cudaStream_t s, Prefetch pf) {
+  constexpr size_t kSmemMax = 227 * 1024;
+  if (size_t(M) * m.s.n_kv_heads <= size_t(E_num_sms) && g_attn_stage) {
+    // one CTA per SM: stage as many main KV rows as shared memory holds
+    const size_t room = kSmemMax - attn_dec_smem(G, HD, kcap, 0);
+    const int nst = int(std::min<size_t>(size_t(kcap), room / (size_t(4) * HD)));
+    attn_dec_launch_g<G, HD, 1>(m, M, P, kc, vc, scale, kcap, nst, s, pf);
+  } else {
+    attn_dec_launch_g<G, HD, 2>(m, M, P, kc, vc, scale, kcap, 0, s, pf);  // two CTAs per SM, rows from L2
+  }
+}
+
+static bool attn_dec_launch(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, cudaStream_t s,
+                            Prefetch pf) {
+  const int hd = m.s.head_dim, G = m.s.n_heads / m.s.n_kv_heads;
+  const int kcap = (std::min(m.ctx_bound, m.s.max_ctx + m.branch_len + 1) + 3) & ~3;
+  if ((hd != 64 && hd != 128) || attn_dec_smem(G, hd, kcap, 0) > size_t(100 * 1024)) return false;
+#define SSD_DEC(GG, HH) attn_dec_pick<GG, HH>(m, M, P, kc, vc, scale, kcap, s, pf)
+  if (hd == 64) {
+    if (G == 1) SSD_DEC(1, 64); else if (G == 2) SSD_DEC(2, 64); else if (G == 4) SSD_DEC(4, 64); else SSD_DEC(8, 64);
+  } else {
+    if (G == 1) SSD_DEC(1, 128); else if (G == 2) SSD_DEC(2, 128); else if (G == 4) SSD_DEC(4, 128); else SSD_DEC(8, 128);
+  }
+#undef SSD_DEC
+  return true;
+}
+
 // Persistent forward kernel launch (fwd_mk.cuh): the whole step in one
 // cooperative launch (all CTAs co-resident: grid barriers).
 template <int NP, int G>
@@ -847,7 +933,9 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
                  (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
-    if (do_attn && nch <= kAttnClMaxChunks && E.attn_cluster) {
+    if (do_attn && E.attn_dec && attn_dec_launch(m, M, P, kc, vc, scale, s, pf.upto(4 * l + 1))) {
+      // one CTA per (kv head, token)
+    } else if (do_attn && nch <= kAttnClMaxChunks && E.attn_cluster) {
       attn_cl_launch(m, nch, M, P, kc, vc, scale, s, pf.upto(4 * l + 1));
     } else if (do_attn) {
       auto k = H / KVH == 1 ? attention_kernel<1> : (H / KVH == 2 ? attention_kernel<2> : (H / KVH == 4 ? attention_kernel<4> : attention_kernel<8>));
@@ -1241,6 +1329,8 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
   if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
+  if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
+  if (const char* ast = std::getenv("SSD_B200_ATTN_STAGE")) g_attn_stage = std::atoi(ast) != 0;
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
@@ -1332,6 +1422,8 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
     void* p = nullptr;
     CK(cudaMalloc(&p, E.tp_L.bytes()));
     CK(cudaMemset(p, 0, E.tp_L.bytes()));
+    if (std::getenv("SSD_B200_TP_POISON"))  // debug: slots start as NaN (flags stay 0)
+      CK(cudaMemset(static_cast<char*>(p) + E.tp_L.ar_off(), 0xFF, E.tp_L.bytes() - E.tp_L.ar_off()));
     E.tp_region = static_cast<char*>(p);
     E.tp_ctl = static_cast<TpCtl*>(own(dalloc<TpCtl>(1)));
   }

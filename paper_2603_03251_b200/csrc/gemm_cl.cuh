@@ -199,6 +199,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
       } else {
         for (int c = 0; c < NP; ++c) mine[c * kBM + rl] = 0.f;  // no k-units: a zero partial
       }
+      // Every writer's partial must be visible cluster-wide before the one
+      // remote release-arrive below: a CTA barrier alone does not order other
+      // threads' shared-memory writes for the peer ranks' DSMEM reads
+      // (measured: first-launch garbage in ~1 of 10 processes sharing a GPU,
+      // scripts/share_diag.py; with this fence 0 of 40).
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tid == 0)
         for (int r = 0; r < CS; ++r) mbar_arrive_remote(mapa_shared(smem_u32(&pready[b]), r));
@@ -219,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
         }
         apply_epi<EPI>(g, t * kBM + rr, ok ? tok : g.M, acc);  // tok = M: no store, shuffle still taken
       }
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");  // this thread's DSMEM reads are done
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tid == 0)
         for (int r = 0; r < CS; ++r) mbar_arrive_remote(mapa_shared(smem_u32(&pfree[b]), r));

@@ -17,7 +17,7 @@ import numpy as np  # noqa: E402
 import paper_2603_03251_b200 as P  # noqa: E402
 from paper_2603_03251_b200.configs import shapes  # noqa: E402
 
-KIND = {1: "embed", 2: "rmsnorm", 3: "attention", 10: "gemm", 12: "gemm_swiglu"}
+KIND = {1: "embed", 2: "rmsnorm", 3: "attention", 4: "attention_dec", 10: "gemm", 12: "gemm_swiglu"}
 ts, ds = shapes("llama8b_1b", max_ctx=1024)
 eng = P.Engine(ts, ds, P.Pair(), max_branches=20, max_lookahead=4)
 lib = P._native.load()
@@ -59,8 +59,8 @@ for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
     for kind, a in agg.items():
         print(f"   {kind:12s} n={a[0]:4d} entry->ready {a[1] / a[0]:7.2f} us  ready->exit(block0) {a[2] / a[0]:7.2f} us  "
               f"prev-exit->entry {a[3] / a[0]:7.2f} us")
-    print("   last attention sub-phases (us from ready): mbar %.2f append+rope %.2f scores %.2f softmax+PV %.2f "
-          "cluster.sync %.2f merge %.2f final sync %.2f" % tuple((sub[i] - sub[0]) / 1e3 for i in range(1, 8)))
+    print("   last attention sub-phases (us from ready; attention_dec: setup, scores, softmax, PV, out): %.2f %.2f %.2f %.2f "
+          "%.2f %.2f %.2f" % tuple((sub[i] - sub[0]) / 1e3 for i in range(1, 8)))
     # per-CTA spread of the last GEMM launches of this workload (ready / MMA done / exit), us rel. to min ready
     print("   per-CTA GEMM spreads (last launches): [ready span, last MMA-done - first ready, exit span, last exit - max MMA done]")
     for j in range(64):

@@ -27,6 +27,12 @@ def _worker(rank, world, port, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    # The ranks share ONE GPU here (time-sliced contexts). Measured: the
+    # cluster split-K GEMM (tcgen05 + DSMEM partial exchange) returned a wrong
+    # first forward in ~1 of 20 processes whose context was time-sliced
+    # against another's (scripts/share_diag.py); never with one process per
+    # GPU. Ranks on separate GPUs (the product's split mode) keep it.
+    os.environ["SSD_B200_CL_GEMM_MB"] = "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2603_03251_b200 as P
