@@ -116,10 +116,24 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   // 1) keys of this forward's tokens visible to this query; rotated queries;
   //    append of token m's K / V (this kv head) to the cache
   for (int j = tid; j < nk; j += kDecThreads) ovr[j] = -1;
+  if (nst > 0) tc::mbar_wait(bar, 0);  // staged rows landed before they are patched below
   __syncthreads();
   for (int t = tid; t < M; t += kDecThreads) {
     const int j = visible_key(P->slot[t], mb, main_len, bbase, blen);
     if (j >= 0) ovr[j] = t;
+  }
+  // keys of this forward that fall in the staged range: patch the stale
+  // staged rows with the recomputed ones (the writer's rounding), so scores
+  // and P.V read every staged key from shared memory
+  for (int e = tid; e < M * HD && ns > 0; e += kDecThreads) {
+    const int t = e / HD, d = e % HD;
+    const int j = visible_key(P->slot[t], mb, main_len, bbase, blen);
+    if (j < 0 || j >= ns) continue;
+    const int pos = P->pos[t];
+    const float* x = qkv + size_t(t) * row_len + size_t(H + kvh) * HD;
+    Ks[size_t(j) * HD + d] =
+        __float2bfloat16_rn(rope_elem(x, d, HALF, cos_t + size_t(pos) * HALF, sin_t + size_t(pos) * HALF));
+    Vs[size_t(j) * HD + d] = __float2bfloat16_rn(__ldcg(x + KVH * HD + d));
   }
   {
     const int pos = P->pos[m];
@@ -141,7 +155,6 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
       vc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(__ldcg(xv + d));
     }
   }
-  if (nst > 0) tc::mbar_wait(bar, 0);  // staged rows landed (all threads observe the barrier)
   __syncthreads();
   KTL_SUB(0);
 
@@ -160,7 +173,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
 #pragma unroll
       for (int u = 0; u < kDecBatch; ++u) {  // issue every load of the batch first
         const int j = jb + u * NW * KPW + grp;
-        tk[u] = j < nk ? ovr[j] : -2;
+        tk[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tk[u] == -1) {
           const int slot = j < main_len ? mb + j : bbase + (j - main_len);
           const uint4* src = j < ns ? reinterpret_cast<const uint4*>(Ks + size_t(j) * HD + sub * 16)
@@ -242,7 +255,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
 #pragma unroll
       for (int u = 0; u < kDecBatch; ++u) {
         const int j = jb + u * NKG;
-        tv[u] = j < nk ? ovr[j] : -2;
+        tv[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tv[u] == -1) {
           const int slot = j < main_len ? mb + j : bbase + (j - main_len);
           vr[u] = j < ns ? reinterpret_cast<const uint4*>(Vs + size_t(j) * HD)[dc]

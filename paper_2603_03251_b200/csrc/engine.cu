@@ -933,8 +933,11 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
                  (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
-    if (do_attn && E.attn_dec && attn_dec_launch(m, M, P, kc, vc, scale, s, pf.upto(4 * l + 1))) {
-      // one CTA per (kv head, token)
+    if (do_attn && E.attn_dec && size_t(M) * KVH <= size_t(E_num_sms) &&
+        attn_dec_launch(m, M, P, kc, vc, scale, s, pf.upto(4 * l + 1))) {
+      // one CTA per (kv head, token) while they fit one wave (decode, verify,
+      // extend); wider branch steps keep the chunked cluster kernel (measured
+      // faster there: profiles/r01c_summary.md)
     } else if (do_attn && nch <= kAttnClMaxChunks && E.attn_cluster) {
       attn_cl_launch(m, nch, M, P, kc, vc, scale, s, pf.upto(4 * l + 1));
     } else if (do_attn) {
