@@ -24,6 +24,7 @@
 #include "fwd_mk.cuh"
 #include "attn_cl.cuh"
 #include "attn_dec.cuh"
+#include "gemv.cuh"
 #include "tp.cuh"
 #include "kernels.cuh"
 #include "probe.cuh"
@@ -211,6 +212,11 @@ struct Engine {
   int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
   int attn_dec = 1;      // one-CTA-per-(kv head, token) attention (attn_dec.cuh; SSD_B200_ATTN_DEC=0: chunked kernels)
+  // CUDA-core GEMV (gemv.cuh) for forwards of <= this many tokens
+  // (SSD_B200_GEMV_M=1|2). Off: measured slower than the tcgen05 stream-K
+  // kernel at M = 1 (8B step GEMMs 4.02 vs 2.99 ms: register-staged LDG
+  // streaming keeps too few bytes in flight; profiles/r01c_summary.md).
+  int gemv_max_m = 0;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
@@ -634,6 +640,11 @@ static void configure_kernels() {
     SSD_DEC_CFG(1, 128) SSD_DEC_CFG(2, 128) SSD_DEC_CFG(4, 128) SSD_DEC_CFG(8, 128)
 #undef SSD_DEC_CFG
   }
+  for (const void* f : {(const void*)gemv_kernel<EPI_STORE, 1>, (const void*)gemv_kernel<EPI_SWIGLU, 1>,
+                        (const void*)gemv_kernel<EPI_STORE, 2>, (const void*)gemv_kernel<EPI_SWIGLU, 2>}) {
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGemvSmemMax)));
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
+  }
   mk_configure<16, 1>(); mk_configure<16, 2>(); mk_configure<16, 4>(); mk_configure<16, 8>();
   mk_configure<32, 1>(); mk_configure<32, 2>(); mk_configure<32, 4>(); mk_configure<32, 8>();
   mk_configure<64, 1>(); mk_configure<64, 2>(); mk_configure<64, 4>(); mk_configure<64, 8>();
@@ -671,9 +682,28 @@ struct GraphSet {
 // Weight-streaming linear layer: tcgen05 swap-AB stream-K GEMM for every M
 // (M = 1 decode steps pad the token operand to 16).
 template <int EPI>
+static bool gemv_launch(Engine& E, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
+                        cudaStream_t s, Prefetch pf) {
+  if (M > E.gemv_max_m || (W.K & 63)) return false;
+  const int MT = M <= 1 ? 1 : 2;
+  const size_t smem = gemv_smem(MT, W.K);
+  if (smem > kGemvSmemMax) return false;
+  const int groups = std::min(int(((W.N + tc::kBM - 1) / tc::kBM) * (tc::kBM / kGemvRows)), 2 * E_num_sms);
+  if (MT == 1)
+    launch_pdl(gemv_kernel<EPI, 1>, dim3(groups), dim3(kGemvThreads), smem, s, (const bf16*)W.w, W.N, W.K, X, M, Y,
+               ldy, Yb, ldyb, pf);
+  else
+    launch_pdl(gemv_kernel<EPI, 2>, dim3(groups), dim3(kGemvThreads), smem, s, (const bf16*)W.w, W.N, W.K, X, M, Y,
+               ldy, Yb, ldyb, pf);
+  return true;
+}
+
+template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                    cudaStream_t s, Prefetch pf) {
   ++E.launches;
+  // decode steps (M <= gemv_max_m): CUDA-core GEMV, whole rows per CTA
+  if (m.gemm_ctas == 0 && gemv_launch<EPI>(E, W, X, M, Y, ldy, Yb, ldyb, s, pf)) return;
   // small weight matrices at branch widths (17..32 tokens): cluster split-K.
   // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
@@ -1334,6 +1364,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
   if (const char* ast = std::getenv("SSD_B200_ATTN_STAGE")) g_attn_stage = std::atoi(ast) != 0;
+  if (const char* gv = std::getenv("SSD_B200_GEMV_M")) E.gemv_max_m = std::max(0, std::min(2, std::atoi(gv)));
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
