@@ -140,6 +140,12 @@ ssd_status ssd_uniform_fanout(int32_t lookahead, int32_t budget, int32_t role, s
 /* cache::conditional_hit_rate (cache.hpp:79-85, cache.cpp:150-169). */
 double ssd_conditional_hit_rate(const ssd_plan* plan, double acceptance, double exponent);
 
+/* hitmodel::fit_powerlaw (hitmodel.hpp:39-50, hitmodel.cpp:65-106): fit
+ * miss = A F^-r to n measured (fan-out, miss rate) samples by log-log least
+ * squares; the exponent r calibrates ssd_geometric_fanout.
+ * SSD_INSUFFICIENT_DATA with fewer than two distinct fan-outs. */
+ssd_status ssd_fit_powerlaw(const double* fan_out, const double* miss_rate, int32_t n, double* exponent,
+                            double* log_amplitude, double* r_squared);
 /* perf::speedup_batch (perf.hpp:54-59, perf.cpp:44-55): per-sequence
  * speedup of a batch whose rounds stall for the backup when any sequence
  * misses (all-hit probability hit_rate^batch). Times in verify passes. */

@@ -165,6 +165,12 @@ def cases():
         add(f"perf p={p_} Eh={eh} Em={em} tp={tp} tb={tb} b={b}",
             {"op": "perf", "hit_rate": p_, "hit_tokens": eh, "miss_tokens": em, "primary_time": tp, "backup_time": tb,
              "batch": b, "critical": True})
+    # ---- miss-rate power law (hitmodel.cpp:65-106) feeding geometric_fanout's exponent
+    add("fit_powerlaw exact r=0.8", {"op": "fit_powerlaw", "samples": [[f, 0.6 * f ** -0.8] for f in (1, 2, 4, 8, 16)]})
+    add("fit_powerlaw noisy", {"op": "fit_powerlaw", "samples": [[1, 0.58], [2, 0.41], [4, 0.22], [4, 0.25], [8, 0.14],
+                                                                 [16, 0.061]]})
+    add("fit_powerlaw one fan-out (InsufficientData)", {"op": "fit_powerlaw", "samples": [[4, 0.2], [4, 0.3]]})
+    add("fit_powerlaw zero miss rejected", {"op": "fit_powerlaw", "samples": [[1, 0.5], [2, 0.0]]})
     add("perf no crossover", {"op": "perf", "hit_rate": 0.5, "hit_tokens": 1.0, "miss_tokens": 3.0, "primary_time": 0.5,
                               "critical": True})
     add("perf hit rate out of range", {"op": "perf", "hit_rate": 1.5, "hit_tokens": 2.0, "miss_tokens": 1.0,

@@ -187,6 +187,12 @@ json run(const json& req) {
     }
     return o;
   }
+  if (op == "fit_powerlaw") {  // hitmodel.cpp:65-106
+    std::vector<std::pair<double, double>> sm;
+    for (const auto& e : req.at("samples")) sm.emplace_back(e.at(0).get<double>(), e.at(1).get<double>());
+    const PowerLaw f = fit_powerlaw(sm);
+    return json{{"exponent", f.exponent}, {"log_amplitude", f.log_amplitude}, {"r_squared", f.r_squared}};
+  }
   if (op == "perf") {  // perf.cpp:19-73
     const Yields y{req.at("hit_tokens").get<double>(), req.at("miss_tokens").get<double>()};
     const double p = req.at("hit_rate"), tp = req.at("primary_time"), tb = req.value("backup_time", 0.0);

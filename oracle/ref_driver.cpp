@@ -17,6 +17,7 @@
 #include "ssdlab/cache.hpp"
 #include "ssdlab/categorical.hpp"
 #include "ssdlab/errors.hpp"
+#include "ssdlab/hitmodel.hpp"
 #include "ssdlab/perf.hpp"
 #include "ssdlab/lm.hpp"
 #include "ssdlab/rng.hpp"
@@ -115,6 +116,12 @@ json run(const json& req) {
       o["continuous"] = cache::geometric_fanout_continuous(g.at(0), g.at(1), K, g.at(2).get<double>()).fan_out;
     }
     return o;
+  }
+  if (op == "fit_powerlaw") {
+    std::vector<std::pair<double, double>> sm;
+    for (const auto& e : req.at("samples")) sm.emplace_back(e.at(0).get<double>(), e.at(1).get<double>());
+    const hitmodel::PowerLawFit f = hitmodel::fit_powerlaw(sm);
+    return json{{"exponent", f.exponent}, {"log_amplitude", f.log_amplitude}, {"r_squared", f.r_squared}};
   }
   if (op == "perf") {
     const perf::TokenYields y{req.at("hit_tokens").get<double>(), req.at("miss_tokens").get<double>(), 1.0, 0.0};

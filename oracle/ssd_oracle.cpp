@@ -701,6 +701,35 @@ double critical_batch(double p, const Yields& y, double tp) {
   return std::log(arg) / std::log(p);
 }
 
+// hitmodel.cpp:65-106
+PowerLaw fit_powerlaw(const std::vector<std::pair<double, double>>& samples) {
+  std::vector<double> xs;
+  for (const auto& [f, m] : samples) {
+    if (!(f >= 1.0)) throw Error("fit_powerlaw: fan-out values must be >= 1");
+    if (!(m > 0.0) || !(m <= 1.0)) throw Error("fit_powerlaw: miss rates must be in (0, 1]");
+    if (std::find(xs.begin(), xs.end(), f) == xs.end()) xs.push_back(f);
+  }
+  if (xs.size() < 2) throw InsufficientDataError("fit_powerlaw: need at least two distinct fan-out values");
+  const double n = double(samples.size());
+  double mx = 0.0, my = 0.0;
+  for (const auto& [f, m] : samples) { mx += std::log(f); my += std::log(m); }
+  mx /= n;
+  my /= n;
+  double sxx = 0.0, sxy = 0.0, syy = 0.0;
+  for (const auto& [f, m] : samples) {
+    const double dx = std::log(f) - mx, dy = std::log(m) - my;
+    sxx += dx * dx;
+    sxy += dx * dy;
+    syy += dy * dy;
+  }
+  const double slope = sxy / sxx;
+  PowerLaw out;
+  out.exponent = -slope;
+  out.log_amplitude = my - slope * mx;
+  out.r_squared = syy > 0.0 ? 1.0 - (syy - slope * sxy) / syy : 1.0;
+  return out;
+}
+
 // ============================================================== Markov LM
 // lm.cpp:49-63
 MarkovLM::MarkovLM(int V, int order, std::uint64_t seed, std::vector<Row> rows)

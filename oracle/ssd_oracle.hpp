@@ -25,6 +25,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace oracle {
@@ -148,6 +149,10 @@ struct Yields { double hit = 1.0, miss = 1.0; };
 double speedup_ssd(double p, const Yields& y, double tp, double tb);
 double speedup_batch(double p, const Yields& y, double tp, double tb, double batch);
 double critical_batch(double p, const Yields& y, double tp);
+
+// hitmodel.cpp:65-106: log-log least squares of miss = A F^-r.
+struct PowerLaw { double exponent = 0.0, log_amplitude = 0.0, r_squared = 1.0; };
+PowerLaw fit_powerlaw(const std::vector<std::pair<double, double>>& samples);
 
 struct CacheEntry {
   Outcome key;

@@ -64,6 +64,8 @@ SIGNATURES = {
     "ssd_conditional_hit_rate": (C.c_double, [P(Plan), C.c_double, C.c_double]),
     "ssd_speedup_batch": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                     P(C.c_double)]),
+    "ssd_fit_powerlaw": (C.c_int, [P(C.c_double), P(C.c_double), C.c_int32, P(C.c_double), P(C.c_double),
+                                   P(C.c_double)]),
     "ssd_critical_batch": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, P(C.c_double)]),
     "ssd_engine_create": (C.c_int, [P(ModelShape), P(ModelShape), P(PairParams), C.c_int32, C.c_int32, C.c_int32,
                                     P(EngineP)]),

@@ -136,6 +136,17 @@ def speedup_batch(hit_rate: float, hit_tokens: float, miss_tokens: float, primar
     return out.value
 
 
+def fit_powerlaw(samples) -> tuple:
+    """hitmodel::fit_powerlaw (hitmodel.cpp:65-106): (exponent r,
+    log_amplitude, r_squared) of miss = A F^-r over (fan-out, miss) pairs."""
+    f = np.ascontiguousarray([float(a) for a, _ in samples], dtype=np.float64)
+    m = np.ascontiguousarray([float(b) for _, b in samples], dtype=np.float64)
+    r, la, r2 = C.c_double(), C.c_double(), C.c_double()
+    _check(N.load().ssd_fit_powerlaw(f.ctypes.data_as(C.POINTER(C.c_double)), m.ctypes.data_as(C.POINTER(C.c_double)),
+                                     len(f), C.byref(r), C.byref(la), C.byref(r2)))
+    return r.value, la.value, r2.value
+
+
 def critical_batch(hit_rate: float, hit_tokens: float, miss_tokens: float, primary_time: float) -> float:
     """perf::critical_batch (perf.cpp:57-73): the batch size b* where the
     free backup overtakes the JIT re-draft (NoCrossoverError if none)."""

@@ -121,6 +121,42 @@ double ssd_conditional_hit_rate(const ssd_plan* p, double a, double r) {
   return hit_rate(f, a, r);
 }
 
+// hitmodel::fit_powerlaw (hitmodel.cpp:65-106): log-log least squares of the
+// measured miss rate against the fan-out, miss = A F^-r; r is the exponent
+// geometric_fanout takes (calibrated plans).
+ssd_status ssd_fit_powerlaw(const double* fan_out, const double* miss, int32_t n, double* exponent,
+                            double* log_amplitude, double* r_squared) {
+  std::vector<double> xs;
+  for (int i = 0; i < n; ++i) {
+    if (!(fan_out[i] >= 1.0)) { ssd::g_last_error = "fit_powerlaw: fan-out values must be >= 1"; return SSD_ERROR; }
+    if (!(miss[i] > 0.0) || !(miss[i] <= 1.0)) {
+      ssd::g_last_error = "fit_powerlaw: miss rates must be in (0, 1]";
+      return SSD_ERROR;
+    }
+    if (std::find(xs.begin(), xs.end(), fan_out[i]) == xs.end()) xs.push_back(fan_out[i]);
+  }
+  if (xs.size() < 2) {
+    ssd::g_last_error = "fit_powerlaw: need at least two distinct fan-out values";
+    return SSD_INSUFFICIENT_DATA;
+  }
+  double mx = 0.0, my = 0.0;
+  for (int i = 0; i < n; ++i) { mx += std::log(fan_out[i]); my += std::log(miss[i]); }
+  mx /= double(n);
+  my /= double(n);
+  double sxx = 0.0, sxy = 0.0, syy = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double dx = std::log(fan_out[i]) - mx, dy = std::log(miss[i]) - my;
+    sxx += dx * dx;
+    sxy += dx * dy;
+    syy += dy * dy;
+  }
+  const double slope = sxy / sxx;
+  *exponent = -slope;
+  *log_amplitude = my - slope * mx;
+  *r_squared = syy > 0.0 ? 1.0 - (syy - slope * sxy) / syy : 1.0;
+  return SSD_OK;
+}
+
 // Latency model of the loop (perf.cpp:19-55) and the backup crossover b*
 // (perf.cpp:57-73) that drives the Saguaro fallback policy at batch > 1:
 // below b* re-using the primary as a JIT backup wins, at or above it the

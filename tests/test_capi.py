@@ -139,3 +139,23 @@ def test_saguaro_fallback_policy(lib):
     assert P.saguaro_backup(3, p, eh, em, tp) == P.FAST_RANDOM
     assert P.saguaro_backup(8, p, eh, em, tp) == P.FAST_RANDOM
     assert P.saguaro_backup(4, 0.5, 1.0, 3.0, 0.5) in (P.SAME_PRIMARY_JIT, P.FAST_RANDOM)
+
+
+def _fit_cases():
+    with open(os.path.join(ROOT, "tests", "golden", "ref_golden.json")) as f:
+        return [c for c in json.load(f) if c["req"]["op"] == "fit_powerlaw"]
+
+
+@pytest.mark.parametrize("case", _fit_cases(), ids=lambda c: c["name"])
+def test_fit_powerlaw_matches_reference_golden(lib, case):
+    """ssd_fit_powerlaw against the compiled reference's hitmodel.cpp:65-106."""
+    import paper_2603_03251_b200 as P
+    out = case["out"]
+    if "error" in out:
+        with pytest.raises(P.InsufficientDataError if out["code"] == 7 else P.Error):
+            P.fit_powerlaw(case["req"]["samples"])
+        return
+    r, la, r2 = P.fit_powerlaw(case["req"]["samples"])
+    assert r == pytest.approx(out["exponent"], rel=1e-13, abs=1e-15)
+    assert la == pytest.approx(out["log_amplitude"], rel=1e-13, abs=1e-15)
+    assert r2 == pytest.approx(out["r_squared"], rel=1e-13, abs=1e-15)
