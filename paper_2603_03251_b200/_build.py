@@ -11,8 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libssd_b200.so")
 SOURCES = ["engine.cu", "plans.cpp"]
-DEPS = SOURCES + ["common.cuh", "kernels.cuh", "gemm_tc.cuh", "rowops.cuh", "probe.cuh", "split.cuh", "tp.cuh",
-                  "attn_cl.cuh", "fwd_mk.cuh", "gemm_cl.cuh"]
+# every header under csrc/ (a missing entry once left a stale library in place)
+DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]

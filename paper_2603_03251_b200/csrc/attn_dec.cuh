@@ -81,11 +81,18 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   const bf16* kb = kc + size_t(kvh) * S * HD;
   const bf16* vb = vc + size_t(kvh) * S * HD;
   const int ns = min(nst, main_len);  // main keys [0, ns) served from shared memory
+  // Stage main rows [0, ns) into shared memory with two bulk copies (rows of
+  // THIS forward's tokens among them are stale and patched after the wait).
+  // The mbarrier is initialised, and the initialisation made visible to every
+  // thread by the CTA barrier, before anyone can wait on it (a wait issued
+  // before that barrier faulted: scripts/ssd_stress.py, compute-sanitizer).
+  if (tid == 0 && nst > 0) {
+    tc::mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   if (tid == 0) {
     if (nst > 0) {
-      tc::mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      // rows of THIS forward's tokens among them are stale; ovr[] replaces them
       const uint32_t sbytes = uint32_t(ns) * HD * 2;
       tc::mbar_expect_tx(bar, 2 * sbytes);
       if (sbytes) {
