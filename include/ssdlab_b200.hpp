@@ -133,6 +133,29 @@ inline FanOutPlan uniform_fanout(int lookahead, int budget, Origin role = Origin
   return FanOutPlan::from_c(p);
 }
 
+// ------------------------------------------------- hitmodel.hpp:39-53, perf.hpp:54-72
+struct PowerLawFit {
+  double exponent = 0.0, log_amplitude = 0.0, r_squared = 1.0;
+};
+inline PowerLawFit fit_powerlaw(std::span<const std::pair<double, double>> samples) {
+  std::vector<double> f, m;
+  for (const auto& [a, b] : samples) { f.push_back(a); m.push_back(b); }
+  PowerLawFit out;
+  check(ssd_fit_powerlaw(f.data(), m.data(), int(f.size()), &out.exponent, &out.log_amplitude, &out.r_squared));
+  return out;
+}
+inline double speedup_batch(double hit_rate, double hit_tokens, double miss_tokens, double primary_time,
+                            double backup_time, double batch) {
+  double out = 0.0;
+  check(ssd_speedup_batch(hit_rate, hit_tokens, miss_tokens, primary_time, backup_time, batch, &out));
+  return out;
+}
+inline double critical_batch(double hit_rate, double hit_tokens, double miss_tokens, double primary_time) {
+  double out = 0.0;
+  check(ssd_critical_batch(hit_rate, hit_tokens, miss_tokens, primary_time, &out));
+  return out;
+}
+
 // ---------------------------------------------------------- specdec.hpp:22-52
 struct Speculation {
   std::vector<int> tokens;
@@ -176,6 +199,7 @@ struct SimConfig {
   long rounds = 1000;
   std::uint64_t seed = 0;
   double accept_scale = 1.0;
+  int batch_size = 1;  // sim.hpp:40 (run_ssd only: whole-batch stall semantics)
   ssd_sim_config c() const {
     ssd_sim_config s{};
     s.lookahead = lookahead;
@@ -195,7 +219,8 @@ struct SimConfig {
 
 struct RunResult {
   ssd_run_stats stats{};
-  std::vector<int> tokens;
+  std::vector<int> tokens;                     // sequence 0
+  std::vector<std::vector<int>> streams;       // run_ssd: one per batch sequence
   std::vector<VerificationOutcome> outcomes;  // run_ssd only
   std::vector<int> hits;                      // run_ssd only (-1 on the last round)
   double hit_rate() const {
@@ -208,9 +233,12 @@ struct RunResult {
 class Engine {
  public:
   Engine(const ssd_model_shape& target, const ssd_model_shape& draft, const ssd_pair_params& pair, int device = 0,
-         int max_branches = 64, int max_lookahead = 8) {
+         int max_branches = 64, int max_lookahead = 8, int max_batch = 1) {
     ssd_engine* e = nullptr;
-    check(ssd_engine_create(&target, &draft, &pair, device, max_branches, max_lookahead, &e));
+    if (max_batch > 1)
+      check(ssd_engine_create_batch(&target, &draft, &pair, device, max_batch, max_branches, max_lookahead, &e));
+    else
+      check(ssd_engine_create(&target, &draft, &pair, device, max_branches, max_lookahead, &e));
     h_.reset(e);
     vocab_ = target.vocab;
   }
@@ -295,18 +323,21 @@ class Engine {
     return r;
   }
 
-  // sim::run_protocol_harness (sim.cpp:502-601)
+  // sim::run_protocol_harness (sim.cpp:502-601), cfg.batch_size sequences
   RunResult run_ssd(std::span<const int> prompt, const SimConfig& cfg) const {
     RunResult r;
     const long cap = cfg.rounds * (cfg.lookahead + 1);
-    r.tokens.resize(size_t(cap));
+    const int b = cfg.batch_size;
+    std::vector<int> all(size_t(cap) * size_t(b > 0 ? b : 1));
+    std::vector<int64_t> lens(size_t(b > 0 ? b : 1));
     std::vector<int> oc(size_t(2 * cfg.rounds));
     r.hits.resize(size_t(cfg.rounds));
     const ssd_sim_config c = cfg.c();
-    int64_t n = 0;
-    check(ssd_run_ssd(h_.get(), prompt.data(), int(prompt.size()), &c, r.tokens.data(), cap, &n, oc.data(),
-                      r.hits.data(), &r.stats));
-    r.tokens.resize(size_t(n));
+    check(ssd_run_ssd_batch(h_.get(), prompt.data(), int(prompt.size()), &c, b, all.data(), cap, lens.data(),
+                            oc.data(), r.hits.data(), &r.stats));
+    for (int j = 0; j < b; ++j)
+      r.streams.emplace_back(all.begin() + long(j) * cap, all.begin() + long(j) * cap + lens[size_t(j)]);
+    r.tokens = r.streams[0];
     for (long i = 0; i < cfg.rounds; ++i) r.outcomes.push_back({oc[size_t(2 * i)], oc[size_t(2 * i + 1)]});
     return r;
   }
