@@ -380,7 +380,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # pair divergence knob calibrated on this workload to alpha ~ 0.8 (
     # scripts/bench_alpha.py, profiles/r01_summary.md); alpha is reported
-    ap.add_argument("--block-out-scale", type=float, default=0.07)
+    ap.add_argument("--block-out-scale", type=float, default=0.06)
     ap.add_argument("--tp", type=int, default=1, help="N>1 split mode: tensor-parallel verifier ranks")
     ap.add_argument("--multi", default="split", choices=["split", "replicas"],
                     help="N>1: split verifier/speculator processes (default) or independent replicas")

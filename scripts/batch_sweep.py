@@ -25,7 +25,7 @@ K, F = 4, 4
 B = F * (K + 1)
 BATCHES = (1, 2, 4, 8)
 ts, ds = shapes("llama8b_1b", max_ctx=1024)
-eng = P.Engine(ts, ds, P.Pair(block_out_scale=0.07), max_branches=B, max_lookahead=K, max_batch=max(BATCHES))
+eng = P.Engine(ts, ds, P.Pair(block_out_scale=0.06), max_branches=B, max_lookahead=K, max_batch=max(BATCHES))
 prompt = np.random.default_rng(20250809).integers(0, ts.vocab, 128).tolist()
 
 

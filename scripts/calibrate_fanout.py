@@ -26,7 +26,7 @@ R = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 NP = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 K, BUDGET = 4, 20
 ts, ds = shapes("llama8b_1b", max_ctx=1024)
-eng = P.Engine(ts, ds, P.Pair(block_out_scale=0.07), max_branches=2 * BUDGET, max_lookahead=K)
+eng = P.Engine(ts, ds, P.Pair(block_out_scale=0.06), max_branches=2 * BUDGET, max_lookahead=K)
 prompts = [np.random.default_rng(20250809 + i).integers(0, ts.vocab, 128).tolist() for i in range(NP)]
 
 
