@@ -177,6 +177,8 @@ def run_split(args):
     # NCCL needs one GPU per rank; fewer GPUs than ranks (a functional run of
     # the split protocol on one GPU) falls back to gloo for the plumbing
     backend = "nccl" if ndev >= ws else "gloo"
+    if ndev < ws:  # ranks time-share a GPU: no cluster split-K GEMM (shared GPUs)
+        os.environ.setdefault("SSD_B200_CL_GEMM_MB", "0")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     else:
