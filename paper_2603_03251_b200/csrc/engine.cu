@@ -180,6 +180,14 @@ struct Engine {
   int nbmax = 1;            // batch lanes (run_protocol_harness batch_size)
   int hist_stride = 0;      // history capacity of one lane
   int* d_lanes = nullptr;   // device list of the lanes a batched draft serves
+  // Round graphs of the last run_ssd call, reused while every baked-in
+  // parameter is unchanged (ssd_graph_key): capturing two graphs of ~600
+  // kernels each is host work paid per call otherwise.
+  std::string ssd_graph_key;
+  std::vector<cudaGraphExec_t> ssd_graphs;
+  long long ssd_graph_launches = 0;  // kernels per round of the cached graphs
+  int* ssd_log = nullptr;            // [2 * cap] outcomes + [cap] hits (baked into the graphs)
+  int64_t ssd_log_cap = 0;
   int V = 0;
   cudaStream_t sv = nullptr, ss = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_verified = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
@@ -289,6 +297,10 @@ static ssd_model_shape tp_local(const ssd_model_shape& s, int tp) {
 // tp_rank (column-parallel QKV / gate-up, row-parallel O / down,
 // vocabulary-parallel head, replicated embedding), generated as the exact
 // blocks of the unsharded synthetic tensors.
+// Forward capacity floor: prompts up to this length prefill in ONE forward
+// (one weight pass per model; the bench's 128-token prompt).
+constexpr int kPrefillChunk = 128;
+
 static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_shape& dr, const ssd_pair_params& pp,
                         int role, int branch_slots, int maxM, int tp_rank = 0, int tp_size = 1, int lanes = 1) {
   const ssd_model_shape s = tp_local(sfull, tp_size);
@@ -1379,10 +1391,10 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (maxM > kMaxM) throw Fail(SSD_TOO_LARGE, "engine: batch x branches above the forward capacity");
   // a split process materialises only its own model
   if (role != SSD_ROLE_SPECULATOR)
-    build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, 64), tp_rank, tp_size, nb);
+    build_model(E.T, *target, *draft, *pair, 0, 0, std::max(maxM, kPrefillChunk), tp_rank, tp_size, nb);
   else E.T.s = *target;
   if (role != SSD_ROLE_VERIFIER)
-    build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, 64), 0, 1, nb);
+    build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, kPrefillChunk), 0, 1, nb);
   else E.D.s = *draft;
   for (const ssd_model_shape* s : {target, draft})
     if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
@@ -1492,6 +1504,9 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   if (E.tp_region) cudaFree(E.tp_region);
   if (E.inbox) cudaFree(E.inbox);
   if (E.peers_dev) cudaFree(E.peers_dev);
+  for (auto g : E.ssd_graphs)
+    if (g) cudaGraphExecDestroy(g);
+  if (E.ssd_log) cudaFree(E.ssd_log);
   for (void* p : E.owned) cudaFree(p);
   cudaStreamDestroy(E.sv);
   cudaStreamDestroy(E.ss);
@@ -1616,12 +1631,15 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   if (nb * B > E.D.maxM || nb * (K + 1) > E.T.maxM) throw Fail(SSD_TOO_LARGE, "sim: batch x branches exceeds capacity");
   set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2), nb);
   const int64_t R = c->rounds;
-  struct DevBuf {
-    int* p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
-  } d_out, d_hit;
-  d_out.p = dalloc<int>(size_t(2 * R));
-  d_hit.p = dalloc<int>(size_t(R));
+  if (R > E.ssd_log_cap) {  // per-round logs (their address is baked into the graphs)
+    if (E.ssd_log) cudaFree(E.ssd_log);
+    E.ssd_log = nullptr;
+    E.ssd_log_cap = 0;
+    E.ssd_log = dalloc<int>(size_t(3 * R));
+    E.ssd_log_cap = R;
+  }
+  int* const d_out = E.ssd_log;
+  int* const d_hit = E.ssd_log + 2 * E.ssd_log_cap;
   cudaStream_t sv = E.sv, ss = E.ss;
   for (int l = 0; l < nb; ++l) {
     reset_state(E, K, n0, R, derive_seed(c->seed, uint64_t(l)), derive_seed(derive_seed(c->seed, 0x5EED), uint64_t(l)),
@@ -1646,7 +1664,6 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   // from the verifier stream and join at the lookup. Two graphs alternate the
   // branch-row buffers (the next round's verifier reads this round's rows).
   E.launches = 0;
-  GraphSet gs;
   // verifier and speculator GEMMs on disjoint SM sets so both streams run at once
   E.T.gemm_ctas = E.split_t;
   E.D.gemm_ctas = E.split_d;
@@ -1654,6 +1671,20 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
     Engine& e;
     ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; }
   } uncap{E};
+  // every value the capture bakes into kernel parameters or launch shapes
+  char keybuf[512];
+  std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p",
+                K, B, max_f, nb, c->scheme.kind, c->scheme.fan_out, c->scheme.temperature, c->scheme.downweight,
+                c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
+                c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
+                static_cast<void*>(E.ssd_log));
+  const std::string key(keybuf);
+  if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
+    for (auto g : E.ssd_graphs)
+      if (g) cudaGraphExecDestroy(g);
+    E.ssd_graphs.clear();
+    E.ssd_graph_key.clear();
+    GraphSet gs;
   for (int parity = 0; parity < 2; ++parity) {
     gs.g.push_back(capture_graph(sv, [&] {
       CK(cudaEventRecord(E.ev_fork, sv));
@@ -1663,19 +1694,25 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
       CK(cudaEventRecord(E.ev_verified, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
       lookup_kernel<<<1, 32, 0, ss>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V, E.cum,
-                                      d_out.p, d_hit.p);
+                                      d_out, d_hit);
       KCHECK();
       ++E.launches;
       CK(cudaEventRecord(E.ev_join, ss));
       CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
     }));
   }
-  const long long per_round = E.launches / 2;
+    E.ssd_graphs = gs.g;
+    gs.g.clear();
+    E.ssd_graph_key = key;
+    E.ssd_graph_launches = E.launches / 2;
+  }
+  const long long per_round = E.ssd_graph_launches;
+  E.launches = 0;
   long long jit_launches = 0;
   std::vector<int> hits(static_cast<size_t>(nb));
   CK(cudaEventRecord(E.ev_t0, sv));
   for (int64_t r = 0; r < R; ++r) {
-    CK(cudaGraphLaunch(gs.g[size_t(r & 1)], sv));
+    CK(cudaGraphLaunch(E.ssd_graphs[size_t(r & 1)], sv));
     if (jit && r + 1 < R) {
       // SamePrimaryJIT: the lanes that missed re-draft from their new
       // history, batched (the one host round trip of the JIT backup)
@@ -1700,8 +1737,8 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
   std::vector<LoopState> sts;
   for (int l = 0; l < nb; ++l) sts.push_back(read_state(E, l));
-  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out.p, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
-  if (out_hits) CK(cudaMemcpy(out_hits, d_hit.p, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
+  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
   const LoopState st = sum_lanes(sts);
   raise_device_error(st);
   fill_stats(st, R, ms, E.launches, stats);
