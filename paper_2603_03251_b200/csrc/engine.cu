@@ -220,6 +220,10 @@ struct Engine {
   int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
   int attn_dec = 1;      // one-CTA-per-(kv head, token) attention (attn_dec.cuh; SSD_B200_ATTN_DEC=0: chunked kernels)
+  // ... and for forwards of >= this many tokens (prefill chunks): the chunked
+  // kernels append every token in every chunk CTA (quadratic in M); measured
+  // 8B M=128 forward 24.9 -> 14.9 ms (SSD_B200_ATTN_DEC_WIDE_M)
+  int attn_dec_wide_m = 48;
   // CUDA-core GEMV (gemv.cuh) for forwards of <= this many tokens
   // (SSD_B200_GEMV_M=1|2). Off: measured slower than the tcgen05 stream-K
   // kernel at M = 1 (8B step GEMMs 4.02 vs 2.99 ms: register-staged LDG
@@ -975,7 +979,7 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
       launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
                  (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
     linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
-    if (do_attn && E.attn_dec && size_t(M) * KVH <= size_t(E_num_sms) &&
+    if (do_attn && E.attn_dec && (size_t(M) * KVH <= size_t(E_num_sms) || M >= E.attn_dec_wide_m) &&
         attn_dec_launch(m, M, P, kc, vc, scale, s, pf.upto(4 * l + 1))) {
       // one CTA per (kv head, token) while they fit one wave (decode, verify,
       // extend); wider branch steps keep the chunked cluster kernel (measured
@@ -1376,6 +1380,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
   if (const char* ast = std::getenv("SSD_B200_ATTN_STAGE")) g_attn_stage = std::atoi(ast) != 0;
+  if (const char* aw = std::getenv("SSD_B200_ATTN_DEC_WIDE_M")) E.attn_dec_wide_m = std::max(1, std::atoi(aw));
   if (const char* gv = std::getenv("SSD_B200_GEMV_M")) E.gemv_max_m = std::max(0, std::min(2, std::atoi(gv)));
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
