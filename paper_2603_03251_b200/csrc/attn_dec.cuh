@@ -41,6 +41,29 @@ __device__ __forceinline__ float rope_elem(const float* x, int d, int half, cons
 
 __host__ __device__ constexpr int dec_nkg(int HD) { return kDecThreads / (HD / 8); }
 
+// RoPE + KV append of every token of a wide forward (prefill chunks), one
+// CTA per (token, kv head), with the writer rounding of attention_dec; the
+// attention that follows (appended = 1) then reads every key from the cache
+// instead of recomputing this forward's keys per query (quadratic in M).
+__global__ void __launch_bounds__(128) rope_append_kernel(const float* __restrict__ qkv,
+                                                          const FwdParams* __restrict__ P, const float* __restrict__ cos_t,
+                                                          const float* __restrict__ sin_t, bf16* __restrict__ kc,
+                                                          bf16* __restrict__ vc, int S, int H, int KVH, int HD) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int m = blockIdx.x, kvh = blockIdx.y, half = HD >> 1;
+  const size_t row_len = size_t(H + 2 * KVH) * HD;
+  const int pos = P->pos[m], slot = P->slot[m];
+  const float* c = cos_t + size_t(pos) * half;
+  const float* s = sin_t + size_t(pos) * half;
+  const float* xk = qkv + size_t(m) * row_len + size_t(H + kvh) * HD;
+  const float* xv = qkv + size_t(m) * row_len + size_t(H + KVH + kvh) * HD;
+  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+    kc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(rope_elem(xk, d, half, c, s));
+    vc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(__ldcg(xv + d));
+  }
+}
+
 // Shared memory: [qs][sc][red][stat][ovr] then (16-byte aligned) the staged
 // K and V rows ([nst][HD] bf16 each) and one mbarrier.
 __host__ __device__ constexpr size_t attn_dec_base(int G, int HD, int kcap) {
@@ -55,7 +78,7 @@ template <int G, int HD, int MINB>
 __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
     const float* __restrict__ qkv, const FwdParams* __restrict__ P, int M, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, bf16* __restrict__ kc, bf16* __restrict__ vc, int S, int H, int KVH, float scale,
-    bf16* __restrict__ out, int kcap, int nst, Prefetch pf) {
+    bf16* __restrict__ out, int kcap, int nst, int appended, Prefetch pf) {
   constexpr int NW = kDecThreads / 32;
   constexpr int LPK = HD / 16;   // lanes per key
   constexpr int KPW = 32 / LPK;  // keys per warp pass
@@ -125,7 +148,9 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   for (int j = tid; j < nk; j += kDecThreads) ovr[j] = -1;
   if (nst > 0) tc::mbar_wait(bar, 0);  // staged rows landed before they are patched below
   __syncthreads();
-  for (int t = tid; t < M; t += kDecThreads) {
+  // appended: rope_append_kernel wrote this forward's rows before this
+  // launch (wide forwards), so every key is read from the cache
+  for (int t = tid; t < M && !appended; t += kDecThreads) {
     const int j = visible_key(P->slot[t], mb, main_len, bbase, blen);
     if (j >= 0) ovr[j] = t;
   }
@@ -157,7 +182,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
     const float* xk = qkv + size_t(m) * row_len + size_t(H + kvh) * HD;
     const float* xv = qkv + size_t(m) * row_len + size_t(H + KVH + kvh) * HD;
     const int slot = P->slot[m];
-    for (int d = tid; d < HD; d += kDecThreads) {
+    for (int d = tid; d < HD && !appended; d += kDecThreads) {
       kc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(rope_elem(xk, d, HALF, c, s));
       vc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(__ldcg(xv + d));
     }

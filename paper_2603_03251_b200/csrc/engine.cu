@@ -627,6 +627,7 @@ static void configure_kernels() {
   carveout_max(sample_rows_kernel);
   carveout_max(gen_layer_kernel);
   carveout_max(gen_table_kernel);
+  carveout_max(rope_append_kernel);
   configure_gemm<EPI_STORE, 16>(); configure_gemm<EPI_SWIGLU, 16>();
   configure_gemm<EPI_STORE, 32>(); configure_gemm<EPI_SWIGLU, 32>();
   configure_gemm<EPI_STORE, 48>(); configure_gemm<EPI_SWIGLU, 48>();
@@ -836,7 +837,7 @@ static void attn_cl_launch(Model& m, int nch, int M, const FwdParams* P, bf16* k
 // do not fit shared memory): the caller then uses the chunked kernels.
 template <int G, int HD, int MINB>
 static void attn_dec_launch_g(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap, int nst,
-                              cudaStream_t s, Prefetch pf) {
+                              int appended, cudaStream_t s, Prefetch pf) {
   const ssd_model_shape& sh = m.s;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sh.n_kv_heads, M);
@@ -849,7 +850,8 @@ static void attn_dec_launch_g(Model& m, int M, const FwdParams* P, bf16* kc, bf1
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, attention_dec_kernel<G, HD, MINB>, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
-                        (const float*)m.rope_sin, kc, vc, m.S, sh.n_heads, sh.n_kv_heads, scale, m.attn, kcap, nst, pf));
+                        (const float*)m.rope_sin, kc, vc, m.S, sh.n_heads, sh.n_kv_heads, scale, m.attn, kcap, nst,
+                        appended, pf));
 }
 
 static int g_attn_stage = 1;  // SSD_B200_ATTN_STAGE=0: never stage KV rows in shared memory
@@ -858,13 +860,20 @@ template <int G, int HD>
 static void attn_dec_pick(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap,
                           cudaStream_t s, Prefetch pf) {
   constexpr size_t kSmemMax = 227 * 1024;
+  if (size_t(M) * m.s.n_kv_heads > size_t(2 * E_num_sms)) {
+    // wide forward (prefill chunk): append every row first, then attend from the cache
+    launch_pdl(rope_append_kernel, dim3(M, m.s.n_kv_heads), dim3(128), 0, s, (const float*)m.qkv, P,
+               (const float*)m.rope_cos, (const float*)m.rope_sin, kc, vc, m.S, m.s.n_heads, m.s.n_kv_heads, HD);
+    attn_dec_launch_g<G, HD, 2>(m, M, P, kc, vc, scale, kcap, 0, 1, s, pf);
+    return;
+  }
   if (size_t(M) * m.s.n_kv_heads <= size_t(E_num_sms) && g_attn_stage) {
     // one CTA per SM: stage as many main KV rows as shared memory holds
     const size_t room = kSmemMax - attn_dec_smem(G, HD, kcap, 0);
     const int nst = int(std::min<size_t>(size_t(kcap), room / (size_t(4) * HD)));
-    attn_dec_launch_g<G, HD, 1>(m, M, P, kc, vc, scale, kcap, nst, s, pf);
+    attn_dec_launch_g<G, HD, 1>(m, M, P, kc, vc, scale, kcap, nst, 0, s, pf);
   } else {
-    attn_dec_launch_g<G, HD, 2>(m, M, P, kc, vc, scale, kcap, 0, s, pf);  // two CTAs per SM, rows from L2
+    attn_dec_launch_g<G, HD, 2>(m, M, P, kc, vc, scale, kcap, 0, 0, s, pf);  // two CTAs per SM, rows from L2
   }
 }
 
