@@ -244,6 +244,25 @@ def run_split(args):
     dist.destroy_process_group()
 
 
+def path_roofline(tw, dw, K, hbm_gbs, ssd_tokens_per_round, sd_tokens_per_round, ssd_tps, ar_tps, sd_tps):
+    """tokens/s each loop would reach if every forward streamed
+    its weights at the measured HBM bandwidth (bytes per round / bandwidth,
+    times the measured tokens per round), and the achieved fraction. One GPU
+    (colocated): an SSD round streams the target once (verify) and the draft
+    K + 1 times (extend + K branch steps); SD streams the draft K times and
+    the target once; AR the target once per token."""
+    bw = hbm_gbs * 1e9
+    ssd_s = (tw + (K + 1) * dw) / bw
+    sd_s = (tw + K * dw) / bw
+    ar_s = tw / bw
+    out = {"ssd_round_bytes": tw + (K + 1) * dw, "ssd_tokens_per_s": ssd_tokens_per_round / ssd_s,
+           "sd_tokens_per_s": sd_tokens_per_round / sd_s, "ar_tokens_per_s": 1.0 / ar_s}
+    out["ssd_frac"] = ssd_tps / out["ssd_tokens_per_s"]
+    out["sd_frac"] = sd_tps / out["sd_tokens_per_s"]
+    out["ar_frac"] = ar_tps / out["ar_tokens_per_s"]
+    return out
+
+
 def alpha_of(mean_accepted: float, K: int) -> float:
     """Per-token acceptance alpha from the mean accepted length
     (E[accepted] = sum_{i=1..K} alpha^i)."""
@@ -349,7 +368,10 @@ def run_ours(args):
                          "draft_branch_step_ms": prof_b["ms_forward"],
                          "draft_branch_gemm_gbs": prof_b["gemm_bytes"] / (prof_b["ms_gemm"] * 1e-3) / 1e9},
             "model_bytes": {"target_step": tw, "draft_step": dw},
+            "path_roofline": path_roofline(tw, dw, cfg.lookahead, hbm, tokens / sum(r.rounds for r in runs),
+                                           sd.accepted_sum / max(1, sd.rounds) + 1.0, ssd_tps, ar_tps, sd_tps),
             "clocks": clk.summary()}
+    line["roofline"]["frac_of_8tbs_spec"] = achieved / 8000.0
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         s = cpu_sample(args, os.cpu_count() or 1, rounds=1)
         line["cpu_baseline"] = {"value": s["tokens"] / s["seconds"], "unit": "tokens/s", "cores": os.cpu_count(),
