@@ -124,3 +124,21 @@ def test_batch_capacity_errors(tiny_batch):
         eng.run_ssd(_prompt(8), _cfg(P, 4, 4, 1, 0.0, [4] * 5, [4] * 5, "fast_random", 5, 0.0))
     with pytest.raises(P.Error):
         eng.run_ssd(_prompt(8), _cfg(P, 4, 4, 1, 0.0, [4] * 5, [4] * 5, "fast_random", 0, 0.0))
+
+
+def test_round_graph_cache_invalidation(tiny_batch):
+    """run_ssd reuses its captured round graphs while every baked-in parameter
+    matches; interleaving configurations (lookahead, plans, batch, scheme,
+    rounds) on one engine must give exactly the results of the first run of
+    each configuration."""
+    P, eng, orc = tiny_batch
+    prompt = _prompt(12, seed=31)
+    a = _cfg(P, 4, 6, 3, 0.0, [4] * 5, [4] * 5, "fast_random", 1, 0.0)
+    b = _cfg(P, 3, 9, 3, 0.0, [2, 2, 2, 2], [2, 2, 2, 2], "fast_random", 2, 0.5)
+    c = _cfg(P, 4, 6, 3, 1.0, [3] * 5, [3] * 5, "fast_random", 1, 0.0)
+    first = {k: eng.run_ssd(prompt, cfg) for k, cfg in (("a", a), ("b", b), ("c", c))}
+    for k, cfg in (("c", c), ("a", a), ("b", b), ("a", a)):
+        r = eng.run_ssd(prompt, cfg)
+        assert r.streams == first[k].streams, k
+        assert r.outcomes.tolist() == first[k].outcomes.tolist(), k
+        assert abs(r.virtual_time - first[k].virtual_time) < 1e-12, k
