@@ -211,7 +211,9 @@ struct Engine {
   std::vector<void*> owned;
   long long launches = 0;
   int skip_mask = 0;  // profiling only (SSD_B200_SKIP): drop norms / attention
-  long long pf_ahead = 32LL << 20;  // L2 prefetch look-ahead of the weight stream (SSD_B200_PF_MB)
+  // L2 prefetch look-ahead of the weight stream (SSD_B200_PF_MB). 16 MB:
+  // colocated SSD round 9.53 -> 9.41 ms vs 32 MB (scripts/split_sms_sweep.py)
+  long long pf_ahead = 16LL << 20;
   // Persistent forward kernel (fwd_mk.cuh) for M <= 64: SSD_B200_MK=1. Off by
   // default: measured slower than the per-op PDL chain (profiles/r01_summary.md:
   // tcgen05 at N <= 32 consumes a 32 KB unit per ~0.77 us per SM, i.e. no faster
@@ -220,10 +222,11 @@ struct Engine {
   int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
   int attn_dec = 1;      // one-CTA-per-(kv head, token) attention (attn_dec.cuh; SSD_B200_ATTN_DEC=0: chunked kernels)
-  // ... and for forwards of >= this many tokens (prefill chunks): the chunked
-  // kernels append every token in every chunk CTA (quadratic in M); measured
-  // 8B M=128 forward 24.9 -> 14.9 ms (SSD_B200_ATTN_DEC_WIDE_M)
-  int attn_dec_wide_m = 48;
+  // ... and for forwards of >= this many tokens: the branch steps (M = 20:
+  // colocated SSD round 9.71 -> 9.53 ms) and prefill chunks (the chunked
+  // kernels append every token in every chunk CTA, quadratic in M: 8B M=128
+  // forward 24.9 -> 12.3 ms) (SSD_B200_ATTN_DEC_WIDE_M)
+  int attn_dec_wide_m = 20;
   // CUDA-core GEMV (gemv.cuh) for forwards of <= this many tokens
   // (SSD_B200_GEMV_M=1|2). Off: measured slower than the tcgen05 stream-K
   // kernel at M = 1 (8B step GEMMs 4.02 vs 2.99 ms: register-staged LDG

@@ -1,6 +1,7 @@
-"""Colocated SSD round time (bench workload) under SSD_B200_SPLIT_SMS settings
-(GEMM CTAs of the verifier, speculator): one process per setting is launched
-by the caller; prints ms per round (median of 3 runs after one warm run)."""
+"""Colocated SSD round time (bench workload) under the current SSD_B200_*
+knobs (e.g. SSD_B200_SPLIT_SMS = GEMM CTAs of the verifier, speculator): one
+process per setting is launched by the caller; prints ms per round (median of
+3 runs after one warm run)."""
 import json
 import os
 import statistics
@@ -23,5 +24,5 @@ cfg = P.SimConfig(lookahead=K, scheme=P.SamplingScheme.greedy(), primary_plan=P.
                   backup_kind=P.FAST_RANDOM, rounds=32, seed=20250809)
 eng.run_ssd(prompt, cfg)
 ms = [eng.run_ssd(prompt, cfg).device_ms / 32 for _ in range(3)]
-print(json.dumps({"split_sms": os.environ.get("SSD_B200_SPLIT_SMS", "0,0"), "spec_prio": os.environ.get("SSD_B200_SPEC_PRIO", "0"),
-                  "ms_per_round": round(statistics.median(ms), 3)}), flush=True)
+env = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("SSD_B200_")) or "default"
+print(json.dumps({"env": env, "ms_per_round": round(statistics.median(ms), 3)}), flush=True)

@@ -39,8 +39,9 @@ def _logits(env, cfg="tiny", n=40, steps=None):
 
 @pytest.mark.parametrize("n", [1, 40, 300])
 def test_cluster_attention_bit_identical_to_global_merge(n):
-    a = _logits({"SSD_B200_ATTN_CL": "0"}, n=n, steps=6)
-    b = _logits({"SSD_B200_ATTN_CL": "1"}, n=n, steps=6)
+    # the chunked kernels only (attention_dec is the default for most widths)
+    a = _logits({"SSD_B200_ATTN_CL": "0", "SSD_B200_ATTN_DEC": "0"}, n=n, steps=6)
+    b = _logits({"SSD_B200_ATTN_CL": "1", "SSD_B200_ATTN_DEC": "0"}, n=n, steps=6)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert a[2] == b[2]
 
