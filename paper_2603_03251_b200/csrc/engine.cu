@@ -234,6 +234,13 @@ struct Engine {
   int gemv_max_m = 0;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
+  // ... inside the colocated SSD round, where the verifier and speculator
+  // streams run at once: the 108 KB co-resident GEMM config lets their CTAs
+  // share SMs. Measured (scripts/split_sms_sweep.py): round 9.41 -> 9.13 ms
+  // for all GEMMs, while single-stream forwards (AR, SD) are faster with the
+  // full config (8B step 3.62 vs 3.73 ms), so it applies to that loop only
+  // (SSD_B200_CORUN_SMALL_GEMM_MB).
+  long long corun_small_gemm_bytes = 2000LL << 20;
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
@@ -1396,6 +1403,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* gv = std::getenv("SSD_B200_GEMV_M")) E.gemv_max_m = std::max(0, std::min(2, std::atoi(gv)));
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
+  if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
   {
@@ -1684,17 +1692,20 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   // verifier and speculator GEMMs on disjoint SM sets so both streams run at once
   E.T.gemm_ctas = E.split_t;
   E.D.gemm_ctas = E.split_d;
+  const long long small_saved = E.small_gemm_bytes;
+  E.small_gemm_bytes = std::max(E.small_gemm_bytes, E.corun_small_gemm_bytes);  // co-running streams
   struct Uncap {
     Engine& e;
-    ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; }
-  } uncap{E};
+    long long small;
+    ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; e.small_gemm_bytes = small; }
+  } uncap{E, small_saved};
   // every value the capture bakes into kernel parameters or launch shapes
   char keybuf[512];
-  std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p",
+  std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p %lld",
                 K, B, max_f, nb, c->scheme.kind, c->scheme.fan_out, c->scheme.temperature, c->scheme.downweight,
                 c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
-                static_cast<void*>(E.ssd_log));
+                static_cast<void*>(E.ssd_log), E.small_gemm_bytes);
   const std::string key(keybuf);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
@@ -1725,6 +1736,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   }
   const long long per_round = E.ssd_graph_launches;
   E.launches = 0;
+  E.small_gemm_bytes = small_saved;  // JIT re-drafts below run alone on one stream
   long long jit_launches = 0;
   std::vector<int> hits(static_cast<size_t>(nb));
   CK(cudaEventRecord(E.ev_t0, sv));
