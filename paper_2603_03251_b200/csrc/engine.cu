@@ -241,6 +241,10 @@ struct Engine {
   // full config (8B step 3.62 vs 3.73 ms), so it applies to that loop only
   // (SSD_B200_CORUN_SMALL_GEMM_MB).
   long long corun_small_gemm_bytes = 2000LL << 20;
+  // SSD_B200_CL_SMALL=1: the cluster GEMMs also take a co-resident (116 KB,
+  // 2-stage) budget inside the co-running round. Off: measured slower
+  // (round 9.47 vs 9.15 ms; too few stages in flight for the branch step).
+  int cl_small = 0;
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
@@ -516,10 +520,10 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
 }
 
 // Cluster split-K GEMM (gemm_cl.cuh): NC clusters of CS CTAs.
-template <int EPI, int NP, int CS>
+template <int EPI, int NP, int CS, int BUDGET_KB = 224>
 static void gemm_cl_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                            cudaStream_t s, Prefetch pf) {
-  using C = tc::ClCfg<NP>;
+  using C = tc::ClCfg<NP, BUDGET_KB>;
   const int NC = E_num_sms / CS;
   const int KU = W.K / (tc::kBK * tc::kKPS);
   tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, 0};
@@ -537,7 +541,7 @@ static void gemm_cl_launch(Model& m, const WMat& W, const bf16* X, int M, float*
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  CK(cudaLaunchKernelEx(&cfg, tc::gemm_cl_kernel<EPI, NP, CS>, act_map(m, X, W.K, NP), g));
+  CK(cudaLaunchKernelEx(&cfg, tc::gemm_cl_kernel<EPI, NP, CS, BUDGET_KB>, act_map(m, X, W.K, NP), g));
 }
 
 // Cluster size minimising the units on a CTA's critical path (whole tiles
@@ -553,21 +557,31 @@ static int pick_cluster(const WMat& W) {
   return best;
 }
 
+// small = the co-resident budget (114 KB with its partial buffers): one such
+// CTA fits beside a 108 KB GEMM CTA of the other stream (co-running loops).
+constexpr int kClSmallBudgetKB = 116;
 template <int EPI, int NP>
 static void gemm_cl_dispatch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                             cudaStream_t s, Prefetch pf) {
-  switch (pick_cluster(W)) {
+                             cudaStream_t s, Prefetch pf, bool small) {
+  const int cs = pick_cluster(W);
+  if (small) {
+    if (cs == 2) gemm_cl_launch<EPI, NP, 2, kClSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    else if (cs == 4) gemm_cl_launch<EPI, NP, 4, kClSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    else gemm_cl_launch<EPI, NP, 8, kClSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    return;
+  }
+  switch (cs) {
     case 2: gemm_cl_launch<EPI, NP, 2>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
     case 4: gemm_cl_launch<EPI, NP, 4>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
     default: gemm_cl_launch<EPI, NP, 8>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf); break;
   }
 }
 
-template <int EPI, int NP, int CS>
+template <int EPI, int NP, int CS, int BUDGET_KB = 224>
 static void configure_cl() {
-  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(tc::ClCfg<NP>::kSmem)));
-  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS, BUDGET_KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(tc::ClCfg<NP, BUDGET_KB>::kSmem)));
+  CK(cudaFuncSetAttribute(tc::gemm_cl_kernel<EPI, NP, CS, BUDGET_KB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           int(cudaSharedmemCarveoutMaxShared)));
 }
 
@@ -649,6 +663,9 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
   configure_cl<EPI_STORE, 32, 2>(); configure_cl<EPI_STORE, 32, 4>(); configure_cl<EPI_STORE, 32, 8>();
   configure_cl<EPI_SWIGLU, 32, 2>(); configure_cl<EPI_SWIGLU, 32, 4>(); configure_cl<EPI_SWIGLU, 32, 8>();
+  configure_cl<EPI_STORE, 32, 2, kClSmallBudgetKB>(); configure_cl<EPI_STORE, 32, 4, kClSmallBudgetKB>();
+  configure_cl<EPI_STORE, 32, 8, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 32, 2, kClSmallBudgetKB>();
+  configure_cl<EPI_SWIGLU, 32, 4, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 32, 8, kClSmallBudgetKB>();
   configure_gemm<EPI_STORE, 32, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 32, tc::kSmallBudgetKB>();
   for (auto f : {attention_cl_kernel<1>, attention_cl_kernel<2>, attention_cl_kernel<4>, attention_cl_kernel<8>})
     carveout_max(f);
@@ -735,7 +752,7 @@ static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, flo
   // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
   if (W.bytes <= E.cl_gemm_bytes && M > 16 && M <= 32 && m.gemm_ctas == 0) {
-    gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
     return;
   }
   // small weight matrices: the co-resident (small-budget) configuration
@@ -1404,6 +1421,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
+  if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
   {

@@ -52,13 +52,13 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <int NP>
+template <int NP, int BUDGET_KB = 224>
 struct ClCfg {
   static constexpr int kBBlock = NP * kBK * 2;
   static constexpr int kBBytes = kBBlock * kKPS;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kPart = NP * kBM * 4;  // one partial [NP][128] fp32
-  static constexpr int kBudget = 224 * 1024 - 2 * kPart - 2048;
+  static constexpr int kBudget = BUDGET_KB * 1024 - 2 * kPart - 2048;
   static constexpr int kStages = (kBudget / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
                                                                                : kBudget / kStageBytes;
   static_assert(kStages >= 2, "cluster GEMM: shared memory");
@@ -70,9 +70,9 @@ struct ClCfg {
 // Unit range of rank r in a tile of KU units split over CS ranks.
 __device__ __forceinline__ int kbeg(int r, int KU, int CS) { return r * KU / CS; }
 
-template <int EPI, int NP, int CS>
+template <int EPI, int NP, int CS, int BUDGET_KB = 224>
 __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
-  using C = ClCfg<NP>;
+  using C = ClCfg<NP, BUDGET_KB>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
