@@ -245,6 +245,9 @@ struct Engine {
   // 2-stage) budget inside the co-running round. Off: measured slower
   // (round 9.47 vs 9.15 ms; too few stages in flight for the branch step).
   int cl_small = 0;
+  // SSD_B200_CORUN_ATTN_KB: attention_dec smem cap inside the co-running round
+  // (measured neutral: 80-140 KB give 9.13-9.16 vs 9.12-9.13 ms per round)
+  int corun_attn_kb = 227;
   // colocated SSD: SMs given to the verifier's / speculator's GEMMs so that
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
@@ -882,6 +885,9 @@ static void attn_dec_launch_g(Model& m, int M, const FwdParams* P, bf16* kc, bf1
 }
 
 static int g_attn_stage = 1;  // SSD_B200_ATTN_STAGE=0: never stage KV rows in shared memory
+// shared-memory cap of an attention_dec CTA (its staged rows), KB; lowered
+// inside the co-running SSD round when SSD_B200_CORUN_ATTN_KB is set
+static int g_attn_smem_cap_kb = 227;
 
 template <int G, int HD>
 static void attn_dec_pick(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap,
@@ -896,7 +902,9 @@ static void attn_dec_pick(Model& m, int M, const FwdParams* P, bf16* kc, bf16* v
   }
   if (size_t(M) * m.s.n_kv_heads <= size_t(E_num_sms) && g_attn_stage) {
     // one CTA per SM: stage as many main KV rows as shared memory holds
-    const size_t room = kSmemMax - attn_dec_smem(G, HD, kcap, 0);
+    const size_t cap = std::min(kSmemMax, size_t(g_attn_smem_cap_kb) * 1024);
+    const size_t base = attn_dec_smem(G, HD, kcap, 0);
+    const size_t room = cap > base ? cap - base : 0;
     const int nst = int(std::min<size_t>(size_t(kcap), room / (size_t(4) * HD)));
     attn_dec_launch_g<G, HD, 1>(m, M, P, kc, vc, scale, kcap, nst, 0, s, pf);
   } else {
@@ -1422,6 +1430,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
+  if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
   {
@@ -1712,18 +1721,19 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   E.D.gemm_ctas = E.split_d;
   const long long small_saved = E.small_gemm_bytes;
   E.small_gemm_bytes = std::max(E.small_gemm_bytes, E.corun_small_gemm_bytes);  // co-running streams
+  g_attn_smem_cap_kb = E.corun_attn_kb;
   struct Uncap {
     Engine& e;
     long long small;
-    ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; e.small_gemm_bytes = small; }
+    ~Uncap() { e.T.gemm_ctas = e.D.gemm_ctas = 0; e.small_gemm_bytes = small; g_attn_smem_cap_kb = 227; }
   } uncap{E, small_saved};
   // every value the capture bakes into kernel parameters or launch shapes
   char keybuf[512];
-  std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p %lld",
+  std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p %lld %d",
                 K, B, max_f, nb, c->scheme.kind, c->scheme.fan_out, c->scheme.temperature, c->scheme.downweight,
                 c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
-                static_cast<void*>(E.ssd_log), E.small_gemm_bytes);
+                static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
   const std::string key(keybuf);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
@@ -1755,6 +1765,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   const long long per_round = E.ssd_graph_launches;
   E.launches = 0;
   E.small_gemm_bytes = small_saved;  // JIT re-drafts below run alone on one stream
+  g_attn_smem_cap_kb = 227;
   long long jit_launches = 0;
   std::vector<int> hits(static_cast<size_t>(nb));
   CK(cudaEventRecord(E.ev_t0, sv));
