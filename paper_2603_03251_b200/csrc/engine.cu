@@ -214,6 +214,9 @@ struct Engine {
   // L2 prefetch look-ahead of the weight stream (SSD_B200_PF_MB). 16 MB:
   // colocated SSD round 9.53 -> 9.41 ms vs 32 MB (scripts/split_sms_sweep.py)
   long long pf_ahead = 16LL << 20;
+  // SSD_B200_PF_MB_DRAFT: the draft model's look-ahead (-1: pf_ahead); measured
+  // within noise of the shared 16 MB (0 / 4 / 32 MB: 9.09 / 9.11 / 9.17 ms per round)
+  long long pf_ahead_draft = -1;
   // Persistent forward kernel (fwd_mk.cuh) for M <= 64: SSD_B200_MK=1. Off by
   // default: measured slower than the per-op PDL chain (profiles/r01_summary.md:
   // tcgen05 at N <= 32 consumes a 32 KB unit per ~0.77 us per SM, i.e. no faster
@@ -1006,7 +1009,7 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, H = sh.n_heads, KVH = sh.n_kv_heads, hd = sh.head_dim, F = sh.ffn;
   const int nqkv = m.qd + 2 * m.kvd;
-  PfCursor pf(m, E.pf_ahead, logits != nullptr);
+  PfCursor pf(m, (m.role == 1 && E.pf_ahead_draft >= 0) ? E.pf_ahead_draft : E.pf_ahead, logits != nullptr);
   launch_pdl(embed_kernel, dim3(M), dim3(256), 0, s, (const bf16*)m.embed, d, m.embed_tiled, P, m.x, pf.upto(0));
   ++E.launches;
   const float scale = 1.0f / std::sqrt(float(hd));
@@ -1420,6 +1423,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   E.role = role;
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
+  if (const char* pfd = std::getenv("SSD_B200_PF_MB_DRAFT")) E.pf_ahead_draft = std::max(0LL, std::atoll(pfd)) << 20;
   if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
