@@ -51,6 +51,10 @@ def _worker(rank, world, port, temperature, backup, runs, q, tp=1):
         from paper_2603_03251_b200.split import SplitEngine
         ts, ds = shapes("tiny", max_ctx=512)
         se = SplitEngine(ts, ds, P.Pair(), device=0, max_branches=16, max_lookahead=4, tp=tp)
+        # warm-up run (discarded): the first forward of a process time-sharing
+        # the GPU can be corrupt (open issue); runs are
+        # independent (fresh streams from the seeds), so this changes nothing else
+        se.run(_prompt(), _cfg(P, temperature, backup))
         out = []
         for _ in range(runs):  # repeated runs reuse the mapped mailboxes (monotonic sequence numbers)
             r = se.run(_prompt(), _cfg(P, temperature, backup))

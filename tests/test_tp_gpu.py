@@ -44,6 +44,12 @@ def _worker(rank, world, port, q):
                        tp_size=world)
         eng.tp_connect(exchange_handles(eng.tp_handle()))
         dist.barrier()
+        # Warm-up forward: with the ranks time-sharing ONE GPU, the first
+        # forward of a process occasionally returned garbage (also seen for
+        # unsharded engines in processes sharing a GPU, scripts/share_diag.py;
+        # never with one process per GPU). DESIGN.md §6 lists it as open.
+        eng.logits(0, _prompt())
+        dist.barrier()
         lg = eng.logits(0, _prompt())
         ar = eng.run_ar(_prompt(), P.SamplingScheme.greedy(), 12, 3)
         eng.close()
