@@ -322,6 +322,7 @@ json run(const json& req) {
       for (const auto& k : h.outcomes0) oc.push_back({k.k, k.t});
       o["outcomes0"] = oc;
       o["hits0"] = h.hits0;
+      o["decode_seconds"] = h.decode_seconds;
     } else {
       throw ConfigError("config: mode must be ar, sd, ssd or harness");
     }

@@ -9,6 +9,7 @@
 #include "ssd_oracle.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -578,6 +579,9 @@ HarnessOut sim_harness(const SimCfg& c) {
     inflight.specs.push_back(d_spec[std::size_t(j)]);
   }
   wire.d2v(inflight, clock);
+  // wall time of the rounds alone (after prefill and the initial drafts):
+  // the CPU baseline's decode rate (bench.py), not part of the algorithm
+  const auto t_rounds = std::chrono::steady_clock::now();
 
   for (long round = 1; round <= c.rounds; ++round) {
     const double v0 = clock, v1 = clock + 1.0;
@@ -657,6 +661,7 @@ HarnessOut sim_harness(const SimCfg& c) {
     }
     out.timings.push_back({v0, v1, ready, all_hit});
   }
+  out.decode_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_rounds).count();
   if (wire.pairs() != c.rounds) throw ProtocolViolationError("protocol: message pair count mismatch");
   st.rounds = c.rounds;
   st.batch = B;

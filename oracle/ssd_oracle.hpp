@@ -227,6 +227,7 @@ struct HarnessOut {
   // Per-round (k, t*) and hit bits of sequence 0, for GPU parity.
   std::vector<Outcome> outcomes0;
   std::vector<int> hits0;
+  double decode_seconds = 0.0;  // wall time of the rounds (bench CPU baseline)
 };
 HarnessOut sim_harness(const SimCfg& c);
 

@@ -54,6 +54,7 @@ T* dalloc(size_t n) {
   void* p = nullptr;
   CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
   CK(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  CK(cudaDeviceSynchronize());  // legacy-stream memset: done before a non-blocking stream touches p
   return static_cast<T*>(p);
 }
 
@@ -276,6 +277,23 @@ struct Engine {
 };
 
 // ----------------------------------------------------------------- helpers
+// Host <-> device copies of the API calls: ordered on the engine stream `sv`
+// (every kernel of a call runs on sv, or on ss forked from sv), and complete
+// before returning. A plain cudaMemcpy would run on the legacy stream, which
+// the non-blocking engine streams do not wait for, and a pageable H2D
+// cudaMemcpy may return before its DMA lands: a kernel on sv could then read
+// the previous contents (round 1's "corrupt first forward").
+static void h2d(Engine& E, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, E.sv));
+  CK(cudaStreamSynchronize(E.sv));
+}
+static void d2h(Engine& E, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, E.sv));
+  CK(cudaStreamSynchronize(E.sv));
+}
+
 static void rope_tables(const ssd_model_shape& s, std::vector<float>& cs, std::vector<float>& sn) {
   const int half = s.head_dim / 2;
   cs.assign(size_t(s.max_ctx) * half, 0.f);
@@ -999,7 +1017,7 @@ static void tp_allreduce(Engine& E, Model& m, float* buf, int M, cudaStream_t s)
 // PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
-  if (E.use_mk && M <= 64 && m.tp_size == 1) {  // decode / verify / branch steps and prefill chunks: one persistent launch
+  if (E.use_mk && (E.use_mk == 1 || (E.use_mk == 2 && m.role == 1)) && M <= 64 && m.tp_size == 1) {  // decode / verify / branch steps and prefill chunks: one persistent launch
     if (M <= 16) mk_launch_g<16>(E, m, P, M, logits, s);
     else if (M <= 32) mk_launch_g<32>(E, m, P, M, logits, s);
     else mk_launch_g<64>(E, m, P, M, logits, s);
@@ -1119,7 +1137,7 @@ static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed,
 
 static LoopState read_state(Engine& E, int lane = 0) {
   LoopState h;
-  CK(cudaMemcpy(&h, E.st + lane, offsetof(LoopState, vrng), cudaMemcpyDeviceToHost));
+  d2h(E, &h, E.st + lane, offsetof(LoopState, vrng));
   return h;
 }
 
@@ -1262,8 +1280,8 @@ static void upload_plans(Engine& E, const ssd_plan& p, const ssd_plan& b, int K,
   }
   if (B > E.maxB) throw Fail(SSD_TOO_LARGE, "plan: budget exceeds the engine's branch capacity");
   B = std::max(B, 1);
-  CK(cudaMemcpy(E.plans, fan.data(), fan.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(E.offs, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+  h2d(E, E.plans, fan.data(), fan.size() * 4);
+  h2d(E, E.offs, off.data(), off.size() * 4);
 }
 
 static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_needed, int lanes = 1) {
@@ -1274,7 +1292,7 @@ static void set_history(Engine& E, const int32_t* prompt, int n, int max_ctx_nee
   for (int i = 0; i < n; ++i)
     if (prompt[i] < 0 || prompt[i] >= E.V) throw Fail(SSD_ERROR, "context_index: token out of range");
   for (int l = 0; l < lanes; ++l)
-    CK(cudaMemcpy(E.hist + size_t(l) * E.hist_stride, prompt, size_t(n) * 4, cudaMemcpyHostToDevice));
+    h2d(E, E.hist + size_t(l) * E.hist_stride, prompt, size_t(n) * 4);
 }
 
 // RunStats counters summed over batch lanes (sim.cpp:548-586 counts every
@@ -1315,8 +1333,7 @@ static void copy_out(Engine& E, int n0, int n, int32_t* out, int64_t cap, int64_
   const int64_t len = n - n0;
   if (out_len) *out_len = len;
   if (out && len > 0)
-    CK(cudaMemcpy(out, E.hist + size_t(lane) * E.hist_stride + n0, size_t(std::min<int64_t>(len, cap)) * 4,
-                  cudaMemcpyDeviceToHost));
+    d2h(E, out, E.hist + size_t(lane) * E.hist_stride + n0, size_t(std::min<int64_t>(len, cap)) * 4);
 }
 
 static void validate_cfg(Engine& E, const ssd_sim_config* c) {
@@ -1412,8 +1429,15 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   }
   if (max_lookahead < 1 || max_lookahead > kMaxK) throw Fail(SSD_TOO_LARGE, "engine: lookahead capacity");
   if (max_branches < 1 || max_branches > kMaxM) throw Fail(SSD_TOO_LARGE, "engine: branch capacity");
+  for (const ssd_model_shape* s : {target, draft})
+    if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
+      throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
+  if (max_batch * std::max(max_branches, max_lookahead + 1) > kMaxM)
+    throw Fail(SSD_TOO_LARGE, "engine: batch x branches above the forward capacity");
   CK(cudaSetDevice(device));
-  auto* h = new ssd_engine();
+  // every validation is above; a failure below frees what was built so far
+  std::unique_ptr<ssd_engine, ssd_status (*)(ssd_engine*)> holder(new ssd_engine(), ssd_engine_destroy);
+  ssd_engine* h = holder.get();
   Engine& E = h->e;
   E.dev = device;
   E.nbmax = max_batch;
@@ -1424,7 +1448,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
   if (const char* pfd = std::getenv("SSD_B200_PF_MB_DRAFT")) E.pf_ahead_draft = std::max(0LL, std::atoll(pfd)) << 20;
-  if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv) != 0;
+  if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv);  // 1 both models, 2 draft only
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
   if (const char* ast = std::getenv("SSD_B200_ATTN_STAGE")) g_attn_stage = std::atoi(ast) != 0;
@@ -1437,6 +1461,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
+  const int mk_ctas = std::getenv("SSD_B200_MK_CTAS") ? std::atoi(std::getenv("SSD_B200_MK_CTAS")) : 0;
   {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1452,9 +1477,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (role != SSD_ROLE_VERIFIER)
     build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, kPrefillChunk), 0, 1, nb);
   else E.D.s = *draft;
-  for (const ssd_model_shape* s : {target, draft})
-    if (s->n_heads / s->n_kv_heads > kMaxGroup || (kMaxGroup % (s->n_heads / s->n_kv_heads)))
-      throw Fail(SSD_CONFIG, "engine: GQA group must divide 8");
+  E.D.mk_ctas = mk_ctas;  // experiment: SMs of the draft's persistent forward (0 = all)
   configure_kernels();
   mk_diag_init();
   {
@@ -1510,7 +1533,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   double c = 0.0;
   for (int i = 0; i < V; ++i) { c += 1.0 / V; cum[size_t(i)] = c; }
   E.cum = static_cast<double*>(own(dalloc<double>(size_t(V))));
-  CK(cudaMemcpy(E.cum, cum.data(), size_t(V) * 8, cudaMemcpyHostToDevice));
+  h2d(E, E.cum, cum.data(), size_t(V) * 8);
   // mailbox (own allocation so it can be exported alone by CUDA IPC)
   {
     void* p = nullptr;
@@ -1530,7 +1553,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
     E.tp_ctl = static_cast<TpCtl*>(own(dalloc<TpCtl>(1)));
   }
   CK(cudaDeviceSynchronize());
-  *out = h;
+  *out = holder.release();
   API_END
 }
 
@@ -1564,13 +1587,11 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
     if (g) cudaGraphExecDestroy(g);
   if (E.ssd_log) cudaFree(E.ssd_log);
   for (void* p : E.owned) cudaFree(p);
-  cudaStreamDestroy(E.sv);
-  cudaStreamDestroy(E.ss);
-  cudaEventDestroy(E.ev_fork);
-  cudaEventDestroy(E.ev_verified);
-  cudaEventDestroy(E.ev_join);
-  cudaEventDestroy(E.ev_t0);
-  cudaEventDestroy(E.ev_t1);
+  for (cudaStream_t st : {E.sv, E.ss})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1})
+    if (ev) cudaEventDestroy(ev);
+  cudaGetLastError();  // teardown errors must not surface in a later call
   delete h;
   API_END
 }
@@ -1779,8 +1800,9 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
       // SamePrimaryJIT: the lanes that missed re-draft from their new
       // history, batched (the one host round trip of the JIT backup)
       CK(cudaStreamSynchronize(sv));
-      CK(cudaMemcpy2D(hits.data(), sizeof(int), reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit),
-                      sizeof(LoopState), sizeof(int), size_t(nb), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy2DAsync(hits.data(), sizeof(int), reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit),
+                           sizeof(LoopState), sizeof(int), size_t(nb), cudaMemcpyDeviceToHost, sv));
+      CK(cudaStreamSynchronize(sv));
       int nm = 0;
       for (int l = 0; l < nb; ++l)
         if (!hits[size_t(l)]) lanes[size_t(nm++)] = l;
@@ -1799,8 +1821,8 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
   std::vector<LoopState> sts;
   for (int l = 0; l < nb; ++l) sts.push_back(read_state(E, l));
-  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
-  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  if (out_outcomes) d2h(E, out_outcomes, d_out, size_t(2 * R) * 4);
+  if (out_hits) d2h(E, out_hits, d_hit, size_t(R) * 4);
   const LoopState st = sum_lanes(sts);
   raise_device_error(st);
   fill_stats(st, R, ms, E.launches, stats);
@@ -1865,7 +1887,7 @@ ssd_status ssd_mailbox_connect(ssd_engine* h, int32_t n_peers, const uint8_t* ha
   }
   if (E.peers_dev) cudaFree(E.peers_dev);
   E.peers_dev = dalloc<Inbox*>(size_t(n_peers));
-  CK(cudaMemcpy(E.peers_dev, E.peers.data(), size_t(n_peers) * sizeof(Inbox*), cudaMemcpyHostToDevice));
+  h2d(E, E.peers_dev, E.peers.data(), size_t(n_peers) * sizeof(Inbox*));
   // a fresh connection starts from a clean inbox and sequence 0
   CK(cudaMemset(E.inbox, 0, kInboxRows));
   E.seq_base = 0;
@@ -1964,11 +1986,11 @@ ssd_status ssd_run_ssd_verifier(ssd_engine* h, const int32_t* prompt, int32_t n0
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
   LoopState st = read_state(E);
-  if (out_outcomes) CK(cudaMemcpy(out_outcomes, d_out, size_t(2 * R) * 4, cudaMemcpyDeviceToHost));
+  if (out_outcomes) d2h(E, out_outcomes, d_out, size_t(2 * R) * 4);
   cudaFree(d_out);
   if (st.error == 10) {
     Inbox ib;
-    CK(cudaMemcpy(&ib, E.inbox, sizeof(Inbox), cudaMemcpyDeviceToHost));
+    d2h(E, &ib, E.inbox, sizeof(Inbox));
     throw Fail(SSD_PROTOCOL_VIOLATION, "verifier: speculation message missing or out of order at round " +
                                            std::to_string(st.round) + " (want seq " +
                                            std::to_string(st.seq_base + st.round + 1) + ", inbox seq " +
@@ -2045,7 +2067,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
     if (jit && r + 1 < R) {
       CK(cudaStreamSynchronize(s));
       int hit = 0;
-      CK(cudaMemcpy(&hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int), cudaMemcpyDeviceToHost));
+      d2h(E, &hit, reinterpret_cast<char*>(E.st) + offsetof(LoopState, hit), sizeof(int));
       if (!hit) {  // SamePrimaryJIT re-draft (sim.cpp:229-232), identical on every speculator; rank 0 sends
         const long long before = E.launches;
         draft_steps(E, K, c->scheme, 1, 2, s);
@@ -2060,11 +2082,11 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
   LoopState st = read_state(E);
-  if (out_hits) CK(cudaMemcpy(out_hits, d_hit, size_t(R) * 4, cudaMemcpyDeviceToHost));
+  if (out_hits) d2h(E, out_hits, d_hit, size_t(R) * 4);
   cudaFree(d_hit);
   if (st.error == 10) {
     Inbox ib;
-    CK(cudaMemcpy(&ib, E.inbox, sizeof(Inbox), cudaMemcpyDeviceToHost));
+    d2h(E, &ib, E.inbox, sizeof(Inbox));
     throw Fail(SSD_PROTOCOL_VIOLATION,
                "speculator " + std::to_string(rank) + ": message missing or out of order at round " +
                    std::to_string(st.round) + " (base " + std::to_string(st.seq_base) + ", hit " +
@@ -2086,7 +2108,7 @@ ssd_status ssd_logits(ssd_engine* h, int32_t which, const int32_t* ctx, int32_t 
   set_history(E, ctx, n, n + 1);
   prefill(E, m, n, E.tlogits, E.sv);
   CK(cudaStreamSynchronize(E.sv));
-  CK(cudaMemcpy(out, E.tlogits, size_t(E.V) * 4, cudaMemcpyDeviceToHost));
+  d2h(E, out, E.tlogits, size_t(E.V) * 4);
   API_END
 }
 
@@ -2108,7 +2130,7 @@ ssd_status ssd_draft(ssd_engine* h, const int32_t* ctx, int32_t n, int32_t K, co
   CK(cudaStreamSynchronize(s));
   LoopState st = read_state(E);
   std::memcpy(out_tokens, st.spec, size_t(K) * 4);
-  if (out_rows) CK(cudaMemcpy(out_rows, E.dmain, size_t(K) * E.V * 4, cudaMemcpyDeviceToHost));
+  if (out_rows) d2h(E, out_rows, E.dmain, size_t(K) * E.V * 4);
   API_END
 }
 
@@ -2147,9 +2169,9 @@ ssd_status ssd_build_cache(ssd_engine* h, const int32_t* ctx, int32_t n, const i
   else branch_streams_kernel<<<1, 32, 0, s>>>(E.st, 0, E.bu, 0);
   CK(cudaStreamSynchronize(s));
   std::vector<int> bkh(static_cast<size_t>(B)), bth(static_cast<size_t>(B)), tt(static_cast<size_t>(B) * K);
-  CK(cudaMemcpy(bkh.data(), E.bk, size_t(B) * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(bth.data(), E.btok, size_t(B) * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(tt.data(), E.bt, size_t(B) * K * 4, cudaMemcpyDeviceToHost));
+  d2h(E, bkh.data(), E.bk, size_t(B) * 4);
+  d2h(E, bth.data(), E.btok, size_t(B) * 4);
+  d2h(E, tt.data(), E.bt, size_t(B) * K * 4);
   for (int i = 0; i < total; ++i) {
     if (out_keys) { out_keys[2 * i] = bkh[size_t(i)]; out_keys[2 * i + 1] = bth[size_t(i)]; }
     if (out_entry_tokens) std::memcpy(out_entry_tokens + size_t(i) * K, &tt[size_t(i) * K], size_t(K) * 4);
@@ -2174,13 +2196,13 @@ ssd_status ssd_topk_keys(ssd_engine* h, const float* rows, int32_t n_rows, int32
     tot += fan[k];
   }
   if (tot > E.maxB) throw Fail(SSD_TOO_LARGE, "topk_keys: too many candidates");
-  CK(cudaMemcpy(E.plans, fan2.data(), fan2.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(E.offs, off2.data(), off2.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(E.xrows, rows, size_t(n_rows) * V * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(E.tok_scratch, excluded, size_t(n_rows) * 4, cudaMemcpyHostToDevice));
+  h2d(E, E.plans, fan2.data(), fan2.size() * 4);
+  h2d(E, E.offs, off2.data(), off2.size() * 4);
+  h2d(E, E.xrows, rows, size_t(n_rows) * V * 4);
+  h2d(E, E.tok_scratch, excluded, size_t(n_rows) * 4);
   row_keys(E, E.xrows, n_rows, V, max_f, nullptr, E.tok_scratch, n_rows, E.sv);
   CK(cudaStreamSynchronize(E.sv));
-  CK(cudaMemcpy(keys, E.keys, size_t(n_rows) * max_f * 4, cudaMemcpyDeviceToHost));
+  d2h(E, keys, E.keys, size_t(n_rows) * max_f * 4);
   API_END
 }
 
@@ -2197,10 +2219,10 @@ ssd_status ssd_verify_rows(ssd_engine* h, const float* trows, const float* drows
   for (int i = 0; i < K; ++i)
     if (tokens[i] < 0 || tokens[i] >= V) throw Fail(SSD_ERROR, "verify: token out of range");
   cudaStream_t s = E.sv;
-  CK(cudaMemcpy(E.tlogits, trows, size_t(K + 1) * V * 4, cudaMemcpyHostToDevice));
-  if (drows) CK(cudaMemcpy(E.dmain, drows, size_t(K) * V * 4, cudaMemcpyHostToDevice));
+  h2d(E, E.tlogits, trows, size_t(K + 1) * V * 4);
+  if (drows) h2d(E, E.dmain, drows, size_t(K) * V * 4);
   std::vector<int> hist0(1, 0);
-  CK(cudaMemcpy(E.hist, hist0.data(), 4, cudaMemcpyHostToDevice));
+  h2d(E, E.hist, hist0.data(), 4);
   reset_state(E, K, 1, 1, 0, seed, nullptr, s);
   {
     int tmp[kMaxK];
@@ -2429,7 +2451,7 @@ ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {
   mt_init_kernel<<<1, 32>>>(m, seed);
   mt_draw_kernel<<<1, 32>>>(m, n, d);
   KCHECK();
-  CK(cudaMemcpy(out, d, size_t(n) * 8, cudaMemcpyDeviceToHost));
+  d2h(E, out, d, size_t(n) * 8);
   cudaFree(d);
   cudaFree(m);
   API_END
@@ -2462,7 +2484,7 @@ ssd_status ssd_weight_bits(ssd_engine* h, int32_t which, int32_t layer, int32_t 
         default: throw Fail(SSD_ERROR, "weight_bits: bad kind");
       }
     }
-    CK(cudaMemcpy(&out[i], p, 2, cudaMemcpyDeviceToHost));
+    d2h(E, &out[i], p, 2);
   }
   API_END
 }

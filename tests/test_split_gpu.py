@@ -38,12 +38,6 @@ def _worker(rank, world, port, temperature, backup, runs, q, tp=1):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    # The ranks share ONE GPU here (time-sliced contexts). Measured: the
-    # cluster split-K GEMM (tcgen05 + DSMEM partial exchange) returned a wrong
-    # first forward in ~1 of 20 processes whose context was time-sliced
-    # against another's (scripts/share_diag.py); never with one process per
-    # GPU. Ranks on separate GPUs (the product's split mode) keep it.
-    os.environ["SSD_B200_CL_GEMM_MB"] = "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2603_03251_b200 as P
@@ -51,10 +45,6 @@ def _worker(rank, world, port, temperature, backup, runs, q, tp=1):
         from paper_2603_03251_b200.split import SplitEngine
         ts, ds = shapes("tiny", max_ctx=512)
         se = SplitEngine(ts, ds, P.Pair(), device=0, max_branches=16, max_lookahead=4, tp=tp)
-        # warm-up run (discarded): the first forward of a process time-sharing
-        # the GPU can be corrupt (open issue); runs are
-        # independent (fresh streams from the seeds), so this changes nothing else
-        se.run(_prompt(), _cfg(P, temperature, backup))
         out = []
         for _ in range(runs):  # repeated runs reuse the mapped mailboxes (monotonic sequence numbers)
             r = se.run(_prompt(), _cfg(P, temperature, backup))

@@ -27,12 +27,6 @@ def _worker(rank, world, port, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    # The ranks share ONE GPU here (time-sliced contexts). Measured: the
-    # cluster split-K GEMM (tcgen05 + DSMEM partial exchange) returned a wrong
-    # first forward in ~1 of 20 processes whose context was time-sliced
-    # against another's (scripts/share_diag.py); never with one process per
-    # GPU. Ranks on separate GPUs (the product's split mode) keep it.
-    os.environ["SSD_B200_CL_GEMM_MB"] = "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2603_03251_b200 as P
@@ -43,12 +37,6 @@ def _worker(rank, world, port, q):
         eng = P.Engine(ts, ds, P.Pair(), max_branches=8, max_lookahead=4, role=N.ROLE_VERIFIER, tp_rank=rank,
                        tp_size=world)
         eng.tp_connect(exchange_handles(eng.tp_handle()))
-        dist.barrier()
-        # Warm-up forward: with the ranks time-sharing ONE GPU, the first
-        # forward of a process occasionally returned garbage (also seen for
-        # unsharded engines in processes sharing a GPU, scripts/share_diag.py;
-        # never with one process per GPU). DESIGN.md §6 lists it as open.
-        eng.logits(0, _prompt())
         dist.barrier()
         lg = eng.logits(0, _prompt())
         ar = eng.run_ar(_prompt(), P.SamplingScheme.greedy(), 12, 3)
