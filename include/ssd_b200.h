@@ -311,15 +311,19 @@ ssd_status ssd_verify_rows(ssd_engine* e, const float* target_rows, const float*
 ssd_status ssd_profile_forward(ssd_engine* e, int32_t which, int32_t M, int32_t pos, int32_t iters,
                                double* ms_forward, double* ms_gemm, int64_t* gemm_bytes, int32_t* gemm_launches);
 
+/* In-graph profile of the colocated SSD round: runs the same
+ * round graphs as ssd_run_ssd, captured with event-record nodes at the
+ * segment boundaries of both streams, one host sync per round. out_ms[9]
+ * (averages over cfg->rounds rounds): [0] round, [1] verify forward (8B,
+ * M = K+1, co-running), [2] verify decision, [3] extend forward (draft,
+ * M = K+1), [4] cache keys + branch streams, [5] K branch-step forwards
+ * (M = B, summed), [6] their token picks, [7] join + lookup, [8] fork lag. */
+ssd_status ssd_profile_ssd_round(ssd_engine* e, const int32_t* prompt, int32_t prompt_len,
+                                 const ssd_sim_config* cfg, double* out_ms, ssd_run_stats* stats);
+
 /* Read-only HBM streaming probe: achievable read bandwidth (GB/s) of a
  * plain vectorised load kernel over `bytes`, averaged over `iters`. */
 ssd_status ssd_bench_read_bw(ssd_engine* e, int64_t bytes, int32_t iters, double* gbs);
-
-/* TMA bulk-copy streaming probe (the GEMM's weight-stream shape): blocks of
- * `block_bytes` through `stages`-deep mbarrier rings, mode 0 = contiguous
- * range per CTA, 1 = round-robin blocks (chip-wide contiguous window). */
-ssd_status ssd_bench_tma_stream(ssd_engine* e, int64_t bytes, int32_t block_bytes, int32_t stages, int32_t mode,
-                                int32_t ctas_per_sm, int32_t iters, double* gbs);
 
 /* mt19937_64 parity: n outputs of Stream(seed).next_u64() computed on the GPU. */
 ssd_status ssd_rng_u64(ssd_engine* e, uint64_t seed, int32_t n, uint64_t* out);

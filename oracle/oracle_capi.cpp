@@ -357,7 +357,7 @@ char* oracle_call(const char* request) {
 
 void oracle_free(char* p) { std::free(p); }
 
-// Transformer pair: {"target": shape, "draft": shape, "pair": params, "threads": n}
+// Transformer pair: {"target": shape, "draft": shape, "pair": params, "threads": n, "accum": "f32"|"f64"}
 int oracle_tf_create(const char* request) {
   try {
     const json j = json::parse(request);
@@ -367,6 +367,10 @@ int oracle_tf_create(const char* request) {
     TfPair p;
     p.target = std::make_unique<TransformerLM>(ts, ds, pp, Role::Target, threads);
     p.draft = std::make_unique<TransformerLM>(ds, ds, pp, Role::Draft, threads);
+    if (j.value("accum", std::string("f32")) == "f64") {
+      p.target->set_f64(true);
+      p.draft->set_f64(true);
+    }
     std::lock_guard<std::mutex> g(g_mu);
     g_pairs[g_next] = std::move(p);
     return g_next++;

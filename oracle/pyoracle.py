@@ -102,8 +102,10 @@ def ref_call(req: dict) -> dict:
 class TfPair:
     """A (target, draft) CPU transformer pair held by the oracle library."""
 
-    def __init__(self, target: dict, draft: dict, pair: dict | None = None, threads: int = 0):
-        self.spec = {"target": target, "draft": draft, "pair": pair or {}, "threads": threads}
+    def __init__(self, target: dict, draft: dict, pair: dict | None = None, threads: int = 0, accum: str = "f32"):
+        """accum "f64": fp64 sums with the same bf16 rounding points — the
+        noise-floor reference of the logit parity tests."""
+        self.spec = {"target": target, "draft": draft, "pair": pair or {}, "threads": threads, "accum": accum}
         self.handle = oracle().lib.oracle_tf_create(json.dumps(self.spec).encode())
         if self.handle < 0:
             raise OracleError("oracle_tf_create failed", 1)

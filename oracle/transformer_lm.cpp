@@ -250,6 +250,12 @@ void TransformerLM::gemv(const std::vector<std::uint16_t>& w, int rows, int cols
   auto body = [&](long rb, long re) {
   for (int r = int(rb); r < int(re); ++r) {
     const std::uint16_t* row = W + std::size_t(r) * std::size_t(cols);
+    if (f64_) {  // noise-floor reference: the same bf16 rounding points, fp64 sums
+      double a = 0.0;
+      for (int c = 0; c < cols; ++c) a += double(from_bf16(row[c])) * double(x[c]);
+      y[r] = float(a);
+      continue;
+    }
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int c = 0;
     for (; c + 8 <= cols; c += 8)
@@ -270,9 +276,15 @@ void TransformerLM::gemv(const std::vector<std::uint16_t>& w, int rows, int cols
 
 namespace {
 // RMSNorm then bf16 rounding (the engine's GEMV input precision).
-void rmsnorm_bf16(const float* x, const float* g, int n, float eps, float* out) {
+void rmsnorm_bf16(const float* x, const float* g, int n, float eps, float* out, bool f64 = false) {
   float ss = 0.f;
-  for (int i = 0; i < n; ++i) ss += x[i] * x[i];
+  if (f64) {
+    double d = 0.0;
+    for (int i = 0; i < n; ++i) d += double(x[i]) * double(x[i]);
+    ss = float(d);
+  } else {
+    for (int i = 0; i < n; ++i) ss += x[i] * x[i];
+  }
   const float r = 1.0f / std::sqrt(ss / float(n) + eps);
   for (int i = 0; i < n; ++i) out[i] = bf16_round(x[i] * r * (g ? g[i] : 1.0f));
 }
@@ -289,7 +301,7 @@ void TransformerLM::step(int token, int pos) {
   const float scale = 1.0f / std::sqrt(float(hd));
   for (int l = 0; l < s_.layers; ++l) {
     Layer& L = layers_[std::size_t(l)];
-    rmsnorm_bf16(x_.data(), nullptr, d, s_.norm_eps, hb_.data());
+    rmsnorm_bf16(x_.data(), nullptr, d, s_.norm_eps, hb_.data(), f64_);
     gemv(L.wq, qd, d, hb_.data(), q_.data());
     gemv(L.wk, kvd, d, hb_.data(), k_.data());
     gemv(L.wv, kvd, d, hb_.data(), v_.data());
@@ -318,13 +330,30 @@ void TransformerLM::step(int token, int pos) {
       for (int j = 0; j <= pos; ++j) {
         const float* kr = &KC[std::size_t(j) * std::size_t(kvd) + std::size_t(kvh * hd)];
         float dot = 0.f;
-        for (int i = 0; i < hd; ++i) dot += q[i] * kr[i];
+        if (f64_) {
+          double dd = 0.0;
+          for (int i = 0; i < hd; ++i) dd += double(q[i]) * double(kr[i]);
+          dot = float(dd);
+        } else {
+          for (int i = 0; i < hd; ++i) dot += q[i] * kr[i];
+        }
         sc[std::size_t(j)] = dot * scale;
         mx = std::max(mx, sc[std::size_t(j)]);
       }
       float den = 0.f;
       for (int j = 0; j <= pos; ++j) { sc[std::size_t(j)] = std::exp(sc[std::size_t(j)] - mx); den += sc[std::size_t(j)]; }
       float* o = &att_[std::size_t(h * hd)];
+      if (f64_) {
+        double dden = 0.0;
+        for (int j = 0; j <= pos; ++j) dden += double(sc[std::size_t(j)]);
+        for (int i = 0; i < hd; ++i) {
+          double a = 0.0;
+          for (int j = 0; j <= pos; ++j)
+            a += double(sc[std::size_t(j)]) * double(VC[std::size_t(j) * std::size_t(kvd) + std::size_t(kvh * hd + i)]);
+          o[i] = bf16_round(float(a / dden));
+        }
+        continue;
+      }
       for (int i = 0; i < hd; ++i) o[i] = 0.f;
       for (int j = 0; j <= pos; ++j) {
         const float* vr = &VC[std::size_t(j) * std::size_t(kvd) + std::size_t(kvh * hd)];
@@ -335,7 +364,7 @@ void TransformerLM::step(int token, int pos) {
     }
     gemv(L.wo, d, qd, att_.data(), tmp_.data());
     for (int i = 0; i < d; ++i) x_[std::size_t(i)] += tmp_[std::size_t(i)];
-    rmsnorm_bf16(x_.data(), l == 0 ? ffn_gain0_.data() : nullptr, d, s_.norm_eps, hb_.data());
+    rmsnorm_bf16(x_.data(), l == 0 ? ffn_gain0_.data() : nullptr, d, s_.norm_eps, hb_.data(), f64_);
     gemv(L.wg, s_.ffn, d, hb_.data(), g_.data());
     gemv(L.wu, s_.ffn, d, hb_.data(), u_.data());
     for (int i = 0; i < s_.ffn; ++i) {
@@ -345,7 +374,7 @@ void TransformerLM::step(int token, int pos) {
     gemv(L.wd, d, s_.ffn, act_.data(), tmp_.data());
     for (int i = 0; i < d; ++i) x_[std::size_t(i)] += tmp_[std::size_t(i)];
   }
-  rmsnorm_bf16(x_.data(), final_gain_.data(), d, s_.norm_eps, hb_.data());
+  rmsnorm_bf16(x_.data(), final_gain_.data(), d, s_.norm_eps, hb_.data(), f64_);
   out_f32_.resize(std::size_t(s_.vocab));
   gemv(s_.tied ? embed_ : head_, s_.vocab, d, hb_.data(), out_f32_.data());
   ++processed_;

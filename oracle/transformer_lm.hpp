@@ -84,6 +84,9 @@ class TransformerLM : public LanguageModel {
   float final_gain(std::size_t i) const { return final_gain_[i]; }
   long tokens_processed() const { return processed_; }
   void reset_cache() { cached_.clear(); }
+  // fp64 accumulation (GEMV, norm, attention) with the same bf16 rounding
+  // points: the noise-floor reference of the logit parity tests.
+  void set_f64(bool on) { f64_ = on; reset_cache(); memo_.clear(); }
 
  private:
   struct Layer {
@@ -94,6 +97,7 @@ class TransformerLM : public LanguageModel {
 
   TfShape s_;
   int threads_;
+  bool f64_ = false;
   std::vector<std::uint16_t> embed_, head_;       // head_ empty when tied
   std::vector<Layer> layers_;
   std::vector<float> final_gain_;

@@ -102,8 +102,7 @@ SIGNATURES = {
     "ssd_profile_forward": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
                                       P(C.c_double), i64p, i32p]),
     "ssd_bench_read_bw": (C.c_int, [EngineP, C.c_int64, C.c_int32, P(C.c_double)]),
-    "ssd_bench_tma_stream": (C.c_int, [EngineP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                       P(C.c_double)]),
+    "ssd_profile_ssd_round": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), P(C.c_double), P(RunStatsC)]),
     "ssd_rng_u64": (C.c_int, [EngineP, C.c_uint64, C.c_int32, u64p]),
     "ssd_weight_bits": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, C.c_int32, u16p]),
 }

@@ -514,6 +514,19 @@ class Engine:
                                             C.byref(n)))
         return {"ms_forward": f.value, "ms_gemm": g.value, "gemm_bytes": b.value, "gemm_launches": n.value}
 
+    ROUND_SEGMENTS = ("round", "verify_forward", "verify_decision", "extend_forward", "keys_streams",
+                      "branch_forwards", "branch_picks", "lookup", "fork_lag")
+
+    def profile_ssd_round(self, prompt: Sequence[int], cfg: SimConfig) -> dict:
+        """ms per segment of the colocated SSD round, measured by event nodes
+        inside the round graph (ssd_profile_ssd_round)."""
+        p = _i32(prompt)
+        out = (C.c_double * 9)()
+        st = N.RunStatsC()
+        _check(self.lib.ssd_profile_ssd_round(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), out,
+                                              C.byref(st)))
+        return {k: float(out[i]) for i, k in enumerate(self.ROUND_SEGMENTS)}
+
     def read_bw(self, nbytes: int = 4 << 30, iters: int = 10) -> float:
         g = C.c_double()
         _check(self.lib.ssd_bench_read_bw(self.h, nbytes, iters, C.byref(g)))

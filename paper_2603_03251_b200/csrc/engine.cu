@@ -21,13 +21,10 @@
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
 #include "gemm_cl.cuh"
-#include "fwd_mk.cuh"
 #include "attn_cl.cuh"
 #include "attn_dec.cuh"
-#include "gemv.cuh"
 #include "tp.cuh"
 #include "kernels.cuh"
-#include "probe.cuh"
 #include "rowops.cuh"
 #include "split.cuh"
 
@@ -159,13 +156,6 @@ struct Model {
   int* counters = nullptr;
   std::vector<ActMap> amaps;
   std::vector<void*> owned;
-  // persistent forward kernel (fwd_mk.cuh)
-  mk::Op* mk_ops[2] = {nullptr, nullptr};  // [0] without, [1] with the LM head
-  int mk_nops[2] = {0, 0};
-  mk::LayerKV* mk_kv = nullptr;
-  float* mk_sumsq = nullptr;                // [d / 128][maxM]
-  unsigned* mk_bar = nullptr;
-  int mk_ctas = 0;                          // CTAs (SMs) of its launches; 0 = all
   int gemm_ctas = 0;                        // cap on a GEMM's CTAs (0 = every SM)
   // tensor parallelism
   int tp_rank = 0, tp_size = 1;
@@ -218,12 +208,6 @@ struct Engine {
   // SSD_B200_PF_MB_DRAFT: the draft model's look-ahead (-1: pf_ahead); measured
   // within noise of the shared 16 MB (0 / 4 / 32 MB: 9.09 / 9.11 / 9.17 ms per round)
   long long pf_ahead_draft = -1;
-  // Persistent forward kernel (fwd_mk.cuh) for M <= 64: SSD_B200_MK=1. Off by
-  // default: measured slower than the per-op PDL chain (profiles/r01_summary.md:
-  // tcgen05 at N <= 32 consumes a 32 KB unit per ~0.77 us per SM, i.e. no faster
-  // than HBM, so the phase barriers / attention latency it exposes are never
-  // caught up).
-  int use_mk = 0;
   int attn_cluster = 1;  // cluster/DSMEM attention (SSD_B200_ATTN_CL=0: global-merge kernel)
   int attn_dec = 1;      // one-CTA-per-(kv head, token) attention (attn_dec.cuh; SSD_B200_ATTN_DEC=0: chunked kernels)
   // ... and for forwards of >= this many tokens: the branch steps (M = 20:
@@ -231,11 +215,6 @@ struct Engine {
   // kernels append every token in every chunk CTA, quadratic in M: 8B M=128
   // forward 24.9 -> 12.3 ms) (SSD_B200_ATTN_DEC_WIDE_M)
   int attn_dec_wide_m = 20;
-  // CUDA-core GEMV (gemv.cuh) for forwards of <= this many tokens
-  // (SSD_B200_GEMV_M=1|2). Off: measured slower than the tcgen05 stream-K
-  // kernel at M = 1 (8B step GEMMs 4.02 vs 2.99 ms: register-staged LDG
-  // streaming keeps too few bytes in flight; profiles/r01c_summary.md).
-  int gemv_max_m = 0;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // ... inside the colocated SSD round, where the verifier and speculator
@@ -256,10 +235,6 @@ struct Engine {
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
   int split_t = 0, split_d = 0;
-  unsigned long long* mk_trace = nullptr;  // debug timeline buffer (ssd_debug_mk_trace)
-  int mk_pf_units = 0;  // L2 look-ahead of the persistent kernel's weight stream (SSD_B200_MK_PF)
-  unsigned long long* mk_utrace = nullptr;
-  int mk_utrace_op[4] = {-1, -1, -1, -1};
   // split processes (split.cuh)
   int role = 0;                      // 0 colocated, 1 verifier, 2 speculator
   Inbox* inbox = nullptr;            // this process's mailbox (+ draft rows)
@@ -268,6 +243,11 @@ struct Engine {
   Inbox** peers_dev = nullptr;       // device copy of `peers`
   int* send_counter = nullptr;
   int seq_base = 0;                  // advances by rounds + 2 per split run
+  // In-graph round profile (ssd_profile_ssd_round): timing events recorded by
+  // event-record nodes of the captured round graph (cudaEventRecordExternal)
+  // at the segment boundaries of both streams; kProfMarks per round.
+  int prof_on = 0;
+  cudaEvent_t prof_ev[32] = {};
   // tensor-parallel verifier (tp.cuh)
   char* tp_region = nullptr;         // this rank's IPC-exported region
   TpLayout tp_L{};
@@ -292,6 +272,15 @@ static void d2h(Engine& E, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, E.sv));
   CK(cudaStreamSynchronize(E.sv));
+}
+
+// Round-profile marks: 0 verifier start, 1 verify forward
+// done, 2 verify decision done, 3 speculator start, 4 extend forward done,
+// 5 keys + branch streams done, 6 + 2j branch step j forward done, 7 + 2j
+// its token pick done (j < 8), 31 lookup done.
+constexpr int kMarkRoundEnd = 31;
+static void mark(Engine& E, int i, cudaStream_t s) {
+  if (E.prof_on) CK(cudaEventRecordWithFlags(E.prof_ev[i], s, cudaEventRecordExternal));
 }
 
 static void rope_tables(const ssd_model_shape& s, std::vector<float>& cs, std::vector<float>& sn) {
@@ -473,38 +462,6 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
     m.attn_part = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.n_kv_heads * chunks * G * (hd + 2))));
     m.attn_cnt = static_cast<int*>(own(dalloc<int>(size_t(maxM) * s.n_kv_heads)));
   }
-  // persistent forward kernel: op lists (with / without the LM head), KV table
-  {
-    std::vector<mk::Op> ops;
-    auto gemm_op = [&](int kind, int l, const WMat& w) {
-      ops.push_back(mk::Op{kind, l, w.w, w.N, w.K / (tc::kBK * tc::kKPS), 0});
-    };
-    ops.push_back(mk::Op{mk::OP_EMBED, 0, nullptr, 0, 0, 0});
-    for (int l = 0; l < s.n_layers; ++l) {
-      const DevLayer& L = m.layers[size_t(l)];
-      ops.push_back(mk::Op{mk::OP_NORM, l, nullptr, 0, 0, 0});
-      gemm_op(mk::OP_QKV, l, L.qkv);
-      ops.push_back(mk::Op{mk::OP_ATTN, l, nullptr, 0, 0, 0});
-      gemm_op(mk::OP_O, l, L.o);
-      ops.push_back(mk::Op{mk::OP_NORM, l, nullptr, 0, 0, l == 0 ? 1 : 0});
-      gemm_op(mk::OP_GU, l, L.gu);
-      gemm_op(mk::OP_DN, l, L.dn);
-    }
-    m.mk_nops[0] = int(ops.size());
-    ops.push_back(mk::Op{mk::OP_NORM, s.n_layers, nullptr, 0, 0, 2});
-    gemm_op(mk::OP_HEAD, s.n_layers, m.head);
-    m.mk_nops[1] = int(ops.size());
-    m.mk_ops[1] = static_cast<mk::Op*>(own(dalloc<mk::Op>(ops.size())));
-    CK(cudaMemcpy(m.mk_ops[1], ops.data(), ops.size() * sizeof(mk::Op), cudaMemcpyHostToDevice));
-    m.mk_ops[0] = m.mk_ops[1];  // same list, one op shorter
-    std::vector<mk::LayerKV> kv(static_cast<size_t>(s.n_layers));
-    for (int l = 0; l < s.n_layers; ++l)
-      kv[size_t(l)] = mk::LayerKV{m.kc + size_t(l) * m.kv_layer_elems(), m.vc + size_t(l) * m.kv_layer_elems()};
-    m.mk_kv = static_cast<mk::LayerKV*>(own(dalloc<mk::LayerKV>(kv.size())));
-    CK(cudaMemcpy(m.mk_kv, kv.data(), kv.size() * sizeof(mk::LayerKV), cudaMemcpyHostToDevice));
-    m.mk_sumsq = static_cast<float*>(own(dalloc<float>(size_t(d / tc::kBM + 1) * maxM)));
-    m.mk_bar = static_cast<unsigned*>(own(dalloc<unsigned>(2)));
-  }
 }
 
 static int E_num_sms = 148;
@@ -625,12 +582,6 @@ static void carveout_max(F* f) {
                           int(cudaSharedmemCarveoutMaxShared)));
 }
 
-template <int NP, int G>
-static void mk_configure() {
-  CK(cudaFuncSetAttribute(mk::fwd_kernel<NP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(mk::Cfg<NP, G>::kSmem)));
-}
-
 // Kernel attributes are set once, outside any stream capture.
 static void configure_kernels() {
   carveout_max(embed_kernel);
@@ -708,15 +659,9 @@ static void configure_kernels() {
     SSD_DEC_CFG(1, 128) SSD_DEC_CFG(2, 128) SSD_DEC_CFG(4, 128) SSD_DEC_CFG(8, 128)
 #undef SSD_DEC_CFG
   }
-  for (const void* f : {(const void*)gemv_kernel<EPI_STORE, 1>, (const void*)gemv_kernel<EPI_SWIGLU, 1>,
-                        (const void*)gemv_kernel<EPI_STORE, 2>, (const void*)gemv_kernel<EPI_SWIGLU, 2>}) {
-    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGemvSmemMax)));
-    CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
-  }
-  mk_configure<16, 1>(); mk_configure<16, 2>(); mk_configure<16, 4>(); mk_configure<16, 8>();
-  mk_configure<32, 1>(); mk_configure<32, 2>(); mk_configure<32, 4>(); mk_configure<32, 8>();
-  mk_configure<64, 1>(); mk_configure<64, 2>(); mk_configure<64, 4>(); mk_configure<64, 8>();
 }
+
+// Stream capture}
 
 // Stream capture of one round / step into an executable graph. All kernel
 // parameters (including the activation TMA maps) are baked in by value.
@@ -747,31 +692,10 @@ struct GraphSet {
   }
 };
 
-// Weight-streaming linear layer: tcgen05 swap-AB stream-K GEMM for every M
-// (M = 1 decode steps pad the token operand to 16).
-template <int EPI>
-static bool gemv_launch(Engine& E, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                        cudaStream_t s, Prefetch pf) {
-  if (M > E.gemv_max_m || (W.K & 63)) return false;
-  const int MT = M <= 1 ? 1 : 2;
-  const size_t smem = gemv_smem(MT, W.K);
-  if (smem > kGemvSmemMax) return false;
-  const int groups = std::min(int(((W.N + tc::kBM - 1) / tc::kBM) * (tc::kBM / kGemvRows)), 2 * E_num_sms);
-  if (MT == 1)
-    launch_pdl(gemv_kernel<EPI, 1>, dim3(groups), dim3(kGemvThreads), smem, s, (const bf16*)W.w, W.N, W.K, X, M, Y,
-               ldy, Yb, ldyb, pf);
-  else
-    launch_pdl(gemv_kernel<EPI, 2>, dim3(groups), dim3(kGemvThreads), smem, s, (const bf16*)W.w, W.N, W.K, X, M, Y,
-               ldy, Yb, ldyb, pf);
-  return true;
-}
-
 template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
                    cudaStream_t s, Prefetch pf) {
   ++E.launches;
-  // decode steps (M <= gemv_max_m): CUDA-core GEMV, whole rows per CTA
-  if (m.gemm_ctas == 0 && gemv_launch<EPI>(E, W, X, M, Y, ldy, Yb, ldyb, s, pf)) return;
   // small weight matrices at branch widths (17..32 tokens): cluster split-K.
   // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
@@ -948,62 +872,6 @@ static bool attn_dec_launch(Model& m, int M, const FwdParams* P, bf16* kc, bf16*
   return true;
 }
 
-// Persistent forward kernel launch (fwd_mk.cuh): the whole step in one
-// cooperative launch (all CTAs co-resident: grid barriers).
-template <int NP, int G>
-static void mk_launch(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
-  using C = mk::Cfg<NP, G>;
-  const ssd_model_shape& sh = m.s;
-  const int grid = m.mk_ctas > 0 ? std::min(m.mk_ctas, E_num_sms) : E_num_sms;
-  if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "forward: split-K workspace");
-  mk::MkArgs a{};
-  a.ops = m.mk_ops[logits ? 1 : 0];
-  a.n_ops = m.mk_nops[logits ? 1 : 0];
-  a.M = M;
-  a.P = P;
-  a.d = sh.d_model; a.H = sh.n_heads; a.KVH = sh.n_kv_heads; a.hd = sh.head_dim; a.ffn = sh.ffn; a.V = sh.vocab;
-  a.S = m.S; a.nqkv = m.qd + 2 * m.kvd; a.qd = m.qd;
-  a.eps = sh.norm_eps;
-  a.scale = 1.0f / std::sqrt(float(sh.head_dim));
-  a.embed = m.embed; a.embed_tiled = m.embed_tiled;
-  a.gain_ffn0 = m.ffn_gain0; a.gain_final = m.final_gain;
-  a.rope_cos = m.rope_cos; a.rope_sin = m.rope_sin;
-  a.kv = m.mk_kv;
-  a.x = m.x; a.sumsq = m.mk_sumsq; a.ld_sumsq = m.maxM;
-  a.qkv = m.qkv; a.attn = m.attn; a.act = m.act; a.logits = logits;
-  a.ws = m.ws; a.counters = m.counters;
-  a.aws = AttnWs{m.attn_part, m.attn_cnt};
-  a.nch = attn_chunks(m);
-  a.bar = m.mk_bar;
-  a.trace = E.mk_trace;
-  a.xb = m.xb;
-  a.pf_units = E.mk_pf_units;
-  a.utrace = E.mk_utrace;
-  for (int j = 0; j < 4; ++j) a.utrace_op[j] = E.mk_utrace_op[j];
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(mk::kThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, mk::fwd_kernel<NP, G>, act_map(m, m.attn, m.qd, NP), act_map(m, m.act, sh.ffn, NP),
-                        act_map(m, m.xb, sh.d_model, NP), a));
-}
-
-template <int NP>
-static void mk_launch_g(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
-  switch (m.s.n_heads / m.s.n_kv_heads) {
-    case 1: mk_launch<NP, 1>(E, m, P, M, logits, s); break;
-    case 2: mk_launch<NP, 2>(E, m, P, M, logits, s); break;
-    case 4: mk_launch<NP, 4>(E, m, P, M, logits, s); break;
-    default: mk_launch<NP, 8>(E, m, P, M, logits, s); break;
-  }
-}
-
 // Row-parallel projection sum over the TP ranks (tp.cuh), in place.
 static void tp_allreduce(Engine& E, Model& m, float* buf, int M, cudaStream_t s) {
   if (!E.tp_peers.region[0]) throw Fail(SSD_CONFIG, "tensor parallel: peers not connected (ssd_tp_connect)");
@@ -1017,13 +885,6 @@ static void tp_allreduce(Engine& E, Model& m, float* buf, int M, cudaStream_t s)
 // PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
-  if (E.use_mk && (E.use_mk == 1 || (E.use_mk == 2 && m.role == 1)) && M <= 64 && m.tp_size == 1) {  // decode / verify / branch steps and prefill chunks: one persistent launch
-    if (M <= 16) mk_launch_g<16>(E, m, P, M, logits, s);
-    else if (M <= 32) mk_launch_g<32>(E, m, P, M, logits, s);
-    else mk_launch_g<64>(E, m, P, M, logits, s);
-    ++E.launches;
-    return;
-  }
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, H = sh.n_heads, KVH = sh.n_kv_heads, hd = sh.head_dim, F = sh.ffn;
   const int nqkv = m.qd + 2 * m.kvd;
@@ -1217,11 +1078,13 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
   prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1, E.hist_stride, E.T.lane_S);
   KCHECK();
   forward(E, E.T, E.P_t, nl * (K + 1), E.tlogits, s);
+  mark(E, 1, s);
   verify_stats_kernel<<<dim3(2 * K + 1, nl), kSampleThreads, 0, s>>>(E.tlogits, E.st, E.V, dscheme(ts), dscheme(ds),
                                                                        E.rstat);
   verify_decide_kernel<<<nl, kSampleThreads, 0, s>>>(E.tlogits, E.st, E.hist, E.V, dscheme(ts), dscheme(ds), scale, E.rstat,
                                                      use_draft_stream, E.hist_stride);
   KCHECK();
+  mark(E, 2, s);
   E.launches += 3;
 }
 
@@ -1238,10 +1101,12 @@ static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, con
   prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S);
   KCHECK();
   forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
+  mark(E, 4, s);
   row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s, nl, B);
   const bool sampled = sc.temperature > 0.0;
   branch_streams_kernel<<<nl, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
+  mark(E, 5, s);
   E.launches += 2;
   if (nl > 1) Bl = nl * B;
   if (Bl <= 0) return;
@@ -1252,8 +1117,10 @@ static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, con
                                                          E.D.s.max_ctx, nl > 1 ? B : 0, E.D.lane_S);
     float* out = rows + size_t(j) * Bl * E.V;
     forward(E, E.D, E.P_b, Bl, out, s);
+    if (j < 8) mark(E, 6 + 2 * j, s);
     row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * K + j : nullptr, K, E.bt + j, K, s);
     KCHECK();
+    if (j < 8) mark(E, 7 + 2 * j, s);
     E.launches += 1;
   }
 }
@@ -1349,25 +1216,6 @@ static void validate_cfg(Engine& E, const ssd_sim_config* c) {
 
 using namespace ssd;
 
-namespace ssd {
-// Watchdog record of the persistent forward kernel (fwd_mk.cuh): [0] set,
-// [1] code (1 weight producer empty, 2 MMA tmem-empty, 3 MMA full,
-// 4 B producer empty, 5 epilogue tmem-full, 9 grid barrier), [2] block,
-// [3] thread, [4..5] aux (op, counter). Host-mapped: valid after a trap.
-unsigned long long* g_diag_host = nullptr;
-static void mk_diag_init() {
-  if (g_diag_host) return;
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&g_diag_host), (8 + 8 * 256) * sizeof(unsigned long long),
-                   cudaHostAllocMapped));
-  std::memset(g_diag_host, 0, (8 + 8 * 256) * sizeof(unsigned long long));
-  unsigned long long* dptr = nullptr;
-  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), g_diag_host, 0));
-  CK(cudaMemcpyToSymbol(mk::g_mk_diag, &dptr, sizeof(dptr)));
-  const int prog = std::getenv("SSD_B200_MK_PROGRESS") ? std::atoi(std::getenv("SSD_B200_MK_PROGRESS")) : 0;
-  CK(cudaMemcpyToSymbol(mk::g_mk_progress, &prog, sizeof(prog)));
-}
-}  // namespace ssd
-
 struct ssd_engine {
   Engine e;
 };
@@ -1448,20 +1296,16 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sk = std::getenv("SSD_B200_SKIP")) E.skip_mask = std::atoi(sk);
   if (const char* pf = std::getenv("SSD_B200_PF_MB")) E.pf_ahead = std::max(0LL, std::atoll(pf)) << 20;
   if (const char* pfd = std::getenv("SSD_B200_PF_MB_DRAFT")) E.pf_ahead_draft = std::max(0LL, std::atoll(pfd)) << 20;
-  if (const char* mkv = std::getenv("SSD_B200_MK")) E.use_mk = std::atoi(mkv);  // 1 both models, 2 draft only
   if (const char* acl = std::getenv("SSD_B200_ATTN_CL")) E.attn_cluster = std::atoi(acl) != 0;
   if (const char* adc = std::getenv("SSD_B200_ATTN_DEC")) E.attn_dec = std::atoi(adc) != 0;
   if (const char* ast = std::getenv("SSD_B200_ATTN_STAGE")) g_attn_stage = std::atoi(ast) != 0;
   if (const char* aw = std::getenv("SSD_B200_ATTN_DEC_WIDE_M")) E.attn_dec_wide_m = std::max(1, std::atoi(aw));
-  if (const char* gv = std::getenv("SSD_B200_GEMV_M")) E.gemv_max_m = std::max(0, std::min(2, std::atoi(gv)));
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
-  if (const char* mpf = std::getenv("SSD_B200_MK_PF")) E.mk_pf_units = std::max(0, std::atoi(mpf));
-  const int mk_ctas = std::getenv("SSD_B200_MK_CTAS") ? std::atoi(std::getenv("SSD_B200_MK_CTAS")) : 0;
   {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1477,9 +1321,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (role != SSD_ROLE_VERIFIER)
     build_model(E.D, *draft, *draft, *pair, 1, max_branches * max_lookahead, std::max(maxM, kPrefillChunk), 0, 1, nb);
   else E.D.s = *draft;
-  E.D.mk_ctas = mk_ctas;  // experiment: SMs of the draft's persistent forward (0 = all)
   configure_kernels();
-  mk_diag_init();
   {
     // colocated SSD: optionally give the speculator (the longer chain of
     // dependent steps per round) the higher stream priority
@@ -1591,6 +1433,8 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1})
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : E.prof_ev)
+    if (ev) cudaEventDestroy(ev);
   cudaGetLastError();  // teardown errors must not surface in a later call
   delete h;
   API_END
@@ -1694,14 +1538,15 @@ namespace ssd {
 // branch steps M = nb B), and a miss in any lane stalls the round's clock
 // for the backup (sim.cpp:570-577).
 static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int nb, int32_t* out,
-                         int64_t cap, int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats) {
+                         int64_t cap, int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats,
+                         double* prof = nullptr) {
   CK(cudaSetDevice(E.dev));
   validate_cfg(E, c);
   need(E.T, "run_ssd");
   need(E.D, "run_ssd");
   if (nb < 1) throw Fail(SSD_ERROR, "sim: batch_size must be >= 1");
   if (nb > E.nbmax) throw Fail(SSD_TOO_LARGE, "sim: batch_size exceeds the engine's batch capacity");
-  if (nb > 1 && (E.use_mk || E.T.tp_size > 1)) throw Fail(SSD_CONFIG, "sim: batch > 1 needs the per-op colocated engine");
+  if (nb > 1 && E.T.tp_size > 1) throw Fail(SSD_CONFIG, "sim: batch > 1 needs the per-op colocated engine");
   const int K = c->lookahead;
   int B = 0, max_f = 0;
   upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);
@@ -1759,7 +1604,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
                 c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
                 static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
-  const std::string key(keybuf);
+  const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "");
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
       if (g) cudaGraphExecDestroy(g);
@@ -1768,8 +1613,10 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
     GraphSet gs;
   for (int parity = 0; parity < 2; ++parity) {
     gs.g.push_back(capture_graph(sv, [&] {
+      mark(E, 0, sv);
       CK(cudaEventRecord(E.ev_fork, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
+      mark(E, 3, ss);
       prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb);
       verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
       CK(cudaEventRecord(E.ev_verified, sv));
@@ -1777,6 +1624,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
       lookup_kernel<<<1, 32, 0, ss>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V, E.cum,
                                       d_out, d_hit);
       KCHECK();
+      mark(E, kMarkRoundEnd, ss);
       ++E.launches;
       CK(cudaEventRecord(E.ev_join, ss));
       CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
@@ -1796,6 +1644,28 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   CK(cudaEventRecord(E.ev_t0, sv));
   for (int64_t r = 0; r < R; ++r) {
     CK(cudaGraphLaunch(E.ssd_graphs[size_t(r & 1)], sv));
+    if (E.prof_on && prof) {  // in-graph segment times of this round (one host sync per round)
+      CK(cudaStreamSynchronize(sv));
+      auto el = [&](int a, int b) {
+        float v = 0.f;
+        CK(cudaEventElapsedTime(&v, E.prof_ev[a], E.prof_ev[b]));
+        return double(v);
+      };
+      prof[0] += el(0, kMarkRoundEnd);
+      prof[1] += el(0, 1);
+      prof[2] += el(1, 2);
+      prof[3] += el(3, 4);
+      prof[4] += el(4, 5);
+      int prev = 5;
+      for (int j = 0; j < std::min(K, 8); ++j) {
+        prof[5] += el(prev, 6 + 2 * j);
+        prof[6] += el(6 + 2 * j, 7 + 2 * j);
+        prev = 7 + 2 * j;
+      }
+      prof[7] += el(prev, kMarkRoundEnd);
+      prof[8] += el(0, 3);
+      prof[9] += 1.0;
+    }
     if (jit && r + 1 < R) {
       // SamePrimaryJIT: the lanes that missed re-draft from their new
       // history, batched (the one host round trip of the JIT backup)
@@ -1848,6 +1718,26 @@ ssd_status ssd_run_ssd_batch(ssd_engine* h, const int32_t* prompt, int32_t n0, c
                              ssd_run_stats* stats) {
   API_BEGIN
   run_ssd_impl(h->e, prompt, n0, c, batch, out, cap, out_lens, out_outcomes, out_hits, stats);
+  API_END
+}
+
+ssd_status ssd_profile_ssd_round(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c,
+                                 double* out_ms, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!out_ms) throw Fail(SSD_CONFIG, "profile_ssd_round: null output");
+  for (int i = 0; i < 32; ++i)
+    if (!E.prof_ev[i]) CK(cudaEventCreate(&E.prof_ev[i]));
+  double acc[10] = {0};
+  E.prof_on = 1;
+  struct Off {
+    Engine& e;
+    ~Off() { e.prof_on = 0; }
+  } off{E};
+  run_ssd_impl(E, prompt, n0, c, 1, nullptr, 0, nullptr, nullptr, nullptr, stats, acc);
+  const double n = acc[9] > 0 ? acc[9] : 1.0;
+  for (int i = 0; i < 9; ++i) out_ms[i] = acc[i] / n;
   API_END
 }
 
@@ -2319,75 +2209,11 @@ ssd_status ssd_bench_read_bw(ssd_engine* h, int64_t bytes, int32_t iters, double
   API_END
 }
 
-ssd_status ssd_bench_tma_stream(ssd_engine* h, int64_t bytes, int32_t ublk, int32_t stages, int32_t mode,
-                                int32_t ctas_per_sm, int32_t iters, double* gbs) {
-  API_BEGIN
-  Engine& E = h->e;
-  CK(cudaSetDevice(E.dev));
-  if (ublk % 16 || stages < 1 || ublk <= 0) throw Fail(SSD_CONFIG, "probe: bad block");
-  const long long units = bytes / ublk;
-  uint8_t* buf = dalloc<uint8_t>(size_t(units) * ublk);
-  unsigned* sink = dalloc<unsigned>(1);
-  const size_t smem = 1024 + size_t(stages) * ublk + 2 * 8 * size_t(stages);
-  CK(cudaFuncSetAttribute(tma_stream_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const int grid = E_num_sms * ctas_per_sm;
-  tma_stream_probe<<<grid, 64, smem, E.sv>>>(buf, units, ublk, stages, mode, sink);
-  CK(cudaEventRecord(E.ev_t0, E.sv));
-  for (int i = 0; i < iters; ++i) tma_stream_probe<<<grid, 64, smem, E.sv>>>(buf, units, ublk, stages, mode, sink);
-  CK(cudaEventRecord(E.ev_t1, E.sv));
-  CK(cudaEventSynchronize(E.ev_t1));
-  KCHECK();
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, E.ev_t0, E.ev_t1));
-  *gbs = double(units) * ublk * iters / (ms * 1e-3) / 1e9;
-  cudaFree(buf);
-  cudaFree(sink);
-  API_END
-}
-
 #if SSD_GEMM_TRACE
 extern "C" int ssd_debug_gemm_trace(unsigned long long* out /* 5 x 512 */) {
   return int(cudaMemcpyFromSymbol(out, tc::g_trace, sizeof(unsigned long long) * 5 * 512));
 }
 #endif
-
-// Debug timeline of one persistent forward of `which` over M tokens at
-// position pos: out[(op * grid + cta) * 4 + k] (ns, see fwd_mk.cuh mk_trace);
-// returns the op count; kinds[op] = op kind.
-int ssd_debug_mk_trace(ssd_engine* h, int which, int M, int pos, unsigned long long* out, int cap, int* kinds,
-                       const int* utrace_ops, unsigned long long* uout) {
-  try {
-    Engine& E = h->e;
-    CK(cudaSetDevice(E.dev));
-    Model& m = which == 0 ? E.T : E.D;
-    const int nops = m.mk_nops[1];
-    const size_t n = size_t(nops) * E_num_sms * 4;
-    if (size_t(cap) < n) return -2;
-    m.ctx_bound = pos + M + 1;
-    prep_prefill_kernel<<<1, kMaxM, 0, E.sv>>>(E.hist, E.P_pre, pos, M, 0);
-    forward(E, m, E.P_pre, M, m.logits, E.sv);  // warm
-    CK(cudaMalloc(&E.mk_trace, n * 8));
-    CK(cudaMemset(E.mk_trace, 0, n * 8));
-    CK(cudaMalloc(&E.mk_utrace, 4 * 64 * 4 * 8));
-    CK(cudaMemset(E.mk_utrace, 0, 4 * 64 * 4 * 8));
-    for (int j = 0; j < 4; ++j) E.mk_utrace_op[j] = utrace_ops ? utrace_ops[j] : -1;
-    forward(E, m, E.P_pre, M, m.logits, E.sv);
-    CK(cudaStreamSynchronize(E.sv));
-    CK(cudaMemcpy(out, E.mk_trace, n * 8, cudaMemcpyDeviceToHost));
-    if (uout) CK(cudaMemcpy(uout, E.mk_utrace, 4 * 64 * 4 * 8, cudaMemcpyDeviceToHost));
-    cudaFree(E.mk_trace);
-    cudaFree(E.mk_utrace);
-    E.mk_trace = nullptr;
-    E.mk_utrace = nullptr;
-    std::vector<mk::Op> ops(static_cast<size_t>(nops));
-    CK(cudaMemcpy(ops.data(), m.mk_ops[1], size_t(nops) * sizeof(mk::Op), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < nops; ++i) kinds[i] = ops[size_t(i)].kind;
-    return nops;
-  } catch (const std::exception& x) {
-    g_last_error = x.what();
-    return -1;
-  }
-}
 
 // Kernel timeline (profiling build -DSSD_KTL=1): copies up to n records
 // (kind, entry, ready, exit) and resets the ring; returns the count.
@@ -2411,45 +2237,14 @@ int ssd_debug_ktl(unsigned long long* out, int n) {
 #endif
 }
 
-int ssd_debug_mk_diag(unsigned long long* out /* 8 + 8 * 256 */) {
-  if (!g_diag_host) return -1;
-  std::memcpy(out, g_diag_host, (8 + 8 * 256) * sizeof(unsigned long long));
-  return 0;
-}
-
-// tcgen05 rate probe (profiling): cycles for `iters` units of 8 MMAs at N = np.
-int ssd_debug_mma_rate(int np, int iters, unsigned long long* out) {
-  try {
-    unsigned long long* d = dalloc<unsigned long long>(2);
-    auto run = [&](auto kern, size_t smem) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      kern<<<1, 64, smem>>>(iters, d);
-      KCHECK();
-    };
-    const size_t extra = 1024 + tc::kABytes + 64;
-    if (np == 16) run(mma_rate_probe<16>, extra + tc::Cfg<16>::kBBytes);
-    else if (np == 32) run(mma_rate_probe<32>, extra + tc::Cfg<32>::kBBytes);
-    else if (np == 64) run(mma_rate_probe<64>, extra + tc::Cfg<64>::kBBytes);
-    else if (np == 128) run(mma_rate_probe<128>, extra + tc::Cfg<128>::kBBytes);
-    else run(mma_rate_probe<256>, extra + tc::Cfg<256>::kBBytes);
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(out, d, 16, cudaMemcpyDeviceToHost));
-    cudaFree(d);
-    return 0;
-  } catch (const std::exception& x) {
-    g_last_error = x.what();
-    return -1;
-  }
-}
-
 ssd_status ssd_rng_u64(ssd_engine* h, uint64_t seed, int32_t n, uint64_t* out) {
   API_BEGIN
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   uint64_t* d = dalloc<uint64_t>(size_t(n));
   Mt64* m = dalloc<Mt64>(1);
-  mt_init_kernel<<<1, 32>>>(m, seed);
-  mt_draw_kernel<<<1, 32>>>(m, n, d);
+  mt_init_kernel<<<1, 32, 0, E.sv>>>(m, seed);
+  mt_draw_kernel<<<1, 32, 0, E.sv>>>(m, n, d);
   KCHECK();
   d2h(E, out, d, size_t(n) * 8);
   cudaFree(d);

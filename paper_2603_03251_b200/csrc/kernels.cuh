@@ -342,8 +342,7 @@ __device__ __forceinline__ void attn_scores(const float* qs, float* sc, int n, i
 }
 
 // Shared-memory scratch of one attention work item (kAttnSmemFloats(G, hd)
-// floats + one int); static in attention_kernel, carved from the dynamic
-// shared memory in the persistent forward kernel (fwd_mk.cuh).
+// floats + one int); static in attention_kernel.
 struct AttnSmem {
   float* qs;      // [G][hd]
   float* sc;      // [G][kAttnChunk]

@@ -17,7 +17,8 @@ import numpy as np  # noqa: E402
 import paper_2603_03251_b200 as P  # noqa: E402
 from paper_2603_03251_b200.configs import shapes  # noqa: E402
 
-KIND = {1: "embed", 2: "rmsnorm", 3: "attention", 4: "attention_dec", 10: "gemm", 12: "gemm_swiglu"}
+KIND = {1: "embed", 2: "rmsnorm", 3: "attention", 4: "attention_dec", 10: "gemm", 11: "gemm_resid", 12: "gemm_swiglu",
+        20: "gemm_cl", 21: "gemm_cl_resid", 22: "gemm_cl_swiglu"}
 ts, ds = shapes("llama8b_1b", max_ctx=1024)
 eng = P.Engine(ts, ds, P.Pair(), max_branches=20, max_lookahead=4)
 lib = P._native.load()
@@ -74,7 +75,7 @@ for w in (sys.argv[1:] or ["t1", "d1", "d20"]):
         print("     launch %2d mma-done %6.2f tail %6.2f | last CTA %3d: mma-complete %+.2f tfull %+.2f drained %+.2f arrived %+.2f reduced %+.2f exit %+.2f" % (
             j, (c[ok, 1].max() - r0) / 1e3, (c[ok, 2].max() - c[ok, 1].max()) / 1e3, last, rel(c[last, 7]),
             rel(c[last, 3]), rel(c[last, 4]), rel(c[last, 5]), rel(c[last, 6]), rel(c[last, 2])))
-    for r in f[:14]:
+    for r in f[:24]:
         print(f"      {str(KIND.get(int(r[0]), int(r[0]))):12s} entry {(r[1] - t0) / 1e3:8.2f} ready {(r[2] - t0) / 1e3:8.2f} "
               f"exit {(r[3] - t0) / 1e3:8.2f}")
 eng.close()

@@ -15,6 +15,33 @@ LOGIT_TOL = 1e-2   # |GPU - oracle| logit bar (bf16 weights, fp32 accumulation o
 NEAR_TIE = 1e-2    # an argmax flip is accepted only when the oracle's top-2 gap is below this
 
 
+NOISE_FACTOR = 3.0  # GPU deviation allowed, in units of the fp32 oracle's own deviation
+
+
+def logit_noise_check(get_gpu, orc32, orc64, which: int, contexts) -> dict:
+    """Logits against the fp64-accumulating oracle (same bf16 rounding
+    points), with the fp32 oracle's own deviation from it as the noise floor.
+
+    At the 8B/1B shapes an fp32 forward is NOT reproducible to 1e-2: a
+    different fp32 summation order flips bf16 roundings of activations and
+    moves logits by up to ~0.09 (measured: oracle fp32 vs fp64 on the
+    2-layer 8B-shaped model, max 0.04-0.09, rms 0.010-0.019). So the bar is:
+    the GPU's max / rms deviation from fp64, pooled over the contexts, is
+    within NOISE_FACTOR x the fp32 oracle's (floor LOGIT_TOL / 1e-3). A real
+    kernel bug (wrong head, mask, RoPE or tile) moves logits by O(1)."""
+    g_max = g_rms = n_max = n_rms = 0.0
+    for ctx in contexts:
+        ref = orc64.logits(which, ctx).astype(np.float64)
+        g = get_gpu(which, ctx).astype(np.float64) - ref
+        o = orc32.logits(which, ctx).astype(np.float64) - ref
+        g_max, n_max = max(g_max, float(np.abs(g).max())), max(n_max, float(np.abs(o).max()))
+        g_rms, n_rms = max(g_rms, float(np.sqrt((g * g).mean()))), max(n_rms, float(np.sqrt((o * o).mean())))
+    out = {"gpu_max": g_max, "gpu_rms": g_rms, "noise_max": n_max, "noise_rms": n_rms}
+    assert g_max <= max(LOGIT_TOL, NOISE_FACTOR * n_max), out
+    assert g_rms <= max(1e-3, NOISE_FACTOR * n_rms), out
+    return out
+
+
 def first_divergence(a, b):
     for i, (x, y) in enumerate(zip(a, b)):
         if x != y:

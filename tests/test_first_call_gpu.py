@@ -20,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WAVES, PER_WAVE = 6, 4
+CORRUPT_TOL = 0.1
 
 
 def _prompt(i):
@@ -83,7 +84,9 @@ def test_first_call_of_fresh_processes_is_exact(oracle_lib):
                 o = orc.call({"op": "simulate", "mode": "harness", "lookahead": 4, "rounds": 4, "seed": 3,
                               "prompt": _prompt(i), "scheme": {"temperature": 0.0}, "primary_plan": {"fan": [4] * 5},
                               "backup_plan": {"fan": [4] * 5}, "timing": {"primary_time": 0.4}})
-                if err >= 1e-2 or list(st) != o["streams"][0]:
+                # corruption (a stale history / plan) moves logits by O(1-10);
+                # fp32 summation-order noise of the tiny pair is ~1e-2
+                if err >= CORRUPT_TOL or list(st) != o["streams"][0]:
                     bad.append((i, err, list(st)[:6], o["streams"][0][:6]))
     finally:
         stop.set()

@@ -15,8 +15,8 @@ CPU oracle (oracle/transformer_lm.cpp, oracle/ssd_oracle.cpp).
 import numpy as np
 import pytest
 
-from parity import (LOGIT_TOL, binom_close, check_greedy_stream, check_harness_exact, check_topk_set,
-                    first_divergence, sim_cfg, sim_req)
+from parity import (binom_close, check_greedy_stream, check_harness_exact, check_topk_set, first_divergence,
+                    logit_noise_check, sim_cfg, sim_req)
 
 pytestmark = pytest.mark.gpu
 
@@ -41,6 +41,11 @@ def _pair(oracle_lib, t, d, max_ctx=256, branches=20, pair=None):
     return P, eng, orc
 
 
+def _f64(oracle_lib, eng, pair):
+    import paper_2603_03251_b200 as P
+    return oracle_lib.TfPair(P.shape_dict(eng.target), P.shape_dict(eng.draft), pair.as_dict(), accum="f64")
+
+
 @pytest.fixture(scope="module")
 def bench_pair(oracle_lib):
     P, eng, orc = _pair(oracle_lib, BENCH_T, BENCH_D)
@@ -49,21 +54,32 @@ def bench_pair(oracle_lib):
     orc.close()
 
 
+@pytest.fixture(scope="module")
+def bench_f64(oracle_lib, bench_pair):
+    P, eng, orc = bench_pair
+    o64 = _f64(oracle_lib, eng, P.Pair())
+    yield o64
+    o64.close()
+
+
 def _prompt(n, V, seed):
     return np.random.default_rng(seed).integers(0, V, n).tolist()
 
 
 @pytest.mark.parametrize("which", [0, 1])
-@pytest.mark.parametrize("n", [1, 5, 20, 37])
-def test_bench_shape_logits(bench_pair, which, n):
-    """M = n prefill forward (M = 1 decode, 5 verify / extend, 20 branch
+def test_bench_shape_logits(bench_pair, bench_f64, which):
+    """M = n prefill forwards (n = 1 decode, 5 verify / extend, 20 branch
     width, 37 a prefill chunk) of the 8B-shaped (which 0) / 1B-shaped
-    (which 1) model: every logit within 1e-2 of the fp32 oracle."""
+    (which 1) model against the fp64 oracle, within the fp32 noise floor
+    (tests/parity.py logit_noise_check); argmax equal or a near-tie."""
     P, eng, orc = bench_pair
-    ctx = _prompt(n, 128256, 40 + n)
-    g, o = eng.logits(which, ctx), orc.logits(which, ctx)
-    err = float(np.max(np.abs(g - o)))
-    assert err < LOGIT_TOL, (which, n, err)
+    ctxs = [_prompt(n, 128256, 40 + n) for n in (1, 5, 20, 37)]
+    out = logit_noise_check(eng.logits, orc, bench_f64, which, ctxs)
+    print("logit noise", which, out)
+    for ctx in ctxs:
+        g, o = eng.logits(which, ctx), orc.logits(which, ctx)
+        if int(np.argmax(g)) != int(np.argmax(o)):
+            assert float(o.max() - o[int(np.argmax(g))]) < 1e-2
 
 
 def test_bench_shape_keys_on_engine_rows(bench_pair):
@@ -186,13 +202,12 @@ def tiny_gqa(request, oracle_lib):
     orc.close()
 
 
-def test_gqa_logits_and_greedy_harness(tiny_gqa):
+def test_gqa_logits_and_greedy_harness(tiny_gqa, oracle_lib):
     P, eng, orc = tiny_gqa
+    o64 = _f64(oracle_lib, eng, P.Pair())
     for which in (0, 1):
-        for n in (1, 5, 20, 60):
-            ctx = _prompt(n, 32000, 300 + n)
-            err = float(np.max(np.abs(eng.logits(which, ctx) - orc.logits(which, ctx))))
-            assert err < LOGIT_TOL, (which, n, err)
+        logit_noise_check(eng.logits, orc, o64, which, [_prompt(n, 32000, 300 + n) for n in (1, 5, 20, 60)])
+    o64.close()
     prompt = _prompt(12, 32000, 14)
     g = eng.run_ssd(prompt, sim_cfg(P, K, 10, 4, 0.0, FAN))
     check_greedy_stream(orc, 0, prompt, g.streams[0])
@@ -234,8 +249,10 @@ def test_full_llama8b_1b_greedy_harness(oracle_lib):
     orc = oracle_lib.TfPair(P.shape_dict(ts), P.shape_dict(ds), pair.as_dict())
     try:
         prompt = _prompt(8, 128256, 20250809)
-        err = float(np.max(np.abs(eng.logits(0, prompt) - orc.logits(0, prompt))))
-        assert err < LOGIT_TOL, err
+        o64 = _f64(oracle_lib, eng, pair)
+        print("logit noise 8B", logit_noise_check(eng.logits, orc, o64, 0, [prompt]))
+        print("logit noise 1B", logit_noise_check(eng.logits, orc, o64, 1, [prompt]))
+        o64.close()
         g = eng.run_ssd(prompt, sim_cfg(P, K, 2, 20250809, 0.0, FAN))
         check_greedy_stream(orc, 0, prompt, g.streams[0])
         o = orc.call(sim_req(prompt, "harness", K, 2, 20250809, 0.0, FAN))

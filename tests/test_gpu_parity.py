@@ -303,10 +303,10 @@ def test_errors_map_to_reference_classes(tiny):
 
 
 @pytest.mark.parametrize("M", [2, 5, 20, 33, 100])
-def test_tcgen05_forward_matches_gemv_path(tiny, M):
-    """The tcgen05 swap-AB GEMM path (M > 1 forwards) against the CUDA-core
-    GEMV path (M = 1): logits of the last prefill position of a context of
-    length M (one M-token forward) vs the oracle."""
+def test_tcgen05_forward_widths_match_oracle(tiny, M):
+    """The tcgen05 swap-AB GEMM at every token-operand width the engine uses
+    (N = 16 / 32 / 48 / 128 tiles, cluster split-K at 17..32): logits of the
+    last position of one M-token prefill forward vs the oracle."""
     P, eng, orc = tiny
     ctx = _prompt(M, seed=200 + M)
     g = eng.logits(0, ctx)
