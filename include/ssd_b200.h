@@ -222,6 +222,26 @@ ssd_status ssd_run_ssd_batch(ssd_engine* e, const int32_t* prompt, int32_t promp
                              const ssd_sim_config* cfg, int32_t batch, int32_t* out_tokens,
                              int64_t out_capacity, int64_t* out_lens, int32_t* out_outcomes,
                              int32_t* out_hits, ssd_run_stats* stats);
+/* Loop semantics and the round transcript (ssd_run_ssd_ex). */
+enum { SSD_SEMANTICS_HARNESS = 0,    /* sim::run_protocol_harness (sim.cpp:502-601): verifier and
+                                        draft streams, cache built while verifying */
+       SSD_SEMANTICS_SEQUENTIAL = 1  /* sim::run_ssd / run_ssd_batch (sim.cpp:123-250): one stream per
+                                        sequence; verify, then build_cache, then the backup */ };
+typedef struct ssd_run_options {
+  int32_t semantics;        /* SSD_SEMANTICS_* */
+  char* transcript;         /* optional JSONL round transcript (Transcript::to_jsonl, sim.cpp:489-500),
+                               NUL-terminated, harness semantics only */
+  int64_t transcript_cap;   /* bytes available at transcript */
+  int64_t* transcript_len;  /* optional: bytes the full transcript needs (without the NUL) */
+} ssd_run_options;
+
+/* ssd_run_ssd_batch with a choice of semantics and an optional transcript.
+ * Raises SSD_PROTOCOL_VIOLATION when the harness' overlap invariant fails
+ * (sim.cpp:534-537). */
+ssd_status ssd_run_ssd_ex(ssd_engine* e, const int32_t* prompt, int32_t prompt_len, const ssd_sim_config* cfg,
+                          int32_t batch, const ssd_run_options* opt, int32_t* out_tokens, int64_t out_capacity,
+                          int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats);
+
 /* ------------------------------------------ split processes (sim.cpp:258-601)
  * The reference's Channel between VerifierProcess and DraftProcess becomes
  * device mailboxes in HBM, mapped across processes/GPUs by CUDA IPC (NVLink

@@ -51,6 +51,14 @@ class RunStatsC(C.Structure):
                 ("device_ms", C.c_double), ("kernel_launches", C.c_int64)]
 
 
+SEMANTICS_HARNESS, SEMANTICS_SEQUENTIAL = 0, 1
+
+
+class RunOptionsC(C.Structure):
+    _fields_ = [("semantics", C.c_int32), ("transcript", C.c_char_p), ("transcript_cap", C.c_int64),
+                ("transcript_len", C.POINTER(C.c_int64))]
+
+
 P = C.POINTER
 i32p, i64p, u64p, f32p, u16p = P(C.c_int32), P(C.c_int64), P(C.c_uint64), P(C.c_float), P(C.c_uint16)
 EngineP = C.c_void_p
@@ -90,6 +98,8 @@ SIGNATURES = {
     "ssd_run_sd": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), i32p, C.c_int64, i64p, P(RunStatsC)]),
     "ssd_run_ssd": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), i32p, C.c_int64, i64p, i32p, i32p,
                               P(RunStatsC)]),
+    "ssd_run_ssd_ex": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, P(RunOptionsC), i32p, C.c_int64,
+                                 i64p, i32p, i32p, P(RunStatsC)]),
     "ssd_run_ssd_batch": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), C.c_int32, i32p, C.c_int64, i64p, i32p,
                                     i32p, P(RunStatsC)]),
     "ssd_logits": (C.c_int, [EngineP, C.c_int32, i32p, C.c_int32, f32p]),

@@ -218,6 +218,7 @@ class RunStats:
     batch: int = 1
     outcomes: Optional[np.ndarray] = None  # [rounds, 2] (accepted, bonus)
     hits: Optional[np.ndarray] = None      # [rounds] 1/0, -1 on the last round
+    transcript: Optional[list] = None      # harness round transcript (sim.cpp:489-500), parsed JSONL
 
     @classmethod
     def _from_c(cls, s: N.RunStatsC, stream=None):
@@ -385,11 +386,16 @@ class Engine:
                                    C.byref(n), C.byref(st)))
         return RunStats._from_c(st, out[: n.value].tolist())
 
-    def run_ssd(self, prompt: Sequence[int], cfg: SimConfig) -> RunStats:
-        """sim::run_protocol_harness semantics (sim.cpp:502-601), with
-        cfg.batch_size sequences (whole-batch stall: any miss delays the
-        round for the backup). streams[j] is sequence j's output; outcomes /
-        hits are sequence 0's."""
+    def run_ssd(self, prompt: Sequence[int], cfg: SimConfig, semantics: str = "harness",
+                transcript: bool = False) -> RunStats:
+        """semantics "harness": sim::run_protocol_harness (sim.cpp:502-601);
+        "sequential": sim::run_ssd / run_ssd_batch (sim.cpp:123-250, one
+        stream per sequence, the cache built after verify). cfg.batch_size
+        sequences (whole-batch stall: any miss delays the round for the
+        backup). streams[j] is sequence j's output; outcomes / hits are
+        sequence 0's. transcript=True (harness): r.transcript is the JSONL
+        round transcript (Transcript::to_jsonl, sim.cpp:489-500), parsed."""
+        import json
         p = _i32(prompt)
         b = int(cfg.batch_size)
         cap = cfg.rounds * (cfg.lookahead + 1)
@@ -398,10 +404,24 @@ class Engine:
         hits = np.zeros(cfg.rounds, dtype=np.int32)
         lens = np.zeros(b, dtype=np.int64)
         st = N.RunStatsC()
-        _check(self.lib.ssd_run_ssd_batch(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), b,
-                                          _ptr(out, C.c_int32), cap, _ptr(lens, C.c_int64), _ptr(oc, C.c_int32),
-                                          _ptr(hits, C.c_int32), C.byref(st)))
+        opt = N.RunOptionsC()
+        opt.semantics = {"harness": N.SEMANTICS_HARNESS, "sequential": N.SEMANTICS_SEQUENTIAL}[semantics]
+        tlen = C.c_int64(0)
+        tbuf = None
+        if transcript:
+            tcap = 4096 + cfg.rounds * b * (64 + 16 * (cfg.lookahead + 4)) + 256 * cfg.rounds
+            tbuf = C.create_string_buffer(tcap)
+            opt.transcript = C.cast(tbuf, C.c_char_p)
+            opt.transcript_cap = tcap
+            opt.transcript_len = C.pointer(tlen)
+        _check(self.lib.ssd_run_ssd_ex(self.h, _ptr(p, C.c_int32), len(p), C.byref(cfg.c()), b, C.byref(opt),
+                                       _ptr(out, C.c_int32), cap, _ptr(lens, C.c_int64), _ptr(oc, C.c_int32),
+                                       _ptr(hits, C.c_int32), C.byref(st)))
         r = RunStats._from_c(st, out[: int(lens[0])].tolist())
+        if transcript:
+            if tlen.value >= tcap:
+                raise Error("transcript: buffer too small")
+            r.transcript = [json.loads(x) for x in tbuf.value.decode().splitlines() if x]
         r.streams = [out[j * cap: j * cap + int(lens[j])].tolist() for j in range(b)]
         r.batch = b
         r.outcomes = oc.reshape(-1, 2)

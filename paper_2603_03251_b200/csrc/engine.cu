@@ -216,6 +216,7 @@ struct Engine {
   // forward 24.9 -> 12.3 ms) (SSD_B200_ATTN_DEC_WIDE_M)
   int attn_dec_wide_m = 20;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
+  int cl_min_m = 17;                     // SSD_B200_CL_MIN_M: ... for forwards of at least this many tokens
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // ... inside the colocated SSD round, where the verifier and speculator
   // streams run at once: the 108 KB co-resident GEMM config lets their CTAs
@@ -636,6 +637,11 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 192>(); configure_gemm<EPI_SWIGLU, 192>();
   configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
   configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
+  configure_cl<EPI_STORE, 16, 2>(); configure_cl<EPI_STORE, 16, 4>(); configure_cl<EPI_STORE, 16, 8>();
+  configure_cl<EPI_SWIGLU, 16, 2>(); configure_cl<EPI_SWIGLU, 16, 4>(); configure_cl<EPI_SWIGLU, 16, 8>();
+  configure_cl<EPI_STORE, 16, 2, kClSmallBudgetKB>(); configure_cl<EPI_STORE, 16, 4, kClSmallBudgetKB>();
+  configure_cl<EPI_STORE, 16, 8, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 16, 2, kClSmallBudgetKB>();
+  configure_cl<EPI_SWIGLU, 16, 4, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 16, 8, kClSmallBudgetKB>();
   configure_cl<EPI_STORE, 32, 2>(); configure_cl<EPI_STORE, 32, 4>(); configure_cl<EPI_STORE, 32, 8>();
   configure_cl<EPI_SWIGLU, 32, 2>(); configure_cl<EPI_SWIGLU, 32, 4>(); configure_cl<EPI_SWIGLU, 32, 8>();
   configure_cl<EPI_STORE, 32, 2, kClSmallBudgetKB>(); configure_cl<EPI_STORE, 32, 4, kClSmallBudgetKB>();
@@ -699,8 +705,9 @@ static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, flo
   // small weight matrices at branch widths (17..32 tokens): cluster split-K.
   // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
-  if (W.bytes <= E.cl_gemm_bytes && M > 16 && M <= 32 && m.gemm_ctas == 0) {
-    gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
+  if (W.bytes <= E.cl_gemm_bytes && M >= E.cl_min_m && M <= 32 && m.gemm_ctas == 0) {
+    if (M <= 16) gemm_cl_dispatch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
+    else gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
     return;
   }
   // small weight matrices: the co-resident (small-budget) configuration
@@ -985,6 +992,7 @@ static void reset_state(Engine& E, int K, int n, int64_t rounds, uint64_t dseed,
   std::memset(&h, 0, sizeof(h));
   h.n = n;
   h.K = K;
+  h.Kb = K;
   h.rounds = int(rounds);
   h.backup_kind = c ? c->backup_kind : 1;
   h.primary_time = c ? c->primary_time : 0.0;
@@ -1005,6 +1013,7 @@ static LoopState read_state(Engine& E, int lane = 0) {
 static void raise_device_error(const LoopState& h) {
   if (h.error == 1) throw Fail(SSD_ERROR, "verify: drafted token has zero draft probability");
   if (h.error == 3) throw Fail(SSD_DEGENERATE_RESIDUAL, "residual: zero positive mass (draft equals target)");
+  if (h.error == 11) throw Fail(SSD_PROTOCOL_VIOLATION, "protocol: cache missed the overlap window");
   if (h.error) throw Fail(SSD_ERROR, "device error " + std::to_string(h.error));
 }
 
@@ -1096,13 +1105,19 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 // Batch lanes (nl > 1, no sharding: lo = 0, Bl = B): every lane's extend
 // rides one M = nl (K+1) forward, its B branches are rows [l B, (l+1) B) of
 // one M = nl B branch step.
+// before_streams (sequential run_ssd semantics, sim.cpp:159-204): the
+// branch streams' base is drawn from the sequence stream AFTER verify's
+// draws, so the branch half waits for the verifier. Kb: continuation length
+// of each entry (build_cache's next_lookahead; K in the loops).
 static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
-                         cudaStream_t s, int nl = 1) {
+                         cudaStream_t s, int nl = 1, cudaEvent_t before_streams = nullptr, int Kb = -1) {
+  if (Kb < 0) Kb = K;
   prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S);
   KCHECK();
   forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
   mark(E, 4, s);
   row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s, nl, B);
+  if (before_streams) CK(cudaStreamWaitEvent(s, before_streams, 0));
   const bool sampled = sc.temperature > 0.0;
   branch_streams_kernel<<<nl, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
@@ -1112,13 +1127,13 @@ static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, con
   if (Bl <= 0) return;
   const DScheme ds = dscheme(sc);
   float* rows = E.brows[parity];
-  for (int j = 0; j < K; ++j) {
+  for (int j = 0; j < Kb; ++j) {
     prep_branch_kernel<<<(Bl + 127) / 128, 128, 0, s>>>(E.st, E.bk + lo, E.btok + lo, E.bt, E.P_b, Bl, j,
                                                          E.D.s.max_ctx, nl > 1 ? B : 0, E.D.lane_S);
     float* out = rows + size_t(j) * Bl * E.V;
     forward(E, E.D, E.P_b, Bl, out, s);
     if (j < 8) mark(E, 6 + 2 * j, s);
-    row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * K + j : nullptr, K, E.bt + j, K, s);
+    row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * Kb + j : nullptr, Kb, E.bt + j, Kb, s);
     KCHECK();
     if (j < 8) mark(E, 7 + 2 * j, s);
     E.launches += 1;
@@ -1302,6 +1317,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* aw = std::getenv("SSD_B200_ATTN_DEC_WIDE_M")) E.attn_dec_wide_m = std::max(1, std::atoi(aw));
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
+  if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
@@ -1537,9 +1553,14 @@ namespace ssd {
 // lanes share the prompt, their forwards are batched (verify M = nb (K+1),
 // branch steps M = nb B), and a miss in any lane stalls the round's clock
 // for the backup (sim.cpp:570-577).
+// mode 1: run_ssd_batch semantics (sim.cpp:128-250) — one stream per
+// sequence (verify, then the cache base, then the backup), cache built after
+// verify, clock += previous all hit ? max(1, T_p) : 1 + T_b. tr: optional
+// per-round transcript log (sim.cpp:271-317).
 static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int nb, int32_t* out,
                          int64_t cap, int64_t* out_lens, int32_t* out_outcomes, int32_t* out_hits, ssd_run_stats* stats,
-                         double* prof = nullptr) {
+                         double* prof = nullptr, int mode = 0, std::vector<int>* tr_i = nullptr,
+                         std::vector<double>* tr_d = nullptr, std::vector<int>* tr_init = nullptr) {
   CK(cudaSetDevice(E.dev));
   validate_cfg(E, c);
   need(E.T, "run_ssd");
@@ -1553,17 +1574,28 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   if (nb * B > E.D.maxM || nb * (K + 1) > E.T.maxM) throw Fail(SSD_TOO_LARGE, "sim: batch x branches exceeds capacity");
   set_history(E, prompt, n0, int(n0 + c->rounds * (K + 1) + 2 * K + 2), nb);
   const int64_t R = c->rounds;
-  if (R > E.ssd_log_cap) {  // per-round logs (their address is baked into the graphs)
+  // per-round logs (their address is baked into the graphs): [2 cap]
+  // outcomes + [cap] hits, then the transcript log [cap][maxB lanes][kTrInts]
+  // ints and [cap][2] doubles
+  const size_t tr_ints = size_t(E.nbmax) * kTrInts;
+  if (R > E.ssd_log_cap) {
     if (E.ssd_log) cudaFree(E.ssd_log);
     E.ssd_log = nullptr;
     E.ssd_log_cap = 0;
-    E.ssd_log = dalloc<int>(size_t(3 * R));
+    E.ssd_log = dalloc<int>(size_t(R) * (3 + tr_ints + 4));
     E.ssd_log_cap = R;
   }
   int* const d_out = E.ssd_log;
   int* const d_hit = E.ssd_log + 2 * E.ssd_log_cap;
+  TrLog tr{nullptr, nullptr, n0};
+  if (tr_i) {
+    tr.i = E.ssd_log + 3 * E.ssd_log_cap;
+    tr.d = reinterpret_cast<double*>(tr.i + ((size_t(E.ssd_log_cap) * tr_ints + 1) & ~size_t(1)));
+  }
   cudaStream_t sv = E.sv, ss = E.ss;
   for (int l = 0; l < nb; ++l) {
+    // harness: draft stream derive_seed(seed, j), verifier derive_seed(derive_seed(seed, 0x5EED), j)
+    // (sim.cpp:379-380, 516-518); run_ssd_batch: the single stream derive_seed(seed, j) (sim.cpp:142)
     reset_state(E, K, n0, R, derive_seed(c->seed, uint64_t(l)), derive_seed(derive_seed(c->seed, 0x5EED), uint64_t(l)),
                 c, sv, l);
     if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, sv, l);
@@ -1575,10 +1607,17 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   CK(cudaMemcpyAsync(E.d_lanes, lanes.data(), size_t(nb) * 4, cudaMemcpyHostToDevice, sv));
   draft_lanes(E, K, c->scheme, 0, 0, nb, sv);
   for (int l = 0; l < nb; ++l) {
-    const double clock0 = c->primary_time;
+    const double clock0 = mode == 1 ? 1.0 + c->primary_time : c->primary_time;
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st + l) + offsetof(LoopState, clock), &clock0, sizeof(double),
                        cudaMemcpyHostToDevice, sv));
     CK(cudaStreamSynchronize(sv));
+  }
+  if (tr_init) {  // the initial speculations (the transcript's first d2v message)
+    tr_init->clear();
+    for (int l = 0; l < nb; ++l) {
+      const LoopState h0 = read_state(E, l);
+      tr_init->insert(tr_init->end(), h0.spec, h0.spec + K);
+    }
   }
   const bool jit = c->backup_kind == 0;
   // One SSD round = one graph: the verifier branch (verify forward +
@@ -1604,7 +1643,8 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
                 c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
                 static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
-  const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "");
+  const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "") + " mode" + std::to_string(mode) +
+                          (tr.i ? " tr" : "") + " n0 " + std::to_string(n0);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
       if (g) cudaGraphExecDestroy(g);
@@ -1617,12 +1657,20 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
       CK(cudaEventRecord(E.ev_fork, sv));
       CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
       mark(E, 3, ss);
-      prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb);
-      verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
-      CK(cudaEventRecord(E.ev_verified, sv));
-      CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
+      if (mode == 1) {
+        // verify first on the sequence stream; extend + keys overlap it, the
+        // branch streams / steps follow it (their base is drawn after verify)
+        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 1, sv, nb);
+        CK(cudaEventRecord(E.ev_verified, sv));
+        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, E.ev_verified);
+      } else {
+        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb);
+        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
+        CK(cudaEventRecord(E.ev_verified, sv));
+        CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
+      }
       lookup_kernel<<<1, 32, 0, ss>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V, E.cum,
-                                      d_out, d_hit);
+                                      d_out, d_hit, mode, tr);
       KCHECK();
       mark(E, kMarkRoundEnd, ss);
       ++E.launches;
@@ -1680,6 +1728,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
         const long long before = E.launches;
         CK(cudaMemcpyAsync(E.d_lanes, lanes.data(), size_t(nm) * 4, cudaMemcpyHostToDevice, sv));
         draft_lanes(E, K, c->scheme, 1, 2, nm, sv);
+        if (tr.i) tr_log_spec_kernel<<<1, 32, 0, sv>>>(E.st, E.d_lanes, nm, nb, tr);
         jit_launches += E.launches - before;
       }
     }
@@ -1693,6 +1742,13 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   for (int l = 0; l < nb; ++l) sts.push_back(read_state(E, l));
   if (out_outcomes) d2h(E, out_outcomes, d_out, size_t(2 * R) * 4);
   if (out_hits) d2h(E, out_hits, d_hit, size_t(R) * 4);
+  if (tr.i) {
+    tr_i->resize(size_t(R) * nb * kTrInts);
+    tr_d->resize(size_t(2 * R));
+    for (int64_t r = 0; r < R; ++r)
+      d2h(E, tr_i->data() + size_t(r) * nb * kTrInts, tr.i + size_t(r) * nb * kTrInts, size_t(nb) * kTrInts * 4);
+    d2h(E, tr_d->data(), tr.d, size_t(2 * R) * 8);
+  }
   const LoopState st = sum_lanes(sts);
   raise_device_error(st);
   fill_stats(st, R, ms, E.launches, stats);
@@ -1718,6 +1774,70 @@ ssd_status ssd_run_ssd_batch(ssd_engine* h, const int32_t* prompt, int32_t n0, c
                              ssd_run_stats* stats) {
   API_BEGIN
   run_ssd_impl(h->e, prompt, n0, c, batch, out, cap, out_lens, out_outcomes, out_hits, stats);
+  API_END
+}
+
+// JSONL transcript (reference Transcript::to_jsonl, sim.cpp:489-500): one
+// line per message, keys as the reference's Channel writes them.
+static std::string transcript_jsonl(const std::vector<int>& ti, const std::vector<double>& td,
+                                    const std::vector<int>& init, int nb, int K, int V, int64_t R, double t0) {
+  std::string out;
+  char buf[64];
+  auto num = [&](double v) { std::snprintf(buf, sizeof buf, "%.17g", v); return std::string(buf); };
+  auto d2v = [&](int64_t round, const int* hits, const std::vector<std::vector<int>>& toks, double vclock) {
+    std::string h = "[", t = "[";
+    for (int l = 0; l < nb; ++l) {
+      h += (l ? "," : "") + std::to_string(hits ? hits[l] : 0);
+      t += l ? ",[" : "[";
+      for (int i = 0; i < K; ++i) t += (i ? "," : "") + std::to_string(toks[size_t(l)][size_t(i)]);
+      t += "]";
+    }
+    out += "{\"dir\":\"d2v\",\"payload_summary\":{\"dists_shape\":[" + std::to_string(K) + "," + std::to_string(V) +
+           "],\"hits\":" + h + "],\"tokens\":" + t + "]},\"round\":" + std::to_string(round) + ",\"vclock\":" + num(vclock) + "}\n";
+  };
+  std::vector<std::vector<int>> toks(static_cast<size_t>(nb), std::vector<int>(static_cast<size_t>(K)));
+  for (int l = 0; l < nb; ++l)
+    for (int i = 0; i < K; ++i) toks[size_t(l)][size_t(i)] = init[size_t(l) * K + i];
+  d2v(1, nullptr, toks, t0);
+  for (int64_t r = 0; r < R; ++r) {
+    std::string o = "[", sl = "[";
+    std::vector<int> hits(static_cast<size_t>(nb));
+    for (int l = 0; l < nb; ++l) {
+      const int* e = ti.data() + (size_t(r) * nb + l) * kTrInts;
+      o += (l ? ",[" : "[") + std::to_string(e[0]) + "," + std::to_string(e[1]) + "]";
+      sl += (l ? "," : "") + std::to_string(e[3]);
+      hits[size_t(l)] = e[2];
+      for (int i = 0; i < K; ++i) toks[size_t(l)][size_t(i)] = e[4 + i];
+    }
+    out += "{\"dir\":\"v2d\",\"payload_summary\":{\"outcomes\":" + o + "],\"seq_lens\":" + sl + "]},\"round\":" +
+           std::to_string(r + 1) + ",\"vclock\":" + num(td[size_t(2 * r)]) + "}\n";
+    if (r + 1 < R) d2v(r + 2, hits.data(), toks, td[size_t(2 * r + 1)]);
+  }
+  return out;
+}
+
+ssd_status ssd_run_ssd_ex(ssd_engine* h, const int32_t* prompt, int32_t n0, const ssd_sim_config* c, int32_t batch,
+                          const ssd_run_options* opt, int32_t* out, int64_t cap, int64_t* out_lens, int32_t* out_outcomes,
+                          int32_t* out_hits, ssd_run_stats* stats) {
+  API_BEGIN
+  Engine& E = h->e;
+  const int mode = opt ? opt->semantics : SSD_SEMANTICS_HARNESS;
+  if (mode != SSD_SEMANTICS_HARNESS && mode != SSD_SEMANTICS_SEQUENTIAL) throw Fail(SSD_CONFIG, "run_ssd: unknown semantics");
+  const bool want_tr = opt && (opt->transcript || opt->transcript_len);
+  if (want_tr && mode != SSD_SEMANTICS_HARNESS) throw Fail(SSD_CONFIG, "transcript: harness semantics only");
+  std::vector<int> ti, init;
+  std::vector<double> td;
+  run_ssd_impl(E, prompt, n0, c, batch, out, cap, out_lens, out_outcomes, out_hits, stats, nullptr, mode,
+               want_tr ? &ti : nullptr, want_tr ? &td : nullptr, want_tr ? &init : nullptr);
+  if (want_tr) {
+    const std::string j = transcript_jsonl(ti, td, init, batch, c->lookahead, E.V, c->rounds, c->primary_time);
+    if (opt->transcript_len) *opt->transcript_len = int64_t(j.size());
+    if (opt->transcript && opt->transcript_cap > 0) {
+      const size_t n = std::min<size_t>(j.size(), size_t(opt->transcript_cap - 1));
+      std::memcpy(opt->transcript, j.data(), n);
+      opt->transcript[n] = 0;
+    }
+  }
   API_END
 }
 
@@ -1941,7 +2061,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
       prespeculate(E, K, B, lo, Bl, max_f, c->scheme, parity, s);
       recv_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, E.hist);
       lookup_kernel<<<1, 32, 0, s>>>(E.st, 1, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, 0, E.V, E.cum, nullptr,
-                                     d_hit);
+                                     d_hit, 0, TrLog{nullptr, nullptr, 0});
       send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 0, E.send_counter);
       recv_peer_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox);
       KCHECK();

@@ -60,7 +60,7 @@ struct LoopState {
   int backup_kind;   // 0 SamePrimaryJIT, 1 FastRandom
   int own;           // split speculator: the hit slot's branch is decoded here
   int seq_base;      // split runs: mailbox sequence numbers of this run start above it
-  int pad_;
+  int Kb;            // pre-speculation continuation length (build_cache next_lookahead; K in the loops)
   double clock;      // harness virtual clock
   double primary_time, backup_time;
   long long tokens, p_lookups, p_hits, b_lookups, b_hits;
@@ -1000,7 +1000,7 @@ __global__ void prep_branch_kernel(const LoopState* __restrict__ st, const int* 
   if (b >= B) return;
   const int l = bper > 0 ? b / bper : 0, lb = bper > 0 ? b - l * bper : b;
   st += l;
-  const int K = st->K, n = st->n, k = bk[b];
+  const int K = st->Kb, n = st->n, k = bk[b];
   const int mb = l * lane_slots, bb = mb + kv_base + lb * K;
   P->tokens[b] = j == 0 ? btok[b] : bt[b * K + j - 1];
   P->pos[b] = n + k + j;
@@ -1017,11 +1017,11 @@ __global__ void prep_branch_kernel(const LoopState* __restrict__ st, const int* 
 __global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__ bu /* [B][K] */, int need) {
   __shared__ uint64_t base;
   st += blockIdx.x;
-  bu += size_t(blockIdx.x) * B * st->K;
+  bu += size_t(blockIdx.x) * B * st->Kb;
   if (threadIdx.x == 0) base = mt_next(st->drng);
   __syncthreads();
   if (!need) return;
-  const int K = st->K;
+  const int K = st->Kb;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     Mt64 m;
     mt_seed(m, derive_seed(base, uint64_t(b)));
@@ -1035,10 +1035,24 @@ __global__ void branch_streams_kernel(LoopState* st, int B, double* __restrict__
 // :133-138 on a vector of 1/V), for the FastRandom tokens (sim.cpp:35-48).
 // Branch sharding: this engine decodes branches [lo, lo + Bl)
 // of the B keyed ones; bt / brows hold only those ([Bl][K], [K][Bl][V]).
+// Per-round transcript log (sim.cpp:271-317 Channel, 489-500 to_jsonl):
+// ints [round][lane][kTrInts] = (k, t, hit, emitted so far, next spec[K]),
+// doubles [round][2] = (v2d vclock, d2v vclock).
+constexpr int kTrInts = 4 + kMaxK;
+struct TrLog {
+  int* i;
+  double* d;
+  int n0;  // prompt length (seq_lens count emitted tokens)
+};
+
+// mode: 0 run_protocol_harness (sim.cpp:502-601: verifier / draft streams,
+// cache ready at v0 + T_p, clock = all hit ? max(v1, ready) : v1 + T_b),
+// 1 run_ssd_batch (sim.cpp:128-250: one stream per sequence, clock +=
+// previous all hit ? max(1, T_p) : 1 + T_b).
 __global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ keys, int max_f,
                               const int* __restrict__ off2, const int* __restrict__ bt, const float* __restrict__ brows,
                               int lo, int Bl, int bper, int V, const double* __restrict__ cum,
-                              int* __restrict__ log_outcomes, int* __restrict__ log_hits) {
+                              int* __restrict__ log_outcomes, int* __restrict__ log_hits, int mode, TrLog tr) {
   if (threadIdx.x != 0) return;
   // Batch lanes (sim.cpp:548-577): every lane looks up its own outcome; the
   // round's virtual clock stalls the whole batch for the backup when any
@@ -1047,6 +1061,11 @@ __global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ key
   const double v0 = st[0].clock, v1 = v0 + 1.0, ready = v0 + st[0].primary_time;
   const int r = st[0].round;  // 0-based round being closed
   const bool last = r + 1 >= st[0].rounds;  // last round: no lookup, no backup
+  // harness overlap invariant (sim.cpp:534-537)
+  if (mode == 0 && st[0].primary_time < 1.0 && ready >= v1) {
+    for (int l = 0; l < nb; ++l) st[l].error = 11;
+    return;
+  }
   bool all_hit = true;
   for (int l = 0; l < nb; ++l) {
     LoopState* s = st + l;
@@ -1060,6 +1079,8 @@ __global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ key
     if (l == 0 && log_outcomes) { log_outcomes[2 * r] = k; log_outcomes[2 * r + 1] = t; }
     s->n += k + 1;
     s->round = r + 1;
+    int* tl = tr.i ? tr.i + (size_t(r) * nb + l) * kTrInts : nullptr;
+    if (tl) { tl[0] = k; tl[1] = t; tl[2] = 0; tl[3] = s->n - tr.n0; }
     if (last) {
       if (l == 0 && log_hits) log_hits[r] = -1;
       continue;
@@ -1102,9 +1123,26 @@ __global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ key
         s->spec_uniform = 0;  // the host runs the JIT re-draft
       }
     }
+    if (tl) {
+      tl[2] = hit ? 1 : 0;
+      for (int i = 0; i < K; ++i) tl[4 + i] = s->spec[i];  // JIT lanes: rewritten after the re-draft
+    }
   }
-  const double clock = last ? v1 : (all_hit ? fmax(v1, ready) : v1 + st[0].backup_time);
+  double clock;
+  if (mode == 1) clock = last ? v0 : v0 + (all_hit ? fmax(1.0, st[0].primary_time) : 1.0 + st[0].backup_time);
+  else clock = last ? v1 : (all_hit ? fmax(v1, ready) : v1 + st[0].backup_time);
   for (int l = 0; l < nb; ++l) st[l].clock = clock;
+  if (tr.d) { tr.d[2 * r] = mode == 1 ? v0 : v1; tr.d[2 * r + 1] = clock; }
+}
+
+// Transcript: the speculation each listed lane sends after a JIT re-draft.
+__global__ void tr_log_spec_kernel(const LoopState* st, const int* __restrict__ lanes, int nl, int nb, TrLog tr) {
+  if (threadIdx.x != 0 || !tr.i) return;
+  for (int m = 0; m < nl; ++m) {
+    const LoopState* s = st + lanes[m];
+    int* tl = tr.i + (size_t(s->round - 1) * nb + lanes[m]) * kTrInts;
+    for (int i = 0; i < s->K; ++i) tl[4 + i] = s->spec[i];
+  }
 }
 
 // After a JIT / initial draft of spec[] from rows: origin bookkeeping.

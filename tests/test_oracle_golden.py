@@ -63,3 +63,23 @@ def test_oracle_matches_live_reference_on_fresh_seeds(oracle_lib):
         a = oracle_lib.oracle().call(req)
         b = oracle_lib.reference().call(req)
         assert {k: a[k] for k in b} == b, req
+
+
+def test_chi_square_two_sample_restatement():
+    """tests/parity.py chi_square_two_sample restates the reference's
+    stats.cpp:51-94 (the GPU losslessness test's statistic): equal samples
+    give statistic 0 and p = 1; pooling of sparse cells and the scaled
+    two-sample statistic checked against a hand computation."""
+    import numpy as np
+    from parity import bigram_counts, chi_square_two_sample
+    a = np.array([50, 30, 20, 3, 2])
+    p, stat, dof = chi_square_two_sample(a, a)
+    assert stat == 0.0 and p == 1.0 and dof == 3  # cells 3 and 4 pooled (5 < 10 each, 10 together)
+    b = np.array([30, 30, 40, 0, 0])
+    ka, kb = np.sqrt(100 / 105), np.sqrt(105 / 100)
+    want = sum((ka * x - kb * y) ** 2 / (x + y) for x, y in ((50, 30), (30, 30), (20, 40), (5, 0)))
+    p, stat, dof = chi_square_two_sample(a, b)
+    assert abs(stat - want) < 1e-9 and dof == 3
+    from scipy.stats import chi2
+    assert abs(p - chi2.sf(want, 3)) < 1e-12
+    assert bigram_counts([[0, 1, 1, 0]], 2).tolist() == [0, 1, 1, 1]
