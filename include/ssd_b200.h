@@ -305,6 +305,71 @@ ssd_status ssd_build_cache(ssd_engine* e, const int32_t* context, int32_t n,
                            const ssd_scheme* scheme, int32_t next_lookahead, uint64_t base_seed,
                            int32_t* out_keys, int32_t* out_entry_tokens, int32_t* out_count);
 
+/* ------------------------------------------------ caller-owned streams
+ * rng::Stream (rng.hpp:29-48) as a plain C value: the mt19937_64 state of
+ * std::mt19937_64(seed), advanced in place by every call that takes an
+ * ssd_rng_stream* exactly as the reference advances the Stream& it is given
+ * (one uniform per draw, one next_u64 per build_cache). Layout-compatible
+ * with the engine's device streams, so state moves between host and GPU. */
+typedef struct ssd_rng_stream {
+  uint64_t state[312];
+  int32_t index;
+  int32_t reserved_;
+} ssd_rng_stream;
+void ssd_rng_stream_seed(ssd_rng_stream* s, uint64_t seed);  /* Stream(seed) */
+uint64_t ssd_rng_stream_next_u64(ssd_rng_stream* s);          /* Stream::next_u64 */
+double ssd_rng_stream_next_uniform(ssd_rng_stream* s);        /* Stream::next_uniform, (x >> 11) * 2^-53 */
+uint64_t ssd_derive_seed(uint64_t root, uint64_t index);      /* rng::derive_seed (rng.hpp:24-26) */
+
+/* specdec::draft (specdec.hpp:59-61) with the caller's stream: K uniforms
+ * drawn from *rng (greedy draws none); tokens and the fp32 draft logit rows
+ * [K][V] they were drawn from (the Speculation's dists = scheme(rows)). */
+ssd_status ssd_draft_stream(ssd_engine* e, const int32_t* context, int32_t n, int32_t lookahead,
+                            const ssd_scheme* scheme, ssd_rng_stream* rng, int32_t* out_tokens, float* out_rows);
+
+/* specdec::verify (specdec.hpp:81-83, specdec.cpp:27-69): the target's
+ * verify forward over context || spec (K+1 logit rows, M = K+1) and the
+ * fused decision, drawing coins / the bonus from *rng. spec_rows: the draft
+ * logit rows [K][V] the speculation was drawn from under draft_scheme, NULL
+ * for a speculation with uniform dists (the FastRandom backup, sim.cpp:35-48).
+ * Writes the outcome (k, t*) and emitted[0..k] (the accepted prefix plus the
+ * bonus; capacity K+1). VerifyOptions = (target_scheme, accept_scale). */
+ssd_status ssd_verify(ssd_engine* e, const int32_t* context, int32_t n, const int32_t* spec_tokens,
+                      int32_t lookahead, const float* spec_rows, const ssd_scheme* draft_scheme,
+                      const ssd_scheme* target_scheme, double accept_scale, ssd_rng_stream* rng,
+                      int32_t* accepted, int32_t* bonus, int32_t* emitted);
+
+/* cache::build_cache (cache.hpp:149-154, cache.cpp:232-277) with the
+ * caller's stream: exactly one next_u64 taken from *rng as the entries'
+ * base (cache.cpp:245); entry i continues for next_lookahead (1 .. engine
+ * capacity, may differ from the speculation's K) tokens drawn from
+ * Stream(derive_seed(base, i)). Writes the keys (k, t) in ordinal order,
+ * each entry's tokens [count][next_K] and, when out_entry_rows != NULL, the
+ * draft logit rows they were drawn from [count][next_K][V]. */
+ssd_status ssd_build_cache_stream(ssd_engine* e, const int32_t* context, int32_t n, const int32_t* spec_tokens,
+                                  int32_t lookahead, const ssd_plan* plan, const ssd_scheme* scheme,
+                                  int32_t next_lookahead, ssd_rng_stream* rng, int32_t* out_keys,
+                                  int32_t* out_entry_tokens, float* out_entry_rows, int32_t* out_count);
+
+/* ------------------------------------- asynchronous pre-speculation
+ * the speculator's build_cache as a device-side session call.
+ * ssd_prespec_begin enqueues the pre-speculation of DEVICE buffers
+ * d_context[n] / d_spec_tokens[K] on the engine's speculator stream, ordered
+ * after the work already queued on `cuda_stream` (a cudaStream_t, NULL = no
+ * ordering), and returns without waiting; it takes one next_u64 from *rng
+ * on the host (cache.cpp:245). The cache stays valid until the next
+ * ssd_prespec_begin. ssd_cache_lookup / _keys / _entry wait for it. */
+ssd_status ssd_prespec_begin(ssd_engine* e, const int32_t* d_context, int32_t n, const int32_t* d_spec_tokens,
+                             int32_t lookahead, const ssd_plan* plan, const ssd_scheme* scheme,
+                             int32_t next_lookahead, ssd_rng_stream* rng, void* cuda_stream);
+/* SpeculationCache::lookup (cache.hpp:123-126): *slot = entry ordinal of
+ * key (accepted, bonus), or -1 on a miss. */
+ssd_status ssd_cache_lookup(ssd_engine* e, int32_t accepted, int32_t bonus, int32_t* slot);
+/* Every key (k, t) in ordinal order (out_keys[2 * count]) — the parity hook. */
+ssd_status ssd_cache_keys(ssd_engine* e, int32_t* out_keys, int32_t* out_count);
+/* Entry `slot`: tokens [next_K] and (optional) draft logit rows [next_K][V], host buffers. */
+ssd_status ssd_cache_entry(ssd_engine* e, int32_t slot, int32_t* out_tokens, float* out_rows);
+
 /* ------------------------------------------- kernel-level parity hooks
  * (host buffers in, host buffers out; used by tests/). */
 

@@ -9,17 +9,23 @@
 //   dist::SamplingScheme (categorical.hpp:43-60)    -> ssdlab_b200::SamplingScheme
 //   cache::FanOutPlan (cache.hpp:18-25)             -> ssdlab_b200::FanOutPlan
 //   cache::geometric_fanout / uniform_fanout        -> same names (cache.hpp:57-64)
-//   specdec::draft (specdec.hpp:59-61)              -> Engine::draft
-//   specdec::verify (specdec.hpp:81-83)             -> Engine::verify_rows (decision on given logit rows)
-//   cache::build_cache (cache.hpp:149-154)          -> Engine::build_cache -> SpeculationCache
+//   rng::Stream (rng.hpp:29-48)                     -> ssdlab_b200::Stream (same next_u64 / next_uniform)
+//   specdec::draft (specdec.hpp:59-61)              -> Engine::draft(ctx, K, scheme, Stream&)
+//   specdec::verify (specdec.hpp:81-83)             -> Engine::verify(ctx, spec, Stream&, VerifyOptions)
+//   cache::build_cache (cache.hpp:149-154)          -> Engine::build_cache(ctx, spec, plan, scheme, next_K, Stream&)
 //   SpeculationCache::lookup (cache.hpp:123-126)    -> SpeculationCache::lookup (non-owning pointer or nullptr)
-//   sim::run_ar / run_sd / run_protocol_harness     -> Engine::run_ar / run_sd / run_ssd
+//   sim::run_ar / run_sd                            -> Engine::run_ar / run_sd
+//   sim::run_ssd / run_ssd_batch                    -> Engine::run_ssd_sequential
+//   sim::run_protocol_harness (+ Transcript)        -> Engine::run_ssd (+ transcript_jsonl)
 //   lm::SyntheticLM::logits_at (lm.cpp:82-84)       -> Engine::logits
+//   (device side)                       -> Engine::prespec_begin / cache_lookup / cache_keys / cache_entry
 //
-// Differences the caller must know: randomness is passed as a seed (the
-// engine seeds mt19937_64 streams on the device exactly as rng::Stream(seed)
-// does) instead of a mutable rng::Stream&; distributions stay on the device
-// (Speculation carries tokens and, on request, the fp32 logit rows).
+// Differences the caller must know: distributions stay on the device — a
+// Speculation carries its tokens and the fp32 draft LOGIT rows [K][V] they
+// were drawn from (its dists = the scheme applied to those rows; empty rows
+// = the uniform dists of the FastRandom backup). Seed-taking overloads
+// (draft / build_cache / verify_rows with a uint64 seed) start a fresh
+// Stream(seed).
 #pragma once
 
 #include <algorithm>
@@ -156,6 +162,19 @@ inline double critical_batch(double hit_rate, double hit_tokens, double miss_tok
   return out;
 }
 
+// ---------------------------------------------------------------- rng.hpp:29-48
+class Stream {
+ public:
+  explicit Stream(std::uint64_t seed) { ssd_rng_stream_seed(&s_, seed); }
+  std::uint64_t next_u64() { return ssd_rng_stream_next_u64(&s_); }
+  double next_uniform() { return ssd_rng_stream_next_uniform(&s_); }
+  ssd_rng_stream* c() { return &s_; }
+
+ private:
+  ssd_rng_stream s_{};
+};
+inline std::uint64_t derive_seed(std::uint64_t root, std::uint64_t index) { return ssd_derive_seed(root, index); }
+
 // ---------------------------------------------------------- specdec.hpp:22-52
 struct Speculation {
   std::vector<int> tokens;
@@ -169,6 +188,14 @@ struct VerificationOutcome {
   bool operator<(const VerificationOutcome& o) const {
     return accepted != o.accepted ? accepted < o.accepted : bonus < o.bonus;
   }
+};
+struct RoundResult {  // specdec.hpp:44-52
+  VerificationOutcome outcome;
+  std::vector<int> emitted;
+};
+struct VerifyOptions {  // specdec.hpp:63-79
+  SamplingScheme target_scheme = SamplingScheme::standard();
+  double accept_scale = 1.0;
 };
 
 // cache.hpp:114-135: immutable after build; lookup returns a non-owning
@@ -223,6 +250,7 @@ struct RunResult {
   std::vector<std::vector<int>> streams;       // run_ssd: one per batch sequence
   std::vector<VerificationOutcome> outcomes;  // run_ssd only
   std::vector<int> hits;                      // run_ssd only (-1 on the last round)
+  std::string transcript_jsonl;               // run_ssd(..., with_transcript): Transcript::to_jsonl (sim.cpp:489-500)
   double hit_rate() const {
     const long l = stats.primary_origin_lookups + stats.backup_origin_lookups;
     return l ? double(stats.primary_origin_hits + stats.backup_origin_hits) / double(l) : 0.0;
@@ -263,6 +291,93 @@ class Engine {
                     with_rows ? s.rows.data() : nullptr));
     s.origin = origin;
     return s;
+  }
+
+  // specdec::draft (specdec.hpp:59-61) drawing from the caller's Stream
+  Speculation draft(std::span<const int> ctx, int lookahead, const SamplingScheme& scheme, Stream& rng,
+                    Origin origin = Origin::Primary) const {
+    Speculation s;
+    s.tokens.resize(size_t(lookahead));
+    s.rows.resize(size_t(lookahead) * size_t(vocab_));
+    const ssd_scheme sc = scheme.c();
+    check(ssd_draft_stream(h_.get(), ctx.data(), int(ctx.size()), lookahead, &sc, rng.c(), s.tokens.data(),
+                           s.rows.data()));
+    s.origin = origin;
+    return s;
+  }
+
+  // specdec::verify (specdec.hpp:81-83): the target's verify forward over
+  // ctx || spec plus the fused decision, coins and bonus from `rng`;
+  // draft_scheme is the law spec.rows were drawn under
+  RoundResult verify(std::span<const int> ctx, const Speculation& spec, Stream& rng,
+                     const SamplingScheme& draft_scheme, const VerifyOptions& opt = {}) const {
+    const int K = int(spec.tokens.size());
+    if (!spec.rows.empty() && spec.rows.size() != size_t(K) * size_t(vocab_))
+      throw Error("verify: speculation rows must be [K][V]");
+    const ssd_scheme ds = draft_scheme.c(), ts = opt.target_scheme.c();
+    RoundResult r;
+    r.emitted.resize(size_t(K + 1));
+    check(ssd_verify(h_.get(), ctx.data(), int(ctx.size()), spec.tokens.data(), K,
+                     spec.rows.empty() ? nullptr : spec.rows.data(), &ds, &ts, opt.accept_scale, rng.c(),
+                     &r.outcome.accepted, &r.outcome.bonus, r.emitted.data()));
+    r.emitted.resize(size_t(r.outcome.accepted + 1));
+    return r;
+  }
+
+  // cache::build_cache (cache.hpp:149-154): one next_u64 from `rng`, entries
+  // of next_lookahead tokens with the draft rows they were drawn from
+  SpeculationCache build_cache(std::span<const int> ctx, const Speculation& spec, const FanOutPlan& plan,
+                               const SamplingScheme& scheme, int next_lookahead, Stream& rng) const {
+    if (plan.role != spec.origin) throw Error("build_cache: plan role does not match speculation origin");
+    const ssd_plan p = plan.c();
+    const ssd_scheme sc = scheme.c();
+    const int tot = std::max(1, plan.total());
+    std::vector<int> keys(size_t(2 * tot)), toks(size_t(tot) * size_t(next_lookahead));
+    std::vector<float> rows(size_t(tot) * size_t(next_lookahead) * size_t(vocab_));
+    int count = 0;
+    check(ssd_build_cache_stream(h_.get(), ctx.data(), int(ctx.size()), spec.tokens.data(), int(spec.tokens.size()),
+                                 &p, &sc, next_lookahead, rng.c(), keys.data(), toks.data(), rows.data(), &count));
+    SpeculationCache c;
+    c.role = plan.role;
+    const size_t per = size_t(next_lookahead) * size_t(vocab_);
+    for (int i = 0; i < count; ++i) {
+      Speculation e;
+      e.tokens.assign(toks.begin() + i * next_lookahead, toks.begin() + (i + 1) * next_lookahead);
+      e.rows.assign(rows.begin() + long(i * per), rows.begin() + long((i + 1) * per));
+      e.origin = Origin::Primary;
+      c.entries_.emplace(VerificationOutcome{keys[size_t(2 * i)], keys[size_t(2 * i + 1)]}, std::move(e));
+    }
+    return c;
+  }
+
+  // Asynchronous pre-speculation of DEVICE buffers ordered after
+  // `cuda_stream`; lookups wait for it
+  void prespec_begin(const int32_t* d_ctx, int n, const int32_t* d_spec, int lookahead, const FanOutPlan& plan,
+                     const SamplingScheme& scheme, int next_lookahead, Stream& rng, void* cuda_stream = nullptr) {
+    const ssd_plan p = plan.c();
+    const ssd_scheme sc = scheme.c();
+    check(ssd_prespec_begin(h_.get(), d_ctx, n, d_spec, lookahead, &p, &sc, next_lookahead, rng.c(), cuda_stream));
+  }
+  int cache_lookup(const VerificationOutcome& key) const {
+    int slot = -1;
+    check(ssd_cache_lookup(h_.get(), key.accepted, key.bonus, &slot));
+    return slot;
+  }
+  std::vector<VerificationOutcome> cache_keys() const {
+    int n = 0;
+    check(ssd_cache_keys(h_.get(), nullptr, &n));
+    std::vector<int> k(size_t(2 * std::max(n, 1)));
+    check(ssd_cache_keys(h_.get(), k.data(), &n));
+    std::vector<VerificationOutcome> out;
+    for (int i = 0; i < n; ++i) out.push_back({k[size_t(2 * i)], k[size_t(2 * i + 1)]});
+    return out;
+  }
+  Speculation cache_entry(int slot, int next_lookahead) const {
+    Speculation e;
+    e.tokens.resize(size_t(next_lookahead));
+    e.rows.resize(size_t(next_lookahead) * size_t(vocab_));
+    check(ssd_cache_entry(h_.get(), slot, e.tokens.data(), e.rows.data()));
+    return e;
   }
 
   // specdec::verify decision (specdec.cpp:27-69) on target rows [K+1][V] and
@@ -323,8 +438,18 @@ class Engine {
     return r;
   }
 
-  // sim::run_protocol_harness (sim.cpp:502-601), cfg.batch_size sequences
-  RunResult run_ssd(std::span<const int> prompt, const SimConfig& cfg) const {
+  // sim::run_protocol_harness (sim.cpp:502-601), cfg.batch_size sequences;
+  // with_transcript: the JSONL round transcript (sim.cpp:489-500)
+  RunResult run_ssd(std::span<const int> prompt, const SimConfig& cfg, bool with_transcript = false) const {
+    return run(prompt, cfg, SSD_SEMANTICS_HARNESS, with_transcript);
+  }
+  // sim::run_ssd / run_ssd_batch (sim.cpp:123-250)
+  RunResult run_ssd_sequential(std::span<const int> prompt, const SimConfig& cfg) const {
+    return run(prompt, cfg, SSD_SEMANTICS_SEQUENTIAL, false);
+  }
+
+ private:
+  RunResult run(std::span<const int> prompt, const SimConfig& cfg, int semantics, bool with_transcript) const {
     RunResult r;
     const long cap = cfg.rounds * (cfg.lookahead + 1);
     const int b = cfg.batch_size;
@@ -333,8 +458,22 @@ class Engine {
     std::vector<int> oc(size_t(2 * cfg.rounds));
     r.hits.resize(size_t(cfg.rounds));
     const ssd_sim_config c = cfg.c();
-    check(ssd_run_ssd_batch(h_.get(), prompt.data(), int(prompt.size()), &c, b, all.data(), cap, lens.data(),
-                            oc.data(), r.hits.data(), &r.stats));
+    ssd_run_options opt{};
+    opt.semantics = semantics;
+    int64_t need = 0;
+    std::vector<char> tbuf;
+    if (with_transcript) {
+      tbuf.resize(size_t(4096 + cfg.rounds * b * (96 + 16 * (cfg.lookahead + 4)) + 256 * cfg.rounds));
+      opt.transcript = tbuf.data();
+      opt.transcript_cap = int64_t(tbuf.size());
+      opt.transcript_len = &need;
+    }
+    check(ssd_run_ssd_ex(h_.get(), prompt.data(), int(prompt.size()), &c, b, &opt, all.data(), cap, lens.data(),
+                         oc.data(), r.hits.data(), &r.stats));
+    if (with_transcript) {
+      if (need >= int64_t(tbuf.size())) throw Error("transcript: buffer too small");
+      r.transcript_jsonl.assign(tbuf.data(), size_t(need));
+    }
     for (int j = 0; j < b; ++j)
       r.streams.emplace_back(all.begin() + long(j) * cap, all.begin() + long(j) * cap + lens[size_t(j)]);
     r.tokens = r.streams[0];
@@ -342,7 +481,6 @@ class Engine {
     return r;
   }
 
- private:
   struct Del {
     void operator()(ssd_engine* e) const { ssd_engine_destroy(e); }
   };

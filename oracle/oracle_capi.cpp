@@ -266,6 +266,33 @@ json run(const json& req) {
     return json{{"keys", keys}};
   }
   Models m = resolve(req);
+  if (op == "chain") {
+    // One caller stream through draft -> verify -> build_cache, as a reference
+    // caller threads its rng::Stream& (specdec.hpp:59-61, 81-83; cache.hpp:149-154);
+    // "next_u64" = the stream's next draw afterwards (its position).
+    const Scheme s = parse_scheme(req.value("scheme", json()));
+    const int K = req.at("lookahead");
+    const auto ctx = req.at("context").get<std::vector<int>>();
+    Rng rng(req.at("seed").get<std::uint64_t>());
+    const Spec spec = draft_tokens(*m.draft, ctx, K, s, rng, Origin::Primary);
+    VerifyOpts vo;
+    if (req.contains("target_scheme")) vo.target_scheme = parse_scheme(req.at("target_scheme"));
+    else vo.target_scheme.temperature = s.temperature;
+    vo.accept_scale = req.value("accept_scale", 1.0);
+    const Round r = verify_spec(*m.target, ctx, spec, rng, vo);
+    const Plan plan = parse_plan(req.at("plan"), K, Origin::Primary);
+    const SpecCache c = prespeculate(*m.draft, ctx, spec, plan, s, req.value("next_lookahead", K), rng);
+    json entries = json::array();
+    for (const auto& e : c.entries) entries.push_back({e.key.k, e.key.t, e.spec.tokens});
+    json o;
+    o["spec"] = spec_json(spec, false);
+    o["accepted"] = r.key.k;
+    o["bonus"] = r.key.t;
+    o["emitted"] = r.emitted;
+    o["entries"] = entries;
+    o["next_u64"] = rng.bits();
+    return o;
+  }
   if (op == "draft" || op == "verify" || op == "build_cache") {
     const Scheme s = parse_scheme(req.value("scheme", json()));
     const int K = req.at("lookahead");

@@ -54,6 +54,11 @@ class RunStatsC(C.Structure):
 SEMANTICS_HARNESS, SEMANTICS_SEQUENTIAL = 0, 1
 
 
+class RngStream(C.Structure):
+    """ssd_rng_stream: the mt19937_64 state of rng::Stream (rng.hpp:29-48)."""
+    _fields_ = [("state", C.c_uint64 * 312), ("index", C.c_int32), ("reserved_", C.c_int32)]
+
+
 class RunOptionsC(C.Structure):
     _fields_ = [("semantics", C.c_int32), ("transcript", C.c_char_p), ("transcript_cap", C.c_int64),
                 ("transcript_len", C.POINTER(C.c_int64))]
@@ -113,6 +118,20 @@ SIGNATURES = {
                                       P(C.c_double), i64p, i32p]),
     "ssd_bench_read_bw": (C.c_int, [EngineP, C.c_int64, C.c_int32, P(C.c_double)]),
     "ssd_profile_ssd_round": (C.c_int, [EngineP, i32p, C.c_int32, P(SimConfigC), P(C.c_double), P(RunStatsC)]),
+    "ssd_rng_stream_seed": (None, [P(RngStream), C.c_uint64]),
+    "ssd_rng_stream_next_u64": (C.c_uint64, [P(RngStream)]),
+    "ssd_rng_stream_next_uniform": (C.c_double, [P(RngStream)]),
+    "ssd_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "ssd_draft_stream": (C.c_int, [EngineP, i32p, C.c_int32, C.c_int32, P(Scheme), P(RngStream), i32p, f32p]),
+    "ssd_verify": (C.c_int, [EngineP, i32p, C.c_int32, i32p, C.c_int32, f32p, P(Scheme), P(Scheme), C.c_double,
+                             P(RngStream), i32p, i32p, i32p]),
+    "ssd_build_cache_stream": (C.c_int, [EngineP, i32p, C.c_int32, i32p, C.c_int32, P(Plan), P(Scheme), C.c_int32,
+                                         P(RngStream), i32p, i32p, f32p, i32p]),
+    "ssd_prespec_begin": (C.c_int, [EngineP, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, P(Plan), P(Scheme),
+                                    C.c_int32, P(RngStream), C.c_void_p]),
+    "ssd_cache_lookup": (C.c_int, [EngineP, C.c_int32, C.c_int32, i32p]),
+    "ssd_cache_keys": (C.c_int, [EngineP, i32p, i32p]),
+    "ssd_cache_entry": (C.c_int, [EngineP, C.c_int32, i32p, f32p]),
     "ssd_rng_u64": (C.c_int, [EngineP, C.c_uint64, C.c_int32, u64p]),
     "ssd_weight_bits": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, C.c_int32, u16p]),
 }

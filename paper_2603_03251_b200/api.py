@@ -249,6 +249,42 @@ class RunStats:
         return self.tokens / (self.device_ms * 1e-3) if self.device_ms > 0 else 0.0
 
 
+class Stream:
+    """rng::Stream (rng.hpp:29-48): a caller-owned mt19937_64 stream. Engine
+    calls that take it advance it exactly as the reference advances the
+    Stream& it is given (one uniform per draw, one next_u64 per build_cache)."""
+
+    def __init__(self, seed: int):
+        self.c = N.RngStream()
+        N.load().ssd_rng_stream_seed(C.byref(self.c), int(seed) & 0xFFFFFFFFFFFFFFFF)
+
+    def next_u64(self) -> int:
+        return int(N.load().ssd_rng_stream_next_u64(C.byref(self.c)))
+
+    def next_uniform(self) -> float:
+        return float(N.load().ssd_rng_stream_next_uniform(C.byref(self.c)))
+
+    def copy(self) -> "Stream":
+        s = Stream.__new__(Stream)
+        s.c = N.RngStream()
+        C.memmove(C.byref(s.c), C.byref(self.c), C.sizeof(N.RngStream))
+        return s
+
+
+def derive_seed(root: int, index: int) -> int:
+    """rng::derive_seed (rng.hpp:24-26)."""
+    return int(N.load().ssd_derive_seed(int(root) & 0xFFFFFFFFFFFFFFFF, int(index) & 0xFFFFFFFFFFFFFFFF))
+
+
+@dataclass
+class RoundResult:
+    """specdec::RoundResult (specdec.hpp:44-52): outcome (k, t*) and the
+    emitted tokens (accepted prefix + bonus)."""
+    accepted: int
+    bonus: int
+    emitted: list
+
+
 @dataclass
 class Speculation:
     """specdec::Speculation (specdec.hpp:22-28): tokens plus the draft logit
@@ -264,9 +300,17 @@ class SpeculationCache:
     """cache::SpeculationCache (cache.hpp:114-135): (accepted, bonus) -> tokens."""
     entries: dict
     round_origin: int = PRIMARY
+    rows: Optional[dict] = None  # (k, t) -> [next_K][V] draft logit rows (build_cache_stream)
 
     def lookup(self, accepted: int, bonus: int):
         return self.entries.get((accepted, bonus))
+
+    def speculation(self, accepted: int, bonus: int) -> Optional["Speculation"]:
+        """The stored Speculation (tokens + the rows they were drawn from)."""
+        t = self.entries.get((accepted, bonus))
+        if t is None:
+            return None
+        return Speculation(list(t), None if self.rows is None else self.rows[(accepted, bonus)], PRIMARY)
 
     def size(self) -> int:
         return len(self.entries)
@@ -502,6 +546,88 @@ class Engine:
         for i in range(cnt.value):
             entries[(int(keys[2 * i]), int(keys[2 * i + 1]))] = toks[i * next_lookahead:(i + 1) * next_lookahead].tolist()
         return SpeculationCache(entries, plan.role)
+
+    # ---- the reference's Stream&-taking interface (specdec.hpp / cache.hpp)
+    def draft_tokens(self, context: Sequence[int], lookahead: int, scheme: SamplingScheme, rng: Stream,
+                     origin: int = PRIMARY) -> Speculation:
+        """specdec::draft (specdec.hpp:59-61) with the caller's stream (named
+        draft_tokens here: `Engine.draft` is the draft model's shape)."""
+        c = _i32(context)
+        toks = np.zeros(lookahead, dtype=np.int32)
+        rows = np.zeros((lookahead, self.vocab), dtype=np.float32)
+        _check(self.lib.ssd_draft_stream(self.h, _ptr(c, C.c_int32), len(c), lookahead, C.byref(scheme.c()),
+                                         C.byref(rng.c), _ptr(toks, C.c_int32), _ptr(rows, C.c_float)))
+        return Speculation(toks.tolist(), rows, origin)
+
+    def verify(self, context: Sequence[int], spec: Speculation, rng: Stream,
+               draft_scheme: Optional[SamplingScheme] = None, target_scheme: Optional[SamplingScheme] = None,
+               accept_scale: float = 1.0) -> RoundResult:
+        """specdec::verify (specdec.hpp:81-83): target forward over context ||
+        spec + the fused decision, with the caller's stream. spec.rows None =
+        uniform dists (the FastRandom backup)."""
+        ds = draft_scheme or SamplingScheme.standard()
+        ts = target_scheme or SamplingScheme.standard(ds.temperature)
+        c = _i32(context)
+        t = _i32(spec.tokens)
+        K = len(t)
+        rows = None if spec.rows is None else np.ascontiguousarray(spec.rows, dtype=np.float32)
+        acc, bonus = C.c_int32(), C.c_int32()
+        em = np.zeros(K + 1, dtype=np.int32)
+        _check(self.lib.ssd_verify(self.h, _ptr(c, C.c_int32), len(c), _ptr(t, C.c_int32), K,
+                                   None if rows is None else _ptr(rows, C.c_float), C.byref(ds.c()), C.byref(ts.c()),
+                                   accept_scale, C.byref(rng.c), C.byref(acc), C.byref(bonus), _ptr(em, C.c_int32)))
+        return RoundResult(acc.value, bonus.value, em[: acc.value + 1].tolist())
+
+    def build_cache_stream(self, context: Sequence[int], spec: Speculation, plan: FanOutPlan, scheme: SamplingScheme,
+                           next_lookahead: int, rng: Stream, with_rows: bool = True) -> SpeculationCache:
+        """cache::build_cache (cache.hpp:149-154) with the caller's stream,
+        any next_lookahead, and each entry's draft rows."""
+        c = _i32(context)
+        s = _i32(spec.tokens)
+        tot = plan.total()
+        keys = np.zeros(2 * max(tot, 1), dtype=np.int32)
+        toks = np.zeros(max(tot, 1) * next_lookahead, dtype=np.int32)
+        rows = np.zeros((max(tot, 1), next_lookahead, self.vocab), dtype=np.float32) if with_rows else None
+        cnt = C.c_int32()
+        _check(self.lib.ssd_build_cache_stream(self.h, _ptr(c, C.c_int32), len(c), _ptr(s, C.c_int32), len(s),
+                                               C.byref(plan.c()), C.byref(scheme.c()), next_lookahead, C.byref(rng.c),
+                                               _ptr(keys, C.c_int32), _ptr(toks, C.c_int32),
+                                               _ptr(rows, C.c_float) if with_rows else None, C.byref(cnt)))
+        entries, erows = {}, ({} if with_rows else None)
+        for i in range(cnt.value):
+            key = (int(keys[2 * i]), int(keys[2 * i + 1]))
+            entries[key] = toks[i * next_lookahead:(i + 1) * next_lookahead].tolist()
+            if with_rows:
+                erows[key] = rows[i]
+        return SpeculationCache(entries, plan.role, erows)
+
+    # ---- asynchronous pre-speculation on device buffers (SURVEY §8b)
+    def prespec_begin(self, d_context, n: int, d_spec, lookahead: int, plan: FanOutPlan, scheme: SamplingScheme,
+                      next_lookahead: int, rng: Stream, cuda_stream: int = 0):
+        """d_context / d_spec: device pointers (int32); cuda_stream: a
+        cudaStream_t handle whose queued work produces them (0 = none)."""
+        _check(self.lib.ssd_prespec_begin(self.h, C.c_void_p(int(d_context)), n, C.c_void_p(int(d_spec)), lookahead,
+                                          C.byref(plan.c()), C.byref(scheme.c()), next_lookahead, C.byref(rng.c),
+                                          C.c_void_p(int(cuda_stream)) if cuda_stream else None))
+
+    def cache_lookup(self, accepted: int, bonus: int) -> int:
+        slot = C.c_int32()
+        _check(self.lib.ssd_cache_lookup(self.h, accepted, bonus, C.byref(slot)))
+        return slot.value
+
+    def cache_keys(self) -> list:
+        n = C.c_int32()
+        _check(self.lib.ssd_cache_keys(self.h, None, C.byref(n)))
+        keys = np.zeros(2 * max(n.value, 1), dtype=np.int32)
+        _check(self.lib.ssd_cache_keys(self.h, _ptr(keys, C.c_int32), C.byref(n)))
+        return [(int(keys[2 * i]), int(keys[2 * i + 1])) for i in range(n.value)]
+
+    def cache_entry(self, slot: int, next_lookahead: int, with_rows: bool = False):
+        toks = np.zeros(next_lookahead, dtype=np.int32)
+        rows = np.zeros((next_lookahead, self.vocab), dtype=np.float32) if with_rows else None
+        _check(self.lib.ssd_cache_entry(self.h, slot, _ptr(toks, C.c_int32),
+                                        _ptr(rows, C.c_float) if with_rows else None))
+        return toks.tolist(), rows
 
     # ---- kernel-level hooks
     def topk_keys(self, rows: np.ndarray, fan_out: Sequence[int], excluded: Sequence[int]) -> np.ndarray:

@@ -141,13 +141,13 @@ __host__ __device__ inline uint64_t derive_seed(uint64_t root, uint64_t index) {
   return splitmix64(root + (index + 1) * 0x9E3779B97F4A7C15ull);
 }
 
-__device__ inline void mt_seed(Mt64& m, uint64_t seed) {
+__host__ __device__ inline void mt_seed(Mt64& m, uint64_t seed) {
   m.s[0] = seed;
   for (int k = 1; k < 312; ++k) m.s[k] = 6364136223846793005ull * (m.s[k - 1] ^ (m.s[k - 1] >> 62)) + uint64_t(k);
   m.i = 312;
 }
 
-__device__ inline uint64_t mt_next(Mt64& m) {
+__host__ __device__ inline uint64_t mt_next(Mt64& m) {
   if (m.i >= 312) {
     const uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
     for (int k = 0; k < 312; ++k) {
@@ -167,7 +167,7 @@ __device__ inline uint64_t mt_next(Mt64& m) {
 }
 
 // rng.hpp:39-41: one engine step per uniform, top 53 bits.
-__device__ inline double mt_unit(Mt64& m) { return double(mt_next(m) >> 11) * 0x1.0p-53; }
+__host__ __device__ inline double mt_unit(Mt64& m) { return double(mt_next(m) >> 11) * 0x1.0p-53; }
 
 // ----------------------------------------------------------- bf16
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {

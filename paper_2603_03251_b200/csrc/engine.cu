@@ -217,6 +217,11 @@ struct Engine {
   int attn_dec_wide_m = 20;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   int cl_min_m = 17;                     // SSD_B200_CL_MIN_M: ... for forwards of at least this many tokens
+  // Deterministic forwards (fixed fp32 summation order: partials + ordered
+  // last-arriver reduction, residual adds in the norm kernel). Forced for the
+  // split roles, whose speculators must compute bit-identical key tables in
+  // separate processes, and for TP; SSD_B200_DETERMINISTIC=1 elsewhere.
+  int deterministic = 0;
   long long small_gemm_bytes = 0;  // SSD_B200_SMALL_GEMM_MB: co-resident GEMM config up to this size (off: no gain measured)
   // ... inside the colocated SSD round, where the verifier and speculator
   // streams run at once: the 108 KB co-resident GEMM config lets their CTAs
@@ -249,6 +254,11 @@ struct Engine {
   // at the segment boundaries of both streams; kProfMarks per round.
   int prof_on = 0;
   cudaEvent_t prof_ev[32] = {};
+  // asynchronous pre-speculation session (ssd_prespec_begin / ssd_cache_*)
+  cudaEvent_t ev_prespec = nullptr, ev_user = nullptr;
+  int pre_active = 0, pre_count = 0, pre_kb = 0, pre_keys_valid = 0;
+  std::vector<int> pre_keys;         // [2 * count] host copy after completion
+  Mt64* pin_rng = nullptr;           // pinned staging of a caller stream
   // tensor-parallel verifier (tp.cuh)
   char* tp_region = nullptr;         // this rank's IPC-exported region
   TpLayout tp_L{};
@@ -482,7 +492,7 @@ static const CUtensorMap& act_map(Model& m, const void* X, int K, int np) {
 
 template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                           cudaStream_t s, Prefetch pf) {
+                           cudaStream_t s, Prefetch pf, int atomic = 0) {
   using C = tc::Cfg<NP, BUDGET_KB>;
   const int tiles = (W.N + tc::kBM - 1) / tc::kBM;
   const int KU = W.K / (tc::kBK * tc::kKPS);
@@ -496,7 +506,7 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
   const int grid = std::min(units, cap);
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
   static int dbg_seq = 0;
-  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++};
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++, EPI == EPI_SWIGLU ? 0 : atomic};
   launch_pdl(tc::gemm_tc_kernel<EPI, NP, BUDGET_KB>, dim3(grid), dim3(tc::kThreads), C::kSmem, s, act_map(m, X, W.K, NP),
              g);
 }
@@ -508,7 +518,7 @@ static void gemm_cl_launch(Model& m, const WMat& W, const bf16* X, int M, float*
   using C = tc::ClCfg<NP, BUDGET_KB>;
   const int NC = E_num_sms / CS;
   const int KU = W.K / (tc::kBK * tc::kKPS);
-  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, 0};
+  tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, 0, 0};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(NC * CS);
   cfg.blockDim = dim3(tc::kThreads);
@@ -637,11 +647,13 @@ static void configure_kernels() {
   configure_gemm<EPI_STORE, 192>(); configure_gemm<EPI_SWIGLU, 192>();
   configure_gemm<EPI_STORE, 256>(); configure_gemm<EPI_SWIGLU, 256>();
   configure_gemm<EPI_STORE, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_SWIGLU, 16, tc::kSmallBudgetKB>();
-  configure_cl<EPI_STORE, 16, 2>(); configure_cl<EPI_STORE, 16, 4>(); configure_cl<EPI_STORE, 16, 8>();
-  configure_cl<EPI_SWIGLU, 16, 2>(); configure_cl<EPI_SWIGLU, 16, 4>(); configure_cl<EPI_SWIGLU, 16, 8>();
-  configure_cl<EPI_STORE, 16, 2, kClSmallBudgetKB>(); configure_cl<EPI_STORE, 16, 4, kClSmallBudgetKB>();
-  configure_cl<EPI_STORE, 16, 8, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 16, 2, kClSmallBudgetKB>();
-  configure_cl<EPI_SWIGLU, 16, 4, kClSmallBudgetKB>(); configure_cl<EPI_SWIGLU, 16, 8, kClSmallBudgetKB>();
+  configure_cl<EPI_RESID, 32, 2>(); configure_cl<EPI_RESID, 32, 4>(); configure_cl<EPI_RESID, 32, 8>();
+  configure_cl<EPI_RESID, 32, 2, kClSmallBudgetKB>(); configure_cl<EPI_RESID, 32, 4, kClSmallBudgetKB>();
+  configure_cl<EPI_RESID, 32, 8, kClSmallBudgetKB>();
+  configure_gemm<EPI_RESID, 16>(); configure_gemm<EPI_RESID, 32>(); configure_gemm<EPI_RESID, 48>();
+  configure_gemm<EPI_RESID, 64>(); configure_gemm<EPI_RESID, 96>(); configure_gemm<EPI_RESID, 128>();
+  configure_gemm<EPI_RESID, 192>(); configure_gemm<EPI_RESID, 256>();
+  configure_gemm<EPI_RESID, 16, tc::kSmallBudgetKB>(); configure_gemm<EPI_RESID, 32, tc::kSmallBudgetKB>();
   configure_cl<EPI_STORE, 32, 2>(); configure_cl<EPI_STORE, 32, 4>(); configure_cl<EPI_STORE, 32, 8>();
   configure_cl<EPI_SWIGLU, 32, 2>(); configure_cl<EPI_SWIGLU, 32, 4>(); configure_cl<EPI_SWIGLU, 32, 8>();
   configure_cl<EPI_STORE, 32, 2, kClSmallBudgetKB>(); configure_cl<EPI_STORE, 32, 4, kClSmallBudgetKB>();
@@ -698,32 +710,36 @@ struct GraphSet {
   }
 };
 
+// atomic: split tiles accumulate into Y with fp32 atomics (gemm_tc.cuh
+// GemmArgs::atomic; Y pre-zeroed for EPI_STORE). The cluster GEMM reduces
+// over DSMEM and applies the epilogue once per element either way.
 template <int EPI>
 static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, float* Y, int ldy, bf16* Yb, int ldyb,
-                   cudaStream_t s, Prefetch pf) {
+                   cudaStream_t s, Prefetch pf, int atomic = 0) {
   ++E.launches;
   // small weight matrices at branch widths (17..32 tokens): cluster split-K.
   // Measured: faster than stream-K for the 1B branch step (M = 20), slower at
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
-  if (W.bytes <= E.cl_gemm_bytes && M >= E.cl_min_m && M <= 32 && m.gemm_ctas == 0) {
-    if (M <= 16) gemm_cl_dispatch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
-    else gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
+  // (M <= 16 measured slower with the cluster kernel too: 1B step 1.29 vs
+  // 1.13 ms, r02 profiles/r02_summary.md)
+  if (W.bytes <= E.cl_gemm_bytes && M >= E.cl_min_m && M > 16 && M <= 32 && m.gemm_ctas == 0) {
+    gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
     return;
   }
   // small weight matrices: the co-resident (small-budget) configuration
   if (W.bytes <= E.small_gemm_bytes && M <= 32) {
-    if (M <= 16) gemm_tc_launch<EPI, 16, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-    else gemm_tc_launch<EPI, 32, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+    if (M <= 16) gemm_tc_launch<EPI, 16, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+    else gemm_tc_launch<EPI, 32, tc::kSmallBudgetKB>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
     return;
   }
-  if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 64) gemm_tc_launch<EPI, 64>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 96) gemm_tc_launch<EPI, 96>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 128) gemm_tc_launch<EPI, 128>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else if (M <= 192) gemm_tc_launch<EPI, 192>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
-  else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf);
+  if (M <= 16) gemm_tc_launch<EPI, 16>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 32) gemm_tc_launch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 48) gemm_tc_launch<EPI, 48>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 64) gemm_tc_launch<EPI, 64>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 96) gemm_tc_launch<EPI, 96>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 128) gemm_tc_launch<EPI, 128>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else if (M <= 192) gemm_tc_launch<EPI, 192>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
+  else gemm_tc_launch<EPI, 256>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, atomic);
 }
 
 // L2 prefetch cursor over the GEMM sequence of one forward: the stream
@@ -903,15 +919,20 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
   const AttnWs aws{m.attn_part, m.attn_cnt};
   // E.skip_mask: profiling only (results are wrong): 1 = norms, 2 = attention
   const bool do_norm = !(E.skip_mask & 1), do_attn = !(E.skip_mask & 2);
+  const int fused = (!E.deterministic && m.tp_size == 1) ? 1 : 0;
   for (int l = 0; l < sh.n_layers; ++l) {
     const DevLayer& L = m.layers[size_t(l)];
     bf16* kc = m.kc + size_t(l) * m.kv_layer_elems();
     bf16* vc = m.vc + size_t(l) * m.kv_layer_elems();
-    // x += (previous layer's down projection); xb = norm(x)
+    // fused residual: the O / down projections add into x
+    // in their epilogues (EPI_RESID); otherwise (deterministic / TP engines)
+    // they store deltas that the next norm adds. xb = norm(x); the fused
+    // path also clears the QKV output for its atomic split-K accumulation.
     if (do_norm)
-      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(l > 0 ? m.dlt2 : nullptr), d,
-                 (const float*)nullptr, sh.norm_eps, m.xb, pf.upto(4 * l));
-    linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
+      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x,
+                 (const float*)(l > 0 && !fused ? m.dlt2 : nullptr), d, (const float*)nullptr, sh.norm_eps, m.xb,
+                 pf.upto(4 * l), fused ? m.qkv : nullptr, nqkv);
+    linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l), fused);
     if (do_attn && E.attn_dec && (size_t(M) * KVH <= size_t(E_num_sms) || M >= E.attn_dec_wide_m) &&
         attn_dec_launch(m, M, P, kc, vc, scale, s, pf.upto(4 * l + 1))) {
       // one CTA per (kv head, token) while they fit one wave (decode, verify,
@@ -924,20 +945,29 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
       launch_pdl(k, dim3(nch, KVH, M), dim3(kAttnThreads), 0, s, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
                  (const float*)m.rope_sin, kc, vc, m.S, H, KVH, hd, scale, m.attn, aws, pf.upto(4 * l + 1));
     }
-    linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
-    if (m.tp_size > 1) tp_allreduce(E, m, m.dlt1, M, s);  // row-parallel O: sum the shards
-    // x += attention projection; xb = norm(x) * g
+    if (fused) {
+      linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s, pf.after(4 * l + 1), 1);
+    } else {
+      linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
+      if (m.tp_size > 1) tp_allreduce(E, m, m.dlt1, M, s);  // row-parallel O: sum the shards
+    }
+    // (x += attention projection); xb = norm(x) * g
     if (do_norm)
-      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt1, d,
-                 (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb, pf.upto(4 * l + 2));
+      launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(fused ? nullptr : m.dlt1), d,
+                 (const float*)(l == 0 ? m.ffn_gain0 : nullptr), sh.norm_eps, m.xb, pf.upto(4 * l + 2),
+                 (float*)nullptr, 0);
     linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s, pf.after(4 * l + 2));
-    linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
-    if (m.tp_size > 1) tp_allreduce(E, m, m.dlt2, M, s);  // row-parallel down projection
+    if (fused) {
+      linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s, pf.after(4 * l + 3), 1);
+    } else {
+      linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
+      if (m.tp_size > 1) tp_allreduce(E, m, m.dlt2, M, s);  // row-parallel down projection
+    }
     E.launches += 3;
   }
   if (logits) {
-    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)m.dlt2, d,
-               (const float*)m.final_gain, sh.norm_eps, m.xb, pf.upto(4 * sh.n_layers));
+    launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, s, m.x, (const float*)(fused ? nullptr : m.dlt2), d,
+               (const float*)m.final_gain, sh.norm_eps, m.xb, pf.upto(4 * sh.n_layers), (float*)nullptr, 0);
     if (m.tp_size > 1) {  // vocabulary-parallel head: local shard, then all-gather the rows
       linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits_shard, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
       tp_gather_logits_kernel<<<64, 256, 0, s>>>(m.logits_shard, M, sh.vocab, logits, E.tp_L, E.tp_peers, m.tp_rank,
@@ -1318,6 +1348,8 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
+  E.deterministic = role != SSD_ROLE_COLOCATED || tp_size > 1;
+  if (const char* dt = std::getenv("SSD_B200_DETERMINISTIC")) E.deterministic = E.deterministic || std::atoi(dt) != 0;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
@@ -1354,6 +1386,9 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   CK(cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming));
   CK(cudaEventCreate(&E.ev_t0));
   CK(cudaEventCreate(&E.ev_t1));
+  CK(cudaEventCreateWithFlags(&E.ev_prespec, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&E.ev_user, cudaEventDisableTiming));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&E.pin_rng), sizeof(Mt64), cudaHostAllocDefault));
   auto own = [&](void* p) { E.owned.push_back(p); return p; };
   const int K = max_lookahead, B = max_branches, V = E.V;
   E.st = static_cast<LoopState*>(own(dalloc<LoopState>(size_t(nb))));
@@ -1447,8 +1482,9 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   for (void* p : E.owned) cudaFree(p);
   for (cudaStream_t st : {E.sv, E.ss})
     if (st) cudaStreamDestroy(st);
-  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1})
+  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1, E.ev_prespec, E.ev_user})
     if (ev) cudaEventDestroy(ev);
+  if (E.pin_rng) cudaFreeHost(E.pin_rng);
   for (cudaEvent_t ev : E.prof_ev)
     if (ev) cudaEventDestroy(ev);
   cudaGetLastError();  // teardown errors must not surface in a later call
@@ -2190,6 +2226,245 @@ ssd_status ssd_build_cache(ssd_engine* h, const int32_t* ctx, int32_t n, const i
   API_END
 }
 
+static_assert(sizeof(ssd_rng_stream) == sizeof(Mt64), "ssd_rng_stream mirrors the device stream");
+
+void ssd_rng_stream_seed(ssd_rng_stream* s, uint64_t seed) { mt_seed(*reinterpret_cast<Mt64*>(s), seed); }
+uint64_t ssd_rng_stream_next_u64(ssd_rng_stream* s) { return mt_next(*reinterpret_cast<Mt64*>(s)); }
+double ssd_rng_stream_next_uniform(ssd_rng_stream* s) { return mt_unit(*reinterpret_cast<Mt64*>(s)); }
+uint64_t ssd_derive_seed(uint64_t root, uint64_t index) { return derive_seed(root, index); }
+
+// The caller's stream into / out of lane 0's draft stream (the single stream
+// of draft / verify / build_cache calls).
+static void put_stream(Engine& E, const ssd_rng_stream* r) {
+  if (!r) throw Fail(SSD_CONFIG, "rng stream required");
+  h2d(E, &E.st->drng, r, sizeof(Mt64));
+}
+static void get_stream(Engine& E, ssd_rng_stream* r) { d2h(E, r, &E.st->drng, sizeof(Mt64)); }
+
+static void check_tokens(const int32_t* t, int n, int V, const char* what) {
+  if (n > 0 && !t) throw Fail(SSD_CONFIG, std::string(what) + ": null tokens");
+  for (int i = 0; i < n; ++i)
+    if (t[i] < 0 || t[i] >= V) throw Fail(SSD_ERROR, "context_index: token out of range");
+}
+
+ssd_status ssd_draft_stream(ssd_engine* h, const int32_t* ctx, int32_t n, int32_t K, const ssd_scheme* sc,
+                            ssd_rng_stream* rng, int32_t* out_tokens, float* out_rows) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  need(E.D, "draft");
+  if (K < 1) throw Fail(SSD_ERROR, "draft: lookahead must be >= 1");
+  if (K > E.maxK) throw Fail(SSD_TOO_LARGE, "draft: lookahead exceeds the engine's capacity");
+  if (!sc || !out_tokens) throw Fail(SSD_CONFIG, "draft: scheme and output required");
+  check_scheme(*sc, E.V);
+  set_history(E, ctx, n, n + K + 1);
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n, 1, 0, 0, nullptr, s);
+  put_stream(E, rng);
+  if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
+  draft_steps(E, K, *sc, 0, 0, s);
+  CK(cudaStreamSynchronize(s));
+  const LoopState st = read_state(E);
+  std::memcpy(out_tokens, st.spec, size_t(K) * 4);
+  if (out_rows) d2h(E, out_rows, E.dmain, size_t(K) * E.V * 4);
+  get_stream(E, rng);
+  API_END
+}
+
+ssd_status ssd_verify(ssd_engine* h, const int32_t* ctx, int32_t n, const int32_t* spec, int32_t K,
+                      const float* spec_rows, const ssd_scheme* ds, const ssd_scheme* ts, double scale,
+                      ssd_rng_stream* rng, int32_t* accepted, int32_t* bonus, int32_t* emitted) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  need(E.T, "verify");
+  if (K < 1) throw Fail(SSD_ERROR, "verify: empty speculation");
+  if (K > E.maxK) throw Fail(SSD_TOO_LARGE, "verify: lookahead exceeds the engine's capacity");
+  if (!ds || !ts || !accepted || !bonus) throw Fail(SSD_CONFIG, "verify: schemes and outputs required");
+  if (!(scale > 0.0) || scale > 1.0) throw Fail(SSD_ERROR, "verify: accept_scale must be in (0, 1]");
+  check_scheme(*ds, E.V);
+  check_scheme(*ts, E.V);
+  check_tokens(spec, K, E.V, "verify");
+  set_history(E, ctx, n, n + K + 2);
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n, 1, 0, 0, nullptr, s);
+  put_stream(E, rng);
+  {
+    int tmp[kMaxK];
+    std::memcpy(tmp, spec, size_t(K) * 4);
+    h2d(E, reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec), tmp, size_t(K) * 4);
+  }
+  if (spec_rows) {
+    h2d(E, E.dmain, spec_rows, size_t(K) * E.V * 4);
+    set_spec_rows_kernel<<<1, 32, 0, s>>>(E.st, E.dmain, E.V, 0, 0);
+    KCHECK();
+  } else {
+    const int one = 1;
+    h2d(E, reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec_uniform), &one, 4);
+  }
+  if (n > 1) prefill(E, E.T, n - 1, nullptr, s);
+  verify_round(E, K, *ts, *ds, scale, /*the caller's stream*/ 1, s);
+  CK(cudaStreamSynchronize(s));
+  const LoopState st = read_state(E);
+  raise_device_error(st);
+  *accepted = st.out_k;
+  *bonus = st.out_t;
+  if (emitted) d2h(E, emitted, E.hist + n, size_t(st.out_k + 1) * 4);
+  get_stream(E, rng);
+  API_END
+}
+
+// Shared by the synchronous and asynchronous build_cache: plan upload and
+// capacity checks; returns the entry count.
+static int prespec_setup(Engine& E, const ssd_plan* plan, const ssd_scheme* sc, int K, int next_K, int& B,
+                         int& max_f) {
+  need(E.D, "build_cache");
+  if (!plan || !sc) throw Fail(SSD_CONFIG, "build_cache: plan and scheme required");
+  if (plan->lookahead != K) throw Fail(SSD_ERROR, "build_cache: plan length does not match speculation");
+  if (K < 1 || K > E.maxK) throw Fail(SSD_TOO_LARGE, "build_cache: lookahead exceeds the engine's capacity");
+  if (next_K < 1) throw Fail(SSD_ERROR, "build_cache: next_lookahead must be >= 1");
+  if (next_K > E.maxK) throw Fail(SSD_TOO_LARGE, "build_cache: next_lookahead exceeds the engine's capacity");
+  check_scheme(*sc, E.V);
+  upload_plans(E, *plan, *plan, K, B, max_f);
+  int total = 0;
+  for (int k = 0; k <= K; ++k) total += plan->fan_out[k];
+  return total;
+}
+
+ssd_status ssd_build_cache_stream(ssd_engine* h, const int32_t* ctx, int32_t n, const int32_t* spec, int32_t K,
+                                  const ssd_plan* plan, const ssd_scheme* sc, int32_t next_K, ssd_rng_stream* rng,
+                                  int32_t* out_keys, int32_t* out_entry_tokens, float* out_entry_rows,
+                                  int32_t* out_count) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  int B = 0, max_f = 0;
+  const int total = prespec_setup(E, plan, sc, K, next_K, B, max_f);
+  check_tokens(spec, K, E.V, "build_cache");
+  set_history(E, ctx, n, n + K + next_K + 2);
+  cudaStream_t s = E.sv;
+  reset_state(E, K, n, 1, 0, 0, nullptr, s);
+  put_stream(E, rng);
+  {
+    int tmp[kMaxK + 1];
+    std::memcpy(tmp, spec, size_t(K) * 4);
+    h2d(E, reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec), tmp, size_t(K) * 4);
+    const int origin = plan->role;
+    h2d(E, reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec_origin), &origin, 4);
+    h2d(E, reinterpret_cast<char*>(E.st) + offsetof(LoopState, Kb), &next_K, 4);
+  }
+  if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
+  if (total > 0) prespeculate(E, K, B, 0, B, max_f, *sc, 0, s, 1, nullptr, next_K);
+  else branch_streams_kernel<<<1, 32, 0, s>>>(E.st, 0, E.bu, 0);  // the one next_u64 (cache.cpp:245)
+  KCHECK();
+  CK(cudaStreamSynchronize(s));
+  std::vector<int> bkh(static_cast<size_t>(B)), bth(static_cast<size_t>(B)), tt(static_cast<size_t>(B) * next_K);
+  d2h(E, bkh.data(), E.bk, size_t(B) * 4);
+  d2h(E, bth.data(), E.btok, size_t(B) * 4);
+  d2h(E, tt.data(), E.bt, size_t(B) * next_K * 4);
+  for (int i = 0; i < total; ++i) {
+    if (out_keys) { out_keys[2 * i] = bkh[size_t(i)]; out_keys[2 * i + 1] = bth[size_t(i)]; }
+    if (out_entry_tokens) std::memcpy(out_entry_tokens + size_t(i) * next_K, &tt[size_t(i) * next_K], size_t(next_K) * 4);
+    if (out_entry_rows)
+      for (int j = 0; j < next_K; ++j)  // branch rows are [j][B][V]
+        d2h(E, out_entry_rows + (size_t(i) * next_K + j) * E.V, E.brows[0] + (size_t(j) * B + i) * E.V,
+            size_t(E.V) * 4);
+  }
+  if (out_count) *out_count = total;
+  get_stream(E, rng);
+  API_END
+}
+
+ssd_status ssd_prespec_begin(ssd_engine* h, const int32_t* d_ctx, int32_t n, const int32_t* d_spec, int32_t K,
+                             const ssd_plan* plan, const ssd_scheme* sc, int32_t next_K, ssd_rng_stream* rng,
+                             void* cuda_stream) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!d_ctx || !d_spec || n < 1) throw Fail(SSD_ERROR, "prespec_begin: context and speculation required");
+  if (!rng) throw Fail(SSD_CONFIG, "rng stream required");
+  if (E.pre_active) CK(cudaEventSynchronize(E.ev_prespec));  // the previous session's buffers are reused
+  int B = 0, max_f = 0;
+  const int total = prespec_setup(E, plan, sc, K, next_K, B, max_f);
+  const int cap = std::min(E.T.s.max_ctx, E.D.s.max_ctx);
+  if (n + K + next_K + 2 > cap) throw Fail(SSD_TOO_LARGE, "context exceeds max_ctx");
+  E.D.ctx_bound = n + K + next_K + 2 + 2 * E.maxK;
+  cudaStream_t s = E.sv;
+  if (cuda_stream) {  // ordered after the caller's producer of d_ctx / d_spec
+    CK(cudaEventRecord(E.ev_user, static_cast<cudaStream_t>(cuda_stream)));
+    CK(cudaStreamWaitEvent(s, E.ev_user, 0));
+  }
+  // the device stream starts from the caller's state; the host copy takes the
+  // same one draw (cache.cpp:245), so both stay in step without a sync
+  std::memcpy(E.pin_rng, rng, sizeof(Mt64));
+  ssd_rng_stream_next_u64(rng);
+  reset_state(E, K, n, 1, 0, 0, nullptr, s);
+  CK(cudaMemcpyAsync(&E.st->drng, E.pin_rng, sizeof(Mt64), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(E.hist, d_ctx, size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, spec), d_spec, size_t(K) * 4,
+                     cudaMemcpyDeviceToDevice, s));
+  set_spec_origin_kernel<<<1, 32, 0, s>>>(E.st, plan->role, next_K);
+  KCHECK();
+  if (n > 1) prefill(E, E.D, n - 1, nullptr, s);
+  if (total > 0) prespeculate(E, K, B, 0, B, max_f, *sc, 0, s, 1, nullptr, next_K);
+  CK(cudaEventRecord(E.ev_prespec, s));
+  E.pre_active = 1;
+  E.pre_count = total;
+  E.pre_kb = next_K;
+  E.pre_keys_valid = 0;
+  API_END
+}
+
+static void prespec_wait(Engine& E) {
+  if (!E.pre_active) throw Fail(SSD_CONFIG, "cache: no pre-speculation started (ssd_prespec_begin)");
+  CK(cudaEventSynchronize(E.ev_prespec));
+  if (E.pre_keys_valid) return;
+  const int n = E.pre_count;
+  std::vector<int> bk(static_cast<size_t>(std::max(n, 1))), bt(static_cast<size_t>(std::max(n, 1)));
+  d2h(E, bk.data(), E.bk, size_t(n) * 4);
+  d2h(E, bt.data(), E.btok, size_t(n) * 4);
+  E.pre_keys.assign(size_t(2 * n), 0);
+  for (int i = 0; i < n; ++i) { E.pre_keys[size_t(2 * i)] = bk[size_t(i)]; E.pre_keys[size_t(2 * i + 1)] = bt[size_t(i)]; }
+  LoopState st = read_state(E);
+  raise_device_error(st);
+  E.pre_keys_valid = 1;
+}
+
+ssd_status ssd_cache_lookup(ssd_engine* h, int32_t k, int32_t t, int32_t* slot) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (!slot) throw Fail(SSD_CONFIG, "cache_lookup: null output");
+  prespec_wait(E);
+  *slot = -1;
+  for (int i = 0; i < E.pre_count; ++i)
+    if (E.pre_keys[size_t(2 * i)] == k && E.pre_keys[size_t(2 * i + 1)] == t) { *slot = i; break; }
+  API_END
+}
+
+ssd_status ssd_cache_keys(ssd_engine* h, int32_t* out_keys, int32_t* out_count) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  prespec_wait(E);
+  if (out_keys) std::memcpy(out_keys, E.pre_keys.data(), E.pre_keys.size() * 4);
+  if (out_count) *out_count = E.pre_count;
+  API_END
+}
+
+ssd_status ssd_cache_entry(ssd_engine* h, int32_t slot, int32_t* out_tokens, float* out_rows) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  prespec_wait(E);
+  if (slot < 0 || slot >= E.pre_count) throw Fail(SSD_ERROR, "cache_entry: slot out of range");
+  const int Kb = E.pre_kb, B = E.pre_count;
+  if (out_tokens) d2h(E, out_tokens, E.bt + size_t(slot) * Kb, size_t(Kb) * 4);
+  if (out_rows)
+    for (int j = 0; j < Kb; ++j) d2h(E, out_rows + size_t(j) * E.V, E.brows[0] + (size_t(j) * B + slot) * E.V, size_t(E.V) * 4);
+  API_END
+}
+
 ssd_status ssd_topk_keys(ssd_engine* h, const float* rows, int32_t n_rows, int32_t V, const int32_t* fan,
                          const int32_t* excluded, int32_t max_f, int32_t* keys) {
   API_BEGIN
@@ -2272,14 +2547,17 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   KCHECK();
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, F = sh.ffn, nqkv = m.qd + 2 * m.kvd;
-  auto gemms = [&]() {
+  const int fused = (!E.deterministic && m.tp_size == 1) ? 1 : 0;
+  auto gemms = [&]() {  // (QKV accumulates into whatever qkv holds: timing only)
     PfCursor pf(m, E.pf_ahead, true);
     for (int l = 0; l < sh.n_layers; ++l) {
       const DevLayer& L = m.layers[size_t(l)];
-      linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l));
-      linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
+      linear<EPI_STORE>(E, m, L.qkv, m.xb, M, m.qkv, nqkv, nullptr, 0, s, pf.after(4 * l), fused);
+      if (fused) linear<EPI_RESID>(E, m, L.o, m.attn, M, m.x, d, nullptr, 0, s, pf.after(4 * l + 1), 1);
+      else linear<EPI_STORE>(E, m, L.o, m.attn, M, m.dlt1, d, nullptr, 0, s, pf.after(4 * l + 1));
       linear<EPI_SWIGLU>(E, m, L.gu, m.xb, M, nullptr, 0, m.act, F, s, pf.after(4 * l + 2));
-      linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
+      if (fused) linear<EPI_RESID>(E, m, L.dn, m.act, M, m.x, d, nullptr, 0, s, pf.after(4 * l + 3), 1);
+      else linear<EPI_STORE>(E, m, L.dn, m.act, M, m.dlt2, d, nullptr, 0, s, pf.after(4 * l + 3));
     }
     linear<EPI_STORE>(E, m, m.head, m.xb, M, m.logits, sh.vocab, nullptr, 0, s, pf.after(4 * sh.n_layers));
   };

@@ -210,6 +210,11 @@ struct GemmArgs {
   // it covers the drain / epilogue / next-launch gap.
   Prefetch pf;
   int dbg_seq;  // profiling build: launch sequence number (per-CTA timeline)
+  // 1: a tile split between CTAs is summed with fp32 atomics straight into Y
+  // (pre-zeroed for EPI_STORE; the residual stream itself for EPI_RESID)
+  // instead of partials + a last-arriver reduction: no ticket / reduce round
+  // trips after the last MMA, summation order not fixed.
+  int atomic;
 };
 
 template <int EPI>
@@ -414,13 +419,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         for (int j = 0; j < 8; ++j) {
           const float f = __uint_as_float(v[j]);
           if (whole) apply_epi<EPI>(g, r, c + j, f);
-          else if (c + j < g.M) part[size_t(c + j) * kBM + rl] = f;
+          else if (EPI != EPI_SWIGLU && g.atomic) {
+            if (r < g.N && c + j < g.M) atomicAdd(g.Y + size_t(c + j) * g.ldy + r, f);
+          } else if (c + j < g.M) part[size_t(c + j) * kBM + rl] = f;
         }
       }
 #if SSD_KTL
       if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][4] = ktl_now();
 #endif
-      if (!whole) {
+      if (!whole && !(EPI != EPI_SWIGLU && g.atomic)) {
         // last-arriving segment of tile t reduces the partials in CTA order
         const int cf = cta_of(t * g.KU, U, P), cl = cta_of((t + 1) * g.KU - 1, U, P);
         // The CTA barrier orders the 128 threads' partial stores before the

@@ -232,9 +232,12 @@ __global__ void embed_kernel(const bf16* __restrict__ E, int d, int tiled, const
 // epilogue a plain store. One CTA per token, float4 accesses, d <= 8192.
 constexpr int kNormThreads = 256;
 
+// zero / zero_n: rows [M][zero_n] of the next GEMM's output, cleared for its
+// atomic split-K accumulation (gemm_tc.cuh GemmArgs::atomic).
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                                                int d, const float* __restrict__ g, float eps,
-                                                               bf16* __restrict__ out, Prefetch pf) {
+                                                               bf16* __restrict__ out, Prefetch pf,
+                                                               float* __restrict__ zero, int zero_n) {
   __shared__ float sh[32];
   KTL_ENTER(2);
   prefetch_window(pf, kPfUnitBytes);
@@ -263,6 +266,9 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
       ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
     }
   }
+  if (zero)
+    for (int i = threadIdx.x; i < (zero_n >> 2); i += kNormThreads)
+      reinterpret_cast<float4*>(zero + size_t(m) * zero_n)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   ss = block_sum(ss, sh);
   const float r = 1.0f / sqrtf(ss / float(d) + eps);
   __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out + size_t(m) * d);
@@ -1133,6 +1139,15 @@ __global__ void lookup_kernel(LoopState* st, int nb, const int* __restrict__ key
   else clock = last ? v1 : (all_hit ? fmax(v1, ready) : v1 + st[0].backup_time);
   for (int l = 0; l < nb; ++l) st[l].clock = clock;
   if (tr.d) { tr.d[2 * r] = mode == 1 ? v0 : v1; tr.d[2 * r + 1] = clock; }
+}
+
+// Pre-speculation session (ssd_prespec_begin): origin of the in-flight
+// speculation and the entries' continuation length, set on the device so the
+// call needs no host round trip.
+__global__ void set_spec_origin_kernel(LoopState* st, int origin, int Kb) {
+  if (threadIdx.x != 0) return;
+  st->spec_origin = origin;
+  st->Kb = Kb;
 }
 
 // Transcript: the speculation each listed lane sends after a JIT re-draft.

@@ -159,3 +159,24 @@ def test_fit_powerlaw_matches_reference_golden(lib, case):
     assert r == pytest.approx(out["exponent"], rel=1e-13, abs=1e-15)
     assert la == pytest.approx(out["log_amplitude"], rel=1e-13, abs=1e-15)
     assert r2 == pytest.approx(out["r_squared"], rel=1e-13, abs=1e-15)
+
+
+def test_host_stream_is_std_mt19937_64():
+    """ssd_rng_stream (the C form of rng::Stream, rng.hpp:29-48) is host
+    code: std::mt19937_64's 10000th output for the default seed is
+    9981545732273789042 ([rand.predef]); next_uniform takes the top 53 bits
+    (rng.hpp:39-41); derive_seed is rng.hpp:24-26."""
+    import paper_2603_03251_b200 as P
+    s = P.Stream(5489)
+    c = s.copy()
+    for _ in range(9999):
+        s.next_u64()
+    assert s.next_u64() == 9981545732273789042
+    x = c.copy().next_u64()
+    assert c.next_uniform() == (x >> 11) * 2.0 ** -53
+    m = 0xFFFFFFFFFFFFFFFF
+    z = (7 + (3 + 1) * 0x9E3779B97F4A7C15) & m
+    z = (z + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    assert P.derive_seed(7, 3) == z ^ (z >> 31)

@@ -47,3 +47,32 @@ def test_shim_drives_engine_like_reference_caller(shim_bin):
     eng.close()
     assert py.streams[0] == got["tokens"]
     assert abs(py.hit_rate() - got["hit_rate"]) < 1e-9
+
+
+REF_CASES = os.path.join(ROOT, "tests", "cpp", "ref_cases.cpp")
+
+
+@pytest.fixture(scope="module")
+def ref_cases_bin(tmp_path_factory):
+    """The reference's own specdec / cache known-answer cases (test_specdec.cpp
+    :43-153, test_cache.cpp:221-302) restated against the shim, compiled
+    with a doctest stand-in (tests/cpp/doctest_shim.h)."""
+    out = str(tmp_path_factory.mktemp("refcases") / "ref_cases")
+    cuda = "/usr/local/cuda"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    "-I", os.path.join(cuda, "include"), REF_CASES, "-L", LIBDIR, "-lssd_b200",
+                    "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{LIBDIR}",
+                    f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", out], check=True)
+    return out
+
+
+def test_reference_cases_compile_against_shim(ref_cases_bin):
+    assert os.path.exists(ref_cases_bin)
+
+
+@pytest.mark.gpu
+def test_reference_cases_pass_on_gpu(ref_cases_bin):
+    r = subprocess.run([ref_cases_bin], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["failed"] == 0 and got["cases"] >= 14, got
