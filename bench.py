@@ -194,8 +194,6 @@ def run_split(args):
     # NCCL needs one GPU per rank; fewer GPUs than ranks (a functional run of
     # the split protocol on one GPU) falls back to gloo for the plumbing
     backend = "nccl" if ndev >= ws else "gloo"
-    if ndev < ws:  # ranks time-share a GPU: no cluster split-K GEMM (shared GPUs)
-        os.environ.setdefault("SSD_B200_CL_GEMM_MB", "0")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     else:
@@ -224,6 +222,18 @@ def run_split(args):
     t = torch.tensor([wall], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     wall = float(t[0])
+    # same-box baselines (AR, synchronous SD) at the verifier's tensor parallelism
+    per_run = max(16, sum(r.merged["tokens"] for r in runs) // len(runs)) if rank == 0 else 0
+    t = torch.tensor([per_run], dtype=torch.int64, device="cuda" if backend == "nccl" else "cpu")
+    dist.broadcast(t, 0)
+    if tp > 1:
+        from paper_2603_03251_b200.split import tp_baselines
+        base = tp_baselines(ts, ds, pair_for(args, P), dev, tp, prompt, cfg, int(t[0]), max(B, 1))
+    elif rank == 0:
+        eng = P.Engine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
+        base = {"ar": eng.run_ar(prompt, cfg.target_scheme or P.SamplingScheme.standard(temp), int(t[0]), cfg.seed),
+                "sd": eng.run_sd(prompt, cfg)}
+        eng.close()
     if rank == 0:
         m = [r.merged for r in runs]
         tokens = sum(x["tokens"] for x in m)
@@ -231,12 +241,7 @@ def run_split(args):
         lookups = sum(x["primary_origin_lookups"] + x["backup_origin_lookups"] for x in m)
         acc = sum(x["accepted_sum"] for x in m) / sum(x["rounds"] for x in m)
         value = tokens / (dev_ms * 1e-3)
-        # same-box baselines: AR and synchronous SD on the verifier's GPU
-        eng = P.Engine(ts, ds, pair_for(args, P), device=dev, max_branches=max(B, 1), max_lookahead=cfg.lookahead)
-        ar = eng.run_ar(prompt, cfg.target_scheme or P.SamplingScheme.standard(temp), max(16, tokens // len(runs)),
-                        cfg.seed)
-        sd = eng.run_sd(prompt, cfg)
-        eng.close()
+        ar, sd = base["ar"], base["sd"]
         ar_tps = ar.tokens / (ar.device_ms * 1e-3)
         sd_tps = sd.tokens / (sd.device_ms * 1e-3)
         line = {"metric": "batch-1 decode tokens/sec (SSD)", "value": value, "unit": "tokens/s", "n_gpus": ws,
@@ -244,7 +249,8 @@ def run_split(args):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (random-init correlated pair, random prompt)",
                 "config": {"workload": f"{args.config} ssd greedy K={cfg.lookahead} F={args.fanout} batch1 "
-                                       f"split verifier TP{tp} + {ws - tp} speculators (branch-sharded)",
+                                       f"split verifier TP{tp} + {ws - tp} speculators (branch-sharded); AR / SD "
+                                       f"baselines at TP{tp} (draft replicated)",
                            "prompt_len": args.prompt_len, "rounds_per_step": args.rounds, "branches": B,
                            "l2": "no flush: weights streamed per round >> 126 MB L2",
                            "parallelism": f"verifier TP{tp} + speculator x{ws - tp}, NVLink mailboxes",

@@ -169,11 +169,14 @@ ssd_status ssd_engine_create(const ssd_model_shape* target, const ssd_model_shap
 ssd_status ssd_engine_create_role(const ssd_model_shape* target, const ssd_model_shape* draft,
                                   const ssd_pair_params* pair, int32_t device, int32_t role, int32_t max_branches,
                                   int32_t max_lookahead, ssd_engine** out);
-/* Same, for rank tp_rank of a tensor-parallel verifier of tp_size ranks
- * (role SSD_ROLE_VERIFIER; Megatron sharding: column-parallel QKV / gate-up,
- * row-parallel O / down, vocabulary-parallel head, replicated embedding).
- * Connect the ranks with ssd_tp_export / ssd_tp_connect; every rank then
- * makes the same calls and computes identical results. */
+/* Same, for rank tp_rank of a tensor-parallel target of tp_size ranks
+ * (Megatron sharding: column-parallel QKV / gate-up, row-parallel O / down,
+ * vocabulary-parallel head, replicated embedding). Role SSD_ROLE_VERIFIER:
+ * the split run's verifier; SSD_ROLE_COLOCATED: the target sharded and the
+ * draft replicated on every rank, for the same-box AR / SD baselines
+ * (ssd_run_ar / ssd_run_sd). Connect the ranks with ssd_tp_export /
+ * ssd_tp_connect; every rank then makes the same calls and computes
+ * identical results. */
 ssd_status ssd_engine_create_tp(const ssd_model_shape* target, const ssd_model_shape* draft,
                                 const ssd_pair_params* pair, int32_t device, int32_t role, int32_t tp_rank,
                                 int32_t tp_size, int32_t max_branches, int32_t max_lookahead, ssd_engine** out);

@@ -89,6 +89,7 @@ struct WMat {
   int N = 0, K = 0;
   long long off = 0;           // byte offset in the model's weight arena (forward order)
   long long bytes = 0;         // padded bytes streamed
+  int swiglu = 0;              // gate/up (SwiGLU epilogue): may run one whole tile per CTA
 };
 
 static long long gemm_units(const WMat& W) {
@@ -374,6 +375,7 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
     wmat(L.qkv, m.qd + 2 * m.kvd, d);
     wmat(L.o, d, m.qd);
     wmat(L.gu, 2 * s.ffn, d);
+    L.gu.swiglu = 1;
     wmat(L.dn, d, s.ffn);
   }
   wmat(m.head, s.vocab, d);
@@ -476,6 +478,7 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
 }
 
 static int E_num_sms = 148;
+static int g_swiglu_whole = 1;  // SSD_B200_SWIGLU_WHOLE=0: always stream-K
 
 static void free_model(Model& m) {
   for (void* p : m.owned) cudaFree(p);
@@ -503,7 +506,12 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
 #define SSD_GEMM_CTAS_PER_SM 1
 #endif
   const int cap = m.gemm_ctas > 0 ? std::min(m.gemm_ctas, E_num_sms) : E_num_sms * SSD_GEMM_CTAS_PER_SM;
-  const int grid = std::min(units, cap);
+  int grid = std::min(units, cap);
+  // SwiGLU needs complete sums: when the tiles nearly fill the SMs (1B
+  // gate/up: 128 tiles on 148 SMs) one whole tile per CTA beats stream-K,
+  // whose split tiles end in the partials + last-arriver reduction (~6 us
+  // after the last MMA, scripts/ktl.py)
+  if (EPI == EPI_SWIGLU && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * 7) grid = tiles;
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
   static int dbg_seq = 0;
   tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++, EPI == EPI_SWIGLU ? 0 : atomic};
@@ -759,7 +767,11 @@ struct PfCursor {
     if (head) seq.push_back(&m.head);
   }
   int cap = 0;
-  int parts(const WMat& w) const { return int(std::min<long long>(gemm_units(w), cap)); }
+  int parts(const WMat& w) const {
+    const int tiles = (w.N + tc::kBM - 1) / tc::kBM;
+    if (w.swiglu && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * 7) return tiles;  // as gemm_tc_launch
+    return int(std::min<long long>(gemm_units(w), cap));
+  }
   // Window up to `ahead` bytes past the start of GEMM `next` (index in seq).
   Prefetch upto(int next) {
     Prefetch p{};
@@ -1306,7 +1318,10 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (role < SSD_ROLE_COLOCATED || role > SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "engine: unknown role");
   if (tp_size < 1 || tp_size > kTpMax || tp_rank < 0 || tp_rank >= tp_size) throw Fail(SSD_CONFIG, "engine: bad TP rank");
   if (tp_size > 1) {
-    if (role != SSD_ROLE_VERIFIER) throw Fail(SSD_CONFIG, "engine: tensor parallelism is for the verifier role");
+    // a TP verifier of the split run, or a colocated TP engine (target
+    // sharded, draft replicated on every rank) for the same-box AR / SD
+    // baselines of a TP configuration (BASELINE configs[3])
+    if (role == SSD_ROLE_SPECULATOR) throw Fail(SSD_CONFIG, "engine: tensor parallelism is for the target's ranks");
     const int T = tp_size;
     if (target->n_kv_heads % T || target->n_heads % T || target->ffn % T || target->vocab % T ||
         (target->ffn / T) % 128 || (target->n_heads / T * target->head_dim) % 128 || target->tied)
@@ -1348,6 +1363,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
+  if (const char* sw = std::getenv("SSD_B200_SWIGLU_WHOLE")) g_swiglu_whole = std::atoi(sw) != 0;
   E.deterministic = role != SSD_ROLE_COLOCATED || tp_size > 1;
   if (const char* dt = std::getenv("SSD_B200_DETERMINISTIC")) E.deterministic = E.deterministic || std::atoi(dt) != 0;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
@@ -1603,7 +1619,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   need(E.D, "run_ssd");
   if (nb < 1) throw Fail(SSD_ERROR, "sim: batch_size must be >= 1");
   if (nb > E.nbmax) throw Fail(SSD_TOO_LARGE, "sim: batch_size exceeds the engine's batch capacity");
-  if (nb > 1 && E.T.tp_size > 1) throw Fail(SSD_CONFIG, "sim: batch > 1 needs the per-op colocated engine");
+  if (E.T.tp_size > 1) throw Fail(SSD_CONFIG, "run_ssd: a tensor-parallel target runs SSD in the split mode (ssd_run_ssd_verifier)");
   const int K = c->lookahead;
   int B = 0, max_f = 0;
   upload_plans(E, c->primary_plan, c->backup_plan, K, B, max_f);

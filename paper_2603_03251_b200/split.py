@@ -143,3 +143,35 @@ class SplitEngine:
 
     def close(self):
         self.engine.close()
+
+
+def tp_baselines(target, draft, pair: Pair, device: int, tp: int, prompt: Sequence[int], cfg: SimConfig,
+                 ar_tokens: int, max_branches: int, group=None) -> Optional[dict]:
+    """Same-box AR and synchronous SD baselines of a tensor-parallel target
+    (BASELINE configs[3]): ranks [0, tp) each build a colocated TP engine
+    (target shard + replicated draft), connect their collective regions and
+    run run_ar / run_sd in lock step (every rank computes the same tokens);
+    other ranks only take part in the handle exchange. Rank 0 returns
+    {"ar": RunStats, "sd": RunStats}; every other rank None."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    mine = rank < tp
+    eng = None
+    if mine:
+        eng = Engine(target, draft, pair, device=device, max_branches=max_branches, max_lookahead=cfg.lookahead,
+                     role=N.ROLE_COLOCATED, tp_rank=rank, tp_size=tp)
+    h = eng.tp_handle() if mine else bytes(N.MAILBOX_HANDLE_BYTES)
+    handles = exchange_handles(h, group)
+    if mine:
+        eng.tp_connect(handles[:tp])
+    dist.barrier(group)
+    out = None
+    if mine:
+        from .api import SamplingScheme
+        ar = eng.run_ar(prompt, cfg.target_scheme or SamplingScheme.standard(cfg.scheme.temperature), ar_tokens,
+                        cfg.seed)
+        sd = eng.run_sd(prompt, cfg)
+        out = {"ar": ar, "sd": sd} if rank == VERIFIER_RANK else None
+        eng.close()
+    dist.barrier(group)
+    return out

@@ -49,7 +49,20 @@ def first_divergence(a, b):
     return None if len(a) == len(b) else min(len(a), len(b))
 
 
-def check_greedy_stream(orc, which: int, prompt, stream, max_flips: int = 2) -> int:
+def near_tie_for(orc32, orc64, contexts, which_list=(0, 1)) -> float:
+    """The near-tie width of a pair: max(NEAR_TIE, 2 x the fp32 noise floor
+    measured on `contexts` (oracle fp32 vs fp64, max |logit| deviation)). At
+    the 8B/1B shapes fp32 summation order alone moves logits by up to ~0.09,
+    so an argmax flip with a gap below that is noise, not a kernel bug."""
+    n = 0.0
+    for which in which_list:
+        for ctx in contexts:
+            n = max(n, float(np.max(np.abs(orc32.logits(which, ctx).astype(np.float64) -
+                                           orc64.logits(which, ctx).astype(np.float64)))))
+    return max(NEAR_TIE, 2.0 * n)
+
+
+def check_greedy_stream(orc, which: int, prompt, stream, max_flips: int = 2, near_tie: float = NEAR_TIE) -> int:
     """Teacher-forced greedy check of `stream` (model `which` of the oracle
     pair, context = prompt + stream[:i] at position i). Returns the number of
     accepted near-tie flips; raises AssertionError on a real mismatch."""
@@ -60,14 +73,14 @@ def check_greedy_stream(orc, which: int, prompt, stream, max_flips: int = 2) -> 
         best = int(np.argmax(z))
         if best != int(t):
             gap = float(z[best] - z[int(t)])
-            assert gap < NEAR_TIE, f"position {i}: engine token {t}, oracle argmax {best}, gap {gap:.4g} (no near-tie)"
+            assert gap < near_tie, f"position {i}: engine token {t}, oracle argmax {best}, gap {gap:.4g} (no near-tie)"
             flips += 1
         ctx.append(int(t))
     assert flips <= max_flips, f"{flips} near-tie flips in {len(stream)} tokens"
     return flips
 
 
-def check_topk_set(zo: np.ndarray, got, want, excluded: int = -1):
+def check_topk_set(zo: np.ndarray, got, want, excluded: int = -1, near_tie: float = NEAR_TIE):
     """Top-F candidate sets (value desc, index asc; cache.cpp:249-270): equal,
     or differing only in candidates that sit within NEAR_TIE of the oracle's
     cut value."""
@@ -80,7 +93,7 @@ def check_topk_set(zo: np.ndarray, got, want, excluded: int = -1):
     F = len(want)
     cut = float(np.sort(z)[-F]) if F else float("inf")
     for t in got ^ want:
-        assert abs(float(z[t]) - cut) < NEAR_TIE, f"candidate {t} logit {z[t]:.5f} not at the cut {cut:.5f}"
+        assert abs(float(z[t]) - cut) < near_tie, f"candidate {t} logit {z[t]:.5f} not at the cut {cut:.5f}"
 
 
 def binom_close(k1, n1, k2, n2, z=4.0):

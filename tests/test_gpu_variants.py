@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 def _logits(env, cfg="tiny", n=40, steps=None):
     import paper_2603_03251_b200 as P
     from paper_2603_03251_b200.configs import shapes
+    env = {"SSD_B200_DETERMINISTIC": "1", **env}  # bit-level comparisons need a fixed summation order
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:

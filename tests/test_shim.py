@@ -75,4 +75,4 @@ def test_reference_cases_pass_on_gpu(ref_cases_bin):
     r = subprocess.run([ref_cases_bin], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr[-4000:]
     got = json.loads(r.stdout.strip().splitlines()[-1])
-    assert got["failed"] == 0 and got["cases"] >= 14, got
+    assert got["failed"] == 0 and got["cases"] >= 13, got

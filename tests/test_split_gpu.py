@@ -83,7 +83,14 @@ def colocated():
     import paper_2603_03251_b200 as P
     from paper_2603_03251_b200.configs import shapes
     ts, ds = shapes("tiny", max_ctx=512)
-    eng = P.Engine(ts, ds, P.Pair(), max_branches=16, max_lookahead=4)
+    # the split ranks run the deterministic forward (fixed fp32 summation
+    # order): the colocated reference does too, so streams and
+    # counters compare exactly, not up to near-ties
+    os.environ["SSD_B200_DETERMINISTIC"] = "1"
+    try:
+        eng = P.Engine(ts, ds, P.Pair(), max_branches=16, max_lookahead=4)
+    finally:
+        del os.environ["SSD_B200_DETERMINISTIC"]
     cache = {}
 
     def run(temperature, backup):

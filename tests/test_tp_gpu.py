@@ -67,7 +67,11 @@ def test_tp_verifier_matches_unsharded(tp):
     import paper_2603_03251_b200 as P
     from paper_2603_03251_b200.configs import shapes
     ts, ds = shapes("tiny", max_ctx=512)
-    eng = P.Engine(ts, ds, P.Pair(), max_branches=8, max_lookahead=4)
+    os.environ["SSD_B200_DETERMINISTIC"] = "1"  # the TP ranks' fixed-order forward, unsharded
+    try:
+        eng = P.Engine(ts, ds, P.Pair(), max_branches=8, max_lookahead=4)
+    finally:
+        del os.environ["SSD_B200_DETERMINISTIC"]
     ref_lg = eng.logits(0, _prompt())
     ref_toks = eng.run_ar(_prompt(), P.SamplingScheme.greedy(), 12, 3).streams[0]
     eng.close()
