@@ -102,6 +102,28 @@ def binom_close(k1, n1, k2, n2, z=4.0):
     return abs(k1 / n1 - k2 / n2) <= z * sd + 1e-9
 
 
+def runs_close(g_runs, o_runs, z=4.0):
+    """Two-sample check of a rate pooled over independent runs (lists of
+    (successes, trials) per run): |p_g - p_o| within z standard errors, the
+    error of each side the cluster-robust variance of the ratio estimator
+    (runs are the independent units: at tau = 1 the acceptance of one
+    trajectory is strongly correlated across its rounds, so a binomial model
+    over rounds understates the spread several-fold), floored at the
+    binomial variance."""
+    def stats(runs):
+        k = np.array([r[0] for r in runs], dtype=np.float64)
+        n = np.array([r[1] for r in runs], dtype=np.float64)
+        p = k.sum() / max(n.sum(), 1.0)
+        N = len(runs)
+        v = p * (1 - p) / max(n.sum(), 1.0)
+        if N > 1:
+            v = max(v, float(((k - p * n) ** 2).sum()) / (N * (N - 1)) / max(n.mean(), 1.0) ** 2)
+        return p, v
+    pg, vg = stats(g_runs)
+    po, vo = stats(o_runs)
+    return abs(pg - po) <= z * np.sqrt(vg + vo) + 1e-9
+
+
 def sim_req(prompt, mode, K, rounds, seed, temperature, fan, backup="fast_random", scheme=None, accept_scale=1.0):
     req = {"op": "simulate", "mode": mode, "lookahead": K, "rounds": rounds, "seed": seed, "prompt": list(prompt),
            "scheme": scheme or {"temperature": temperature}, "primary_plan": {"fan": list(fan)},

@@ -15,8 +15,8 @@ C-ABI against the CPU oracle:
 import numpy as np
 import pytest
 
-from parity import (bigram_counts, binom_close, check_greedy_stream, chi_square_two_sample, first_divergence, sim_cfg,
-                    sim_req)
+from parity import (bigram_counts, check_greedy_stream, chi_square_two_sample, first_divergence, runs_close,
+                    sim_cfg, sim_req)
 
 pytestmark = pytest.mark.gpu
 
@@ -83,19 +83,17 @@ def test_sequential_and_harness_semantics_differ_only_in_rng_order(tiny):
 def test_sequential_sampled_statistics(tiny):
     P, eng, orc = tiny
     R = 30
-    acc_g = acc_o = hit_g = hit_o = look_g = look_o = 0
-    for rep in range(4):
+    acc_g, acc_o, hit_g, hit_o = [], [], [], []
+    for rep in range(6):
         prompt = _prompt(12, 32000, 800 + rep)
         g = eng.run_ssd(prompt, sim_cfg(P, K, R, 900 + rep, 1.0, FAN), semantics="sequential")
         o = orc.call(sim_req(prompt, "ssd", K, R, 900 + rep, 1.0, FAN))
-        acc_g += g.accepted_sum
-        acc_o += o["accepted_sum"]
-        hit_g += g.hits_total()
-        look_g += g.lookups()
-        hit_o += o["p_hits"] + o["b_hits"]
-        look_o += o["p_lookups"] + o["b_lookups"]
-    assert binom_close(acc_g, 4 * R * K, acc_o, 4 * R * K), (acc_g, acc_o)
-    assert binom_close(hit_g, look_g, hit_o, look_o), (hit_g, look_g, hit_o, look_o)
+        acc_g.append((g.accepted_sum, R * K))
+        acc_o.append((o["accepted_sum"], R * K))
+        hit_g.append((g.hits_total(), g.lookups()))
+        hit_o.append((o["p_hits"] + o["b_hits"], o["p_lookups"] + o["b_lookups"]))
+    assert runs_close(acc_g, acc_o), (acc_g, acc_o)
+    assert runs_close(hit_g, hit_o), (hit_g, hit_o)
 
 
 @pytest.mark.parametrize("backup", ["fast_random", "same_primary_jit"])
@@ -167,49 +165,51 @@ def test_corrupted_acceptance_is_detected(micro):
 def test_saguaro_drafting_statistics(tiny, loop):
     """Draft sampling under sigma_{F,C} (F = 4, C = 0.5, tau = 1) inside the
     loops, target Standard(1): acceptance (and the harness' hit rate) within
-    4 sigma of the oracle's over independent prompts."""
+    4 standard errors of the oracle's over independent prompts (runs as the
+    independent units, parity.runs_close)."""
     P, eng, orc = tiny
     sc = P.SamplingScheme.saguaro(4, 0.5, 1.0)
     scd = {"kind": "saguaro", "temperature": 1.0, "fan_out": 4, "downweight": 0.5}
     R = 30
-    acc_g = acc_o = hit_g = hit_o = look_g = look_o = 0
-    for rep in range(4):
+    acc_g, acc_o, hit_g, hit_o = [], [], [], []
+    for rep in range(6):
         prompt = _prompt(12, 32000, 300 + rep)
         cfg = sim_cfg(P, K, R, 400 + rep, 1.0, FAN, scheme=sc)
         req = sim_req(prompt, loop, K, R, 400 + rep, 1.0, FAN, scheme=scd)
         req["target_scheme"] = {"kind": "standard", "temperature": 1.0}
         g = eng.run_sd(prompt, cfg) if loop == "sd" else eng.run_ssd(prompt, cfg)
         o = orc.call(req)
-        acc_g += g.accepted_sum
-        acc_o += o["accepted_sum"]
+        acc_g.append((g.accepted_sum, R * K))
+        acc_o.append((o["accepted_sum"], R * K))
         if loop == "harness":
-            hit_g += g.hits_total()
-            look_g += g.lookups()
-            hit_o += o["p_hits"] + o["b_hits"]
-            look_o += o["p_lookups"] + o["b_lookups"]
-    assert binom_close(acc_g, 4 * R * K, acc_o, 4 * R * K), (acc_g, acc_o)
+            hit_g.append((g.hits_total(), g.lookups()))
+            hit_o.append((o["p_hits"] + o["b_hits"], o["p_lookups"] + o["b_lookups"]))
+    assert runs_close(acc_g, acc_o), (acc_g, acc_o)
     if loop == "harness":
-        assert binom_close(hit_g, look_g, hit_o, look_o), (hit_g, look_g, hit_o, look_o)
+        assert runs_close(hit_g, hit_o), (hit_g, hit_o)
 
 
 @pytest.mark.parametrize("F", [1, 2, 4, 8, 16])
 def test_fanout_sweep_tau1_statistics(tiny, F):
     """BASELINE configs[2] fan-out sweep at tau = 1 (rejection-sampling
     verification): cache hit rate and acceptance of the GPU harness within
-    4 sigma of the oracle's at every F (B = 5 F branches, up to M = 80)."""
+    4 standard errors of the oracle's at every F (B = 5 F branches, up to
+    M = 80), runs as the independent units (parity.runs_close). Sampled
+    streams themselves diverge within a few rounds: at near-uniform tiny-pair
+    laws the CDF steps (~3e-5) are below the fp32 logit noise, so the shared
+    uniforms pick different tokens (scripts/diag_fanout.py: every entry's
+    draft rows match the oracle to 0.03 at F = 4..16)."""
     P, eng, orc = tiny
     fan = [F] * (K + 1)
     R = 24
-    acc_g = acc_o = hit_g = hit_o = look_g = look_o = 0
-    for rep in range(3):
+    acc_g, acc_o, hit_g, hit_o = [], [], [], []
+    for rep in range(8):
         prompt = _prompt(12, 32000, 1200 + 10 * F + rep)
         g = eng.run_ssd(prompt, sim_cfg(P, K, R, 1300 + rep, 1.0, fan))
         o = orc.call(sim_req(prompt, "harness", K, R, 1300 + rep, 1.0, fan))
-        acc_g += g.accepted_sum
-        acc_o += o["accepted_sum"]
-        hit_g += g.hits_total()
-        look_g += g.lookups()
-        hit_o += o["p_hits"] + o["b_hits"]
-        look_o += o["p_lookups"] + o["b_lookups"]
-    assert binom_close(acc_g, 3 * R * K, acc_o, 3 * R * K), (F, acc_g, acc_o)
-    assert binom_close(hit_g, look_g, hit_o, look_o), (F, hit_g, look_g, hit_o, look_o)
+        acc_g.append((g.accepted_sum, R * K))
+        acc_o.append((o["accepted_sum"], R * K))
+        hit_g.append((g.hits_total(), g.lookups()))
+        hit_o.append((o["p_hits"] + o["b_hits"], o["p_lookups"] + o["b_lookups"]))
+    assert runs_close(acc_g, acc_o), (F, acc_g, acc_o)
+    assert runs_close(hit_g, hit_o), (F, hit_g, hit_o)

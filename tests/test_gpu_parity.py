@@ -303,15 +303,19 @@ def test_errors_map_to_reference_classes(tiny):
 
 
 @pytest.mark.parametrize("M", [2, 5, 20, 33, 100])
-def test_tcgen05_forward_widths_match_oracle(tiny, M):
+def test_tcgen05_forward_widths_match_oracle(tiny, oracle_lib, M):
     """The tcgen05 swap-AB GEMM at every token-operand width the engine uses
     (N = 16 / 32 / 48 / 128 tiles, cluster split-K at 17..32): logits of the
-    last position of one M-token prefill forward vs the oracle."""
+    last position of one M-token prefill forward vs the fp64-accumulating
+    oracle, within the fp32 oracle's own deviation (parity.logit_noise_check:
+    a wide prefill re-rounds every activation to bf16, so two fp32 summation
+    orders legitimately differ by more than 1e-2 on some logits)."""
+    from parity import logit_noise_check
     P, eng, orc = tiny
-    ctx = _prompt(M, seed=200 + M)
-    g = eng.logits(0, ctx)
-    o = orc.logits(0, ctx)
-    assert np.max(np.abs(g - o)) < LOGIT_TOL, np.max(np.abs(g - o))
-    g1 = eng.logits(1, ctx)
-    o1 = orc.logits(1, ctx)
-    assert np.max(np.abs(g1 - o1)) < LOGIT_TOL
+    orc64 = oracle_lib.TfPair(P.shape_dict(eng.target), P.shape_dict(eng.draft), P.Pair().as_dict(), accum="f64")
+    try:
+        ctxs = [_prompt(M, seed=200 + M + 1000 * i) for i in range(3)]
+        for which in (0, 1):
+            logit_noise_check(eng.logits, orc, orc64, which, ctxs)
+    finally:
+        orc64.close()
