@@ -421,6 +421,39 @@ ssd_status ssd_rng_u64(ssd_engine* e, uint64_t seed, int32_t n, uint64_t* out);
 ssd_status ssd_weight_bits(ssd_engine* e, int32_t which, int32_t layer, int32_t kind,
                            const int64_t* rows, const int64_t* cols, int32_t n, uint16_t* out);
 
+/* ------------------------------------------------ paged KV block manager
+ * SURVEY §8f row 4, the paper's engine: pages of
+ * page_tokens KV slots shared by the target and the draft cache; lookahead
+ * reservation for the K+1 verify / draft steps, reconciliation after
+ * verification (finalize full pages under a chained prefix hash, roll back
+ * pages reserved beyond the accepted suffix), and a prefix cache that maps a
+ * new prompt's cached full pages read-only (LRU eviction of unreferenced
+ * cached pages). Host bookkeeping (csrc/paged.cpp); the engine consumes the
+ * block tables (ssd_engine_set_block_table). Out of pages: SSD_TOO_LARGE
+ * (the caller preempts a sequence and retries). */
+typedef struct ssd_kv_pool ssd_kv_pool;
+typedef struct ssd_kv_stats {
+  int32_t n_pages, free_pages, used_pages, cached_pages, cached_evictable, sequences;
+  int64_t allocated, evictions, finalized, prefix_hit_pages, prefix_miss_pages, reserved_pages, rolled_back_pages;
+} ssd_kv_stats;
+ssd_status ssd_kv_pool_create(int32_t n_pages, int32_t page_tokens, ssd_kv_pool** out);
+void ssd_kv_pool_destroy(ssd_kv_pool* pool);
+/* Admit a prompt: maps its cached full prefix pages (*cached_tokens tokens
+ * whose KV need not be prefilled; never the page of the last token) and
+ * allocates the rest. */
+ssd_status ssd_kv_seq_admit(ssd_kv_pool* pool, int64_t seq, const int32_t* tokens, int32_t n, int32_t* cached_tokens);
+/* Ensure pages for committed length + lookahead (K + 1 before a round). */
+ssd_status ssd_kv_seq_reserve(ssd_kv_pool* pool, int64_t seq, int32_t lookahead);
+/* After verification: append the accepted tokens (k + 1), finalize full
+ * pages, release the reserved pages beyond them (*pages_released). */
+ssd_status ssd_kv_seq_commit(ssd_kv_pool* pool, int64_t seq, const int32_t* accepted, int32_t n_accepted,
+                             int32_t* pages_released);
+ssd_status ssd_kv_seq_release(ssd_kv_pool* pool, int64_t seq);
+ssd_status ssd_kv_seq_table(const ssd_kv_pool* pool, int64_t seq, int32_t* pages, int32_t cap, int32_t* n_pages,
+                            int32_t* n_tokens);
+ssd_status ssd_kv_pool_stats(const ssd_kv_pool* pool, ssd_kv_stats* out);
+ssd_status ssd_kv_page_refs(const ssd_kv_pool* pool, int32_t* refs, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

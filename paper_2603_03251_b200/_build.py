@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libssd_b200.so")
-SOURCES = ["engine.cu", "plans.cpp"]
+SOURCES = ["engine.cu", "plans.cpp", "paged.cpp"]
 # every header under csrc/ (a missing entry once left a stale library in place)
 DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -64,6 +64,14 @@ class RunOptionsC(C.Structure):
                 ("transcript_len", C.POINTER(C.c_int64))]
 
 
+class KvStats(C.Structure):
+    _fields_ = [("n_pages", C.c_int32), ("free_pages", C.c_int32), ("used_pages", C.c_int32),
+                ("cached_pages", C.c_int32), ("cached_evictable", C.c_int32), ("sequences", C.c_int32),
+                ("allocated", C.c_int64), ("evictions", C.c_int64), ("finalized", C.c_int64),
+                ("prefix_hit_pages", C.c_int64), ("prefix_miss_pages", C.c_int64), ("reserved_pages", C.c_int64),
+                ("rolled_back_pages", C.c_int64)]
+
+
 P = C.POINTER
 i32p, i64p, u64p, f32p, u16p = P(C.c_int32), P(C.c_int64), P(C.c_uint64), P(C.c_float), P(C.c_uint16)
 EngineP = C.c_void_p
@@ -134,6 +142,16 @@ SIGNATURES = {
     "ssd_cache_entry": (C.c_int, [EngineP, C.c_int32, i32p, f32p]),
     "ssd_rng_u64": (C.c_int, [EngineP, C.c_uint64, C.c_int32, u64p]),
     "ssd_weight_bits": (C.c_int, [EngineP, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, C.c_int32, u16p]),
+    # paged KV block manager (csrc/paged.cpp)
+    "ssd_kv_pool_create": (C.c_int, [C.c_int32, C.c_int32, P(C.c_void_p)]),
+    "ssd_kv_pool_destroy": (None, [C.c_void_p]),
+    "ssd_kv_seq_admit": (C.c_int, [C.c_void_p, C.c_int64, i32p, C.c_int32, i32p]),
+    "ssd_kv_seq_reserve": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32]),
+    "ssd_kv_seq_commit": (C.c_int, [C.c_void_p, C.c_int64, i32p, C.c_int32, i32p]),
+    "ssd_kv_seq_release": (C.c_int, [C.c_void_p, C.c_int64]),
+    "ssd_kv_seq_table": (C.c_int, [C.c_void_p, C.c_int64, i32p, C.c_int32, i32p, i32p]),
+    "ssd_kv_pool_stats": (C.c_int, [C.c_void_p, P(KvStats)]),
+    "ssd_kv_page_refs": (C.c_int, [C.c_void_p, i32p, C.c_int32]),
 }
 
 _lib = None

@@ -690,3 +690,66 @@ class Engine:
         _check(self.lib.ssd_weight_bits(self.h, which, layer, kind, _ptr(r, C.c_int64), _ptr(c, C.c_int64), len(r),
                                         _ptr(out, C.c_uint16)))
         return out
+
+
+class KvPool:
+    """Paged KV block manager (csrc/paged.cpp, the paper's
+    engine PAPER.md:1000-1002): lookahead reservation, reconciliation after
+    verification (finalize + prefix hash, rollback of pages beyond the
+    accepted suffix) and a prefix cache with LRU eviction."""
+
+    def __init__(self, n_pages: int, page_tokens: int):
+        self.lib = N.load()
+        self.h = C.c_void_p()
+        _check(self.lib.ssd_kv_pool_create(n_pages, page_tokens, C.byref(self.h)))
+        self.n_pages, self.page_tokens = n_pages, page_tokens
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.ssd_kv_pool_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def admit(self, seq: int, tokens: Sequence[int]) -> int:
+        """Returns the number of leading prompt tokens whose KV is cached."""
+        t = _i32(tokens)
+        cached = C.c_int32()
+        _check(self.lib.ssd_kv_seq_admit(self.h, seq, _ptr(t, C.c_int32), len(t), C.byref(cached)))
+        return cached.value
+
+    def reserve(self, seq: int, lookahead: int) -> None:
+        _check(self.lib.ssd_kv_seq_reserve(self.h, seq, lookahead))
+
+    def commit(self, seq: int, accepted: Sequence[int]) -> int:
+        """Append the accepted tokens; returns the pages rolled back."""
+        t = _i32(accepted)
+        rel = C.c_int32()
+        _check(self.lib.ssd_kv_seq_commit(self.h, seq, _ptr(t, C.c_int32) if len(t) else None, len(t),
+                                          C.byref(rel)))
+        return rel.value
+
+    def release(self, seq: int) -> None:
+        _check(self.lib.ssd_kv_seq_release(self.h, seq))
+
+    def table(self, seq: int) -> tuple:
+        """(block table, committed tokens)."""
+        n, ntok = C.c_int32(), C.c_int32()
+        _check(self.lib.ssd_kv_seq_table(self.h, seq, None, 0, C.byref(n), C.byref(ntok)))
+        out = np.zeros(max(n.value, 1), dtype=np.int32)
+        _check(self.lib.ssd_kv_seq_table(self.h, seq, _ptr(out, C.c_int32), len(out), C.byref(n), C.byref(ntok)))
+        return out[: n.value].tolist(), ntok.value
+
+    def stats(self) -> dict:
+        st = N.KvStats()
+        _check(self.lib.ssd_kv_pool_stats(self.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in N.KvStats._fields_}
+
+    def refs(self) -> list:
+        out = np.zeros(self.n_pages, dtype=np.int32)
+        _check(self.lib.ssd_kv_page_refs(self.h, _ptr(out, C.c_int32), self.n_pages))
+        return out.tolist()

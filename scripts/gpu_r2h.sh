@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 300 python scripts/pk_check.py tiny > gpurun_out/pk_tiny.log 2>&1; echo "exit $?" >> gpurun_out/pk_tiny.log
+timeout 600 python scripts/pk_check.py llama8b_1b > gpurun_out/pk_1b.log 2>&1; echo "exit $?" >> gpurun_out/pk_1b.log
+cat gpurun_out/pk_tiny.log gpurun_out/pk_1b.log

@@ -16,6 +16,14 @@ NEAR_TIE = 1e-2    # an argmax flip is accepted only when the oracle's top-2 gap
 
 
 NOISE_FACTOR = 3.0  # GPU deviation allowed, in units of the fp32 oracle's own deviation
+# A bf16 rounding flip of one activation (a value on a rounding boundary that
+# the GPU's fp32 summation order rounds the other way) moves the tiny target's
+# logits by up to ~0.02: measured, the same M = 33 context gives 0.0009 or
+# 0.0188 against the fp64 oracle from one run to the next under the atomic
+# split-K order (scripts/diag_state2.py, profiles/r02f_summary.md). Kernel bugs
+# (wrong head, mask, RoPE, tile) move logits by O(1).
+FLIP_MAX = 3e-2
+FLIP_RMS = 7.5e-3
 
 
 def logit_noise_check(get_gpu, orc32, orc64, which: int, contexts) -> dict:
@@ -27,8 +35,9 @@ def logit_noise_check(get_gpu, orc32, orc64, which: int, contexts) -> dict:
     moves logits by up to ~0.09 (measured: oracle fp32 vs fp64 on the
     2-layer 8B-shaped model, max 0.04-0.09, rms 0.010-0.019). So the bar is:
     the GPU's max / rms deviation from fp64, pooled over the contexts, is
-    within NOISE_FACTOR x the fp32 oracle's (floors LOGIT_TOL / LOGIT_TOL/4). A real
-    kernel bug (wrong head, mask, RoPE or tile) moves logits by O(1)."""
+    within NOISE_FACTOR x the fp32 oracle's, floored at one activation
+    rounding flip (FLIP_MAX / FLIP_RMS). A real kernel bug (wrong head, mask,
+    RoPE or tile) moves logits by O(1)."""
     g_max = g_rms = n_max = n_rms = 0.0
     for ctx in contexts:
         ref = orc64.logits(which, ctx).astype(np.float64)
@@ -37,8 +46,8 @@ def logit_noise_check(get_gpu, orc32, orc64, which: int, contexts) -> dict:
         g_max, n_max = max(g_max, float(np.abs(g).max())), max(n_max, float(np.abs(o).max()))
         g_rms, n_rms = max(g_rms, float(np.sqrt((g * g).mean()))), max(n_rms, float(np.sqrt((o * o).mean())))
     out = {"gpu_max": g_max, "gpu_rms": g_rms, "noise_max": n_max, "noise_rms": n_rms}
-    assert g_max <= max(LOGIT_TOL, NOISE_FACTOR * n_max), out
-    assert g_rms <= max(LOGIT_TOL / 4, NOISE_FACTOR * n_rms), out
+    assert g_max <= max(FLIP_MAX, NOISE_FACTOR * n_max), out
+    assert g_rms <= max(FLIP_RMS, NOISE_FACTOR * n_rms), out
     return out
 
 
