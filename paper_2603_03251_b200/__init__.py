@@ -6,7 +6,7 @@ Python mirror of the reference's interface used by tests and bench.py.
 """
 from .api import (  # noqa: F401
     BACKUP, FAST_RANDOM, PRIMARY, SAME_PRIMARY_JIT, AllZeroError, BudgetTooSmallError, ConfigError, CudaError,
-    DegenerateResidualError, DivergentError, Engine, Error, FanOutPlan, InsufficientDataError, NoCrossoverError, Pair,
+    DegenerateResidualError, DivergentError, Engine, Error, FanOutPlan, InsufficientDataError, KvPool, NoCrossoverError, Pair,
     ProtocolViolationError, RoundResult, RunStats, SamplingScheme, Stream, SimConfig, Speculation, SpeculationCache, TooLargeError,
     UnreachableError, conditional_hit_rate, critical_batch, derive_seed, fit_powerlaw, geometric_fanout, model_shape, saguaro_backup, shape_dict,
     speedup_batch, uniform_fanout)
