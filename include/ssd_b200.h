@@ -454,6 +454,19 @@ ssd_status ssd_kv_seq_table(const ssd_kv_pool* pool, int64_t seq, int32_t* pages
 ssd_status ssd_kv_pool_stats(const ssd_kv_pool* pool, ssd_kv_stats* out);
 ssd_status ssd_kv_page_refs(const ssd_kv_pool* pool, int32_t* refs, int32_t cap);
 
+/* The engine side of the paged KV cache: the main caches of both models as
+ * pages of page_tokens slots (page p = page p % ppl of lane p / ppl's main
+ * region, ppl = max_ctx / page_tokens; the same index in the target and the
+ * draft arena: *n_pages = lanes * ppl, the pool size). A lane's block table
+ * maps its logical pages to physical ones; its first cached_tokens prompt
+ * tokens already have their KV there (ssd_kv_seq_admit's prefix hit) and are
+ * not prefilled. page_tokens: a power of two dividing max_ctx. Branch slots
+ * (pre-speculation) are never paged. */
+ssd_status ssd_engine_kv_pages(ssd_engine* e, int32_t page_tokens, int32_t* n_pages);
+ssd_status ssd_engine_set_block_table(ssd_engine* e, int32_t lane, const int32_t* pages, int32_t n_pages,
+                                      int32_t page_tokens, int32_t cached_tokens);
+ssd_status ssd_engine_clear_block_tables(ssd_engine* e);
+
 #ifdef __cplusplus
 }
 #endif

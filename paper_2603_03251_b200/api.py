@@ -653,6 +653,21 @@ class Engine:
                                         C.byref(target_scheme.c()), accept_scale, seed, C.byref(acc), C.byref(bonus)))
         return acc.value, bonus.value
 
+    # ---- paged KV cache (ssd_engine_set_block_table)
+    def kv_pages(self, page_tokens: int) -> int:
+        """Pages of this engine's main caches (the KvPool size)."""
+        n = C.c_int32()
+        _check(self.lib.ssd_engine_kv_pages(self.h, page_tokens, C.byref(n)))
+        return n.value
+
+    def set_block_table(self, lane: int, pages: Sequence[int], page_tokens: int, cached_tokens: int = 0) -> None:
+        p = _i32(pages)
+        _check(self.lib.ssd_engine_set_block_table(self.h, lane, _ptr(p, C.c_int32) if len(p) else None, len(p),
+                                                   page_tokens, cached_tokens))
+
+    def clear_block_tables(self) -> None:
+        _check(self.lib.ssd_engine_clear_block_tables(self.h))
+
     def profile_forward(self, which: int, M: int, pos: int, iters: int) -> dict:
         f, g = C.c_double(), C.c_double()
         b, n = C.c_int64(), C.c_int32()

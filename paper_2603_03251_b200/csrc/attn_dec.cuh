@@ -78,7 +78,7 @@ template <int G, int HD, int MINB>
 __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
     const float* __restrict__ qkv, const FwdParams* __restrict__ P, int M, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, bf16* __restrict__ kc, bf16* __restrict__ vc, int S, int H, int KVH, float scale,
-    bf16* __restrict__ out, int kcap, int nst, int appended, Prefetch pf) {
+    bf16* __restrict__ out, int kcap, int nst, int appended, Prefetch pf, KvMap km) {
   constexpr int NW = kDecThreads / 32;
   constexpr int LPK = HD / 16;   // lanes per key
   constexpr int KPW = 32 / LPK;  // keys per warp pass
@@ -115,24 +115,36 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   }
   __syncthreads();
   if (tid == 0) {
+    // main rows are contiguous within a page (one run when unpaged)
+    const int run = km.tab ? (1 << km.shift) : (1 << 30);
     if (nst > 0) {
       const uint32_t sbytes = uint32_t(ns) * HD * 2;
       tc::mbar_expect_tx(bar, 2 * sbytes);
       if (sbytes) {
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        tc::bulk_load(Ks, kb + size_t(mb) * HD, sbytes, bar, pol);
-        tc::bulk_load(Vs, vb + size_t(mb) * HD, sbytes, bar, pol);
+        for (int j0 = 0; j0 < ns; j0 += run) {
+          const uint32_t rb = uint32_t(min(run, ns - j0)) * HD * 2;
+          const int sl = main_slot(km, mb, j0);
+          tc::bulk_load(Ks + size_t(j0) * HD, kb + size_t(sl) * HD, rb, bar, pol);
+          tc::bulk_load(Vs + size_t(j0) * HD, vb + size_t(sl) * HD, rb, bar, pol);
+        }
       }
     }
     prefetch_window(pf, kPfUnitBytes);
-    const uint32_t mbytes = uint32_t(main_len - ns) * HD * 2, bbytes = uint32_t(blen) * HD * 2;
-    if (mbytes >= 16) {
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kb + size_t(mb + ns) * HD), "r"(mbytes & ~15u)
-                   : "memory");
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + size_t(mb + ns) * HD), "r"(mbytes & ~15u)
-                   : "memory");
+    for (int j0 = ns; j0 < main_len; j0 += run) {
+      const int rows = km.tab ? min(run - (j0 & (run - 1)), main_len - j0) : main_len - j0;
+      const uint32_t mbytes = uint32_t(rows) * HD * 2;
+      const int sl = main_slot(km, mb, j0);
+      if (mbytes >= 16) {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kb + size_t(sl) * HD), "r"(mbytes & ~15u)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + size_t(sl) * HD), "r"(mbytes & ~15u)
+                     : "memory");
+      }
+      if (km.tab) j0 -= j0 & (run - 1);  // continue at the next page boundary
     }
+    const uint32_t bbytes = uint32_t(blen) * HD * 2;
     if (bbytes >= 16) {
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kb + size_t(bbase) * HD), "r"(bbytes & ~15u) : "memory");
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + size_t(bbase) * HD), "r"(bbytes & ~15u) : "memory");
@@ -151,7 +163,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   // appended: rope_append_kernel wrote this forward's rows before this
   // launch (wide forwards), so every key is read from the cache
   for (int t = tid; t < M && !appended; t += kDecThreads) {
-    const int j = visible_key(P->slot[t], mb, main_len, bbase, blen);
+    const int j = visible_token_key(P, t, mb, main_len, bbase, blen);
     if (j >= 0) ovr[j] = t;
   }
   // keys of this forward that fall in the staged range: patch the stale
@@ -159,7 +171,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   // and P.V read every staged key from shared memory
   for (int e = tid; e < M * HD && ns > 0; e += kDecThreads) {
     const int t = e / HD, d = e % HD;
-    const int j = visible_key(P->slot[t], mb, main_len, bbase, blen);
+    const int j = visible_token_key(P, t, mb, main_len, bbase, blen);
     if (j < 0 || j >= ns) continue;
     const int pos = P->pos[t];
     const float* x = qkv + size_t(t) * row_len + size_t(H + kvh) * HD;
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
         const int j = jb + u * NW * KPW + grp;
         tk[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tk[u] == -1) {
-          const int slot = j < main_len ? mb + j : bbase + (j - main_len);
+          const int slot = j < main_len ? main_slot(km, mb, j) : bbase + (j - main_len);
           const uint4* src = j < ns ? reinterpret_cast<const uint4*>(Ks + size_t(j) * HD + sub * 16)
                                     : reinterpret_cast<const uint4*>(kb + size_t(slot) * HD + sub * 16);
           kr[u][0] = j < ns ? src[0] : __ldcg(src);
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
         const int j = jb + u * NKG;
         tv[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tv[u] == -1) {
-          const int slot = j < main_len ? mb + j : bbase + (j - main_len);
+          const int slot = j < main_len ? main_slot(km, mb, j) : bbase + (j - main_len);
           vr[u] = j < ns ? reinterpret_cast<const uint4*>(Vs + size_t(j) * HD)[dc]
                          : __ldcg(reinterpret_cast<const uint4*>(vb + size_t(slot) * HD) + dc);
         }

@@ -137,6 +137,7 @@ struct Model {
   std::vector<DevLayer> layers;
   int S = 0;             // KV slots per kv-head: batch lanes x (main + branch region)
   int lane_S = 0;        // KV slots of one batch lane (lane l starts at l * lane_S)
+  KvMap km{nullptr, 0, 0, 0};  // paged main cache (ssd_engine_set_block_table): slot of main key j
   bf16* kc = nullptr;    // [L][KVH][S][hd]
   bf16* vc = nullptr;
   float* rope_cos = nullptr;
@@ -258,7 +259,11 @@ struct Engine {
   int pk_ctas = 0;      // SSD_B200_PK_CTAS: its grid (0 = every SM)
   int pk_pf_units = 4;  // SSD_B200_PK_PF: L2 look-ahead of its weight stream beyond the ring (32 KB units per CTA)
   int pk_nch = 0;       // SSD_B200_PK_NCH: attention key chunks per (kv head, token) (0: about two items per CTA)
-  unsigned long long* pk_trace = nullptr;  // SSD_B200_PK_TRACE=1: [SMs][kTrSlots] stamps of the last forward
+  unsigned long long* pk_trace = nullptr;
+  // paged main cache (ssd_engine_set_block_table): prompt tokens of each lane
+  // whose KV is already in its pages (prefix-cache hits): prefill starts there
+  std::vector<int> prefill_skip;
+  int page_tokens = 0;  // SSD_B200_PK_TRACE=1: [SMs][kTrSlots] stamps of the last forward
   // split processes (split.cuh)
   int role = 0;                      // 0 colocated, 1 verifier, 2 speculator
   Inbox* inbox = nullptr;            // this process's mailbox (+ draft rows)
@@ -459,6 +464,7 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
   // KV cache
   m.lane_S = s.max_ctx + branch_slots;
   m.S = lanes * m.lane_S;
+  m.km.lane_S = m.lane_S;
   m.kc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   m.vc = static_cast<bf16*>(own(dalloc<bf16>(m.kv_layer_elems() * size_t(s.n_layers))));
   std::vector<float> cs, sn;
@@ -943,7 +949,7 @@ static void attn_dec_launch_g(Model& m, int M, const FwdParams* P, bf16* kc, bf1
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, attention_dec_kernel<G, HD, MINB>, (const float*)m.qkv, P, M, (const float*)m.rope_cos,
                         (const float*)m.rope_sin, kc, vc, m.S, sh.n_heads, sh.n_kv_heads, scale, m.attn, kcap, nst,
-                        appended, pf));
+                        appended, pf, m.km));
 }
 
 static int g_attn_stage = 1;  // SSD_B200_ATTN_STAGE=0: never stage KV rows in shared memory
@@ -1009,6 +1015,11 @@ static void attend(Engine& E, Model& m, const FwdParams* P, int M, int l, cudaSt
   const int nch = attn_chunks(m);
   const AttnWs aws{m.attn_part, m.attn_cnt};
   ++E.launches;
+  if (m.km.tab) {  // a paged main cache: attention_dec (the kernel that reads through the block table)
+    if (!attn_dec_launch(m, M, P, kc, vc, scale, s, pf))
+      throw Fail(SSD_CONFIG, "paged KV: attention shape not covered by attention_dec");
+    return;
+  }
   if (E.attn_dec && (size_t(M) * KVH <= size_t(E_num_sms) || M >= E.attn_dec_wide_m) &&
       attn_dec_launch(m, M, P, kc, vc, scale, s, pf)) {
     // one CTA per (kv head, token) while they fit one wave (decode, verify,
@@ -1025,7 +1036,7 @@ static void attend(Engine& E, Model& m, const FwdParams* P, int M, int l, cudaSt
 
 // Persistent forward (fwd_pk.cuh): the whole step in one launch.
 static bool use_pk(const Engine& E, const Model& m, int M) {
-  if (M > pk::kMaxTok || !m.pk_ops || E.skip_mask) return false;
+  if (M > pk::kMaxTok || !m.pk_ops || E.skip_mask || m.km.tab) return false;
   const int hd = m.s.head_dim, G = m.s.n_heads / m.s.n_kv_heads;
   if (!((hd == 64 && (G == 1 || G == 4)) || (hd == 128 && G == 4))) return false;
   if (E.use_pk == 2) return true;
@@ -1150,9 +1161,15 @@ static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logit
 // token to `last_logits` when non-null.
 static void prefill(Engine& E, Model& m, int n, float* last_logits, cudaStream_t s, int lane = 0) {
   const int chunk = std::min(m.maxM, kMaxM);
-  for (int lo = 0; lo < n; lo += chunk) {
+  // a lane whose prompt prefix is mapped from the prefix cache (paged KV)
+  // starts after it; the last token is always computed when its logits are needed
+  int lo0 = 0;
+  if (m.km.tab && size_t(lane) < E.prefill_skip.size())
+    lo0 = std::max(0, std::min(E.prefill_skip[size_t(lane)], last_logits ? n - 1 : n));
+  for (int lo = lo0; lo < n; lo += chunk) {
     const int M = std::min(chunk, n - lo);
-    prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist + size_t(lane) * E.hist_stride, E.P_pre, lo, M, lane * m.lane_S);
+    prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist + size_t(lane) * E.hist_stride, E.P_pre, lo, M, lane * m.lane_S,
+                                            m.km);
     KCHECK();
     const bool last = lo + M >= n;
     forward(E, m, E.P_pre, M, (last && last_logits) ? m.logits : nullptr, s);
@@ -1242,7 +1259,7 @@ static void row_keys(Engine& E, const float* rows, int nrows, int V, int max_f, 
 static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int src, cudaStream_t s) {
   const DScheme ds = dscheme(sc);
   for (int i = 0; i < K; ++i) {
-    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, nullptr, 1, 0, 0);
+    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, nullptr, 1, 0, 0, E.D.km);
     forward(E, E.D, E.P_s, 1, E.dmain + size_t(i) * E.V, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
     row_pick(E, E.dmain + size_t(i) * E.V, size_t(E.V), 1, E.V, ds, E.ubuf, 1, &E.st->spec[i], 1, s);
@@ -1261,7 +1278,7 @@ static void draft_steps(Engine& E, int K, const ssd_scheme& sc, int origin, int 
 static void draft_lanes(Engine& E, int K, const ssd_scheme& sc, int origin, int src, int nl, cudaStream_t s) {
   const DScheme ds = dscheme(sc);
   for (int i = 0; i < K; ++i) {
-    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, E.d_lanes, nl, E.hist_stride, E.D.lane_S);
+    prep_draft_step_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_s, i, E.d_lanes, nl, E.hist_stride, E.D.lane_S, E.D.km);
     float* rows = E.dmain + size_t(i) * E.nbmax * E.V;
     forward(E, E.D, E.P_s, nl, rows, s);
     draw_lane_uniforms_kernel<<<1, 32, 0, s>>>(E.st, E.d_lanes, nl, E.ubuf);
@@ -1279,7 +1296,7 @@ static void draft_lanes(Engine& E, int K, const ssd_scheme& sc, int origin, int 
 // then the decision kernels).
 static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_scheme& ds, double scale, int use_draft_stream,
                          cudaStream_t s, int nl = 1) {
-  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1, E.hist_stride, E.T.lane_S);
+  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_t, K + 1, E.hist_stride, E.T.lane_S, E.T.km);
   KCHECK();
   forward(E, E.T, E.P_t, nl * (K + 1), E.tlogits, s);
   mark(E, 1, s);
@@ -1307,7 +1324,7 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
                          cudaStream_t s, int nl = 1, cudaEvent_t before_streams = nullptr, int Kb = -1) {
   if (Kb < 0) Kb = K;
-  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S);
+  prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S, E.D.km);
   KCHECK();
   forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
   mark(E, 4, s);
@@ -1691,7 +1708,7 @@ ssd_status ssd_run_ar(ssd_engine* h, const int32_t* prompt, int32_t n0, const ss
   E.launches = 0;
   GraphSet gs;
   gs.g.push_back(capture_graph(s, [&] {
-    prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1, E.hist_stride, E.T.lane_S);
+    prep_chain_kernel<<<1, 32, 0, s>>>(E.st, E.hist, E.P_t, 1, E.hist_stride, E.T.lane_S, E.T.km);
     forward(E, E.T, E.P_t, 1, E.tlogits, s);
     draw_uniforms_kernel<<<1, 32, 0, s>>>(&E.st->drng, E.ubuf, 1);
     row_pick(E, E.tlogits, size_t(E.V), 1, E.V, d, E.ubuf, 1, E.tok_scratch, 1, s);
@@ -2719,7 +2736,7 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
   cudaStream_t s = E.sv;
   m.ctx_bound = pos + M + 1;
-  prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M, 0);
+  prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M, 0, m.km);
   KCHECK();
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, F = sh.ffn, nqkv = m.qd + 2 * m.kvd;
@@ -2780,6 +2797,82 @@ ssd_status ssd_bench_read_bw(ssd_engine* h, int64_t bytes, int32_t iters, double
   *gbs = double(n) * 16.0 * iters / (ms * 1e-3) / 1e9;
   cudaFree(buf);
   cudaFree(sink);
+  API_END
+}
+
+
+// ------------------------------------------------------------- paged KV
+// the engine's main caches as pages of page_tokens slots
+// (page p = page p % ppl of lane p / ppl's main region, ppl = max_ctx /
+// page_tokens, the same page index in the target and the draft arena). A
+// lane's block table maps its logical pages to these; csrc/paged.cpp's pool
+// decides them (ssd_kv_seq_admit / reserve / commit).
+static int kv_ppl(const Engine& E, int pt) {
+  int ctx = 1 << 30;
+  for (const Model* m : {&E.T, &E.D})
+    if (m->kc) ctx = std::min(ctx, m->s.max_ctx);
+  if (pt < 1 || (pt & (pt - 1)) || ctx % pt) throw Fail(SSD_CONFIG, "paged KV: page_tokens must be a power of two dividing max_ctx");
+  return ctx / pt;
+}
+
+ssd_status ssd_engine_kv_pages(ssd_engine* h, int32_t page_tokens, int32_t* n_pages) {
+  API_BEGIN
+  Engine& E = h->e;
+  if (!n_pages) throw Fail(SSD_CONFIG, "kv pages: null output");
+  *n_pages = E.nbmax * kv_ppl(E, page_tokens);
+  API_END
+}
+
+ssd_status ssd_engine_set_block_table(ssd_engine* h, int32_t lane, const int32_t* pages, int32_t n, int32_t page_tokens,
+                                      int32_t cached_tokens) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  const int ppl = kv_ppl(E, page_tokens);
+  if (lane < 0 || lane >= E.nbmax) throw Fail(SSD_CONFIG, "block table: lane out of range");
+  if (n < 0 || n > ppl || (n > 0 && !pages)) throw Fail(SSD_TOO_LARGE, "block table: more pages than a lane's main cache");
+  if (E.page_tokens && E.page_tokens != page_tokens) throw Fail(SSD_CONFIG, "block table: page_tokens differs from the tables set");
+  for (int i = 0; i < n; ++i)
+    if (pages[i] < 0 || pages[i] >= E.nbmax * ppl) throw Fail(SSD_CONFIG, "block table: page out of range");
+  if (cached_tokens < 0 || cached_tokens > n * page_tokens) throw Fail(SSD_CONFIG, "block table: cached tokens beyond the pages");
+  int shift = 0;
+  while ((1 << shift) < page_tokens) ++shift;
+  for (Model* m : {&E.T, &E.D}) {
+    if (!m->kc) continue;
+    if (!m->km.tab) {  // identity for every lane
+      int* tab = static_cast<int*>(dalloc<int>(size_t(E.nbmax) * ppl));
+      m->owned.push_back(tab);
+      std::vector<int> id(static_cast<size_t>(E.nbmax) * static_cast<size_t>(ppl));
+      for (int l = 0; l < E.nbmax; ++l)
+        for (int i = 0; i < ppl; ++i) id[size_t(l) * ppl + i] = l * m->lane_S + i * page_tokens;
+      h2d(E, tab, id.data(), id.size() * 4);
+      m->km.tab = tab;
+    }
+    std::vector<int> row(static_cast<size_t>(ppl));
+    for (int i = 0; i < ppl; ++i) {
+      const int p = i < n ? pages[i] : lane * ppl + i;
+      row[size_t(i)] = (p / ppl) * m->lane_S + (p % ppl) * page_tokens;
+    }
+    h2d(E, const_cast<int*>(m->km.tab) + size_t(lane) * ppl, row.data(), row.size() * 4);
+    m->km.shift = shift;
+    m->km.lane_S = m->lane_S;
+    m->km.ppl = ppl;
+  }
+  E.page_tokens = page_tokens;
+  E.prefill_skip.resize(size_t(E.nbmax), 0);
+  E.prefill_skip[size_t(lane)] = cached_tokens;
+  E.ssd_graph_key.clear();  // captured graphs bake the (un)paged layout
+  API_END
+}
+
+ssd_status ssd_engine_clear_block_tables(ssd_engine* h) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  for (Model* m : {&E.T, &E.D}) m->km.tab = nullptr;  // the table allocation stays owned by the model
+  E.page_tokens = 0;
+  E.prefill_skip.clear();
+  E.ssd_graph_key.clear();
   API_END
 }
 

@@ -33,6 +33,28 @@ __device__ __forceinline__ int visible_key(int slot, int mbase, int main_len, in
   return -1;
 }
 
+// Paged main KV cache (the block manager is csrc/paged.cpp):
+// main key j of the lane whose main region starts at slot mb lives at slot
+// tab[lane][j >> shift] + (j & (page - 1)). tab == nullptr: the identity
+// layout, slot mb + j. Branch slots are never paged.
+struct KvMap {
+  const int* tab;  // [lanes][ppl]: slot base of each logical page, this model's arena
+  int shift;       // log2(page_tokens)
+  int lane_S;      // slots of one lane (main + branch region)
+  int ppl;         // pages per lane
+};
+__device__ __forceinline__ int main_slot(const KvMap& k, int mb, int j) {
+  if (!k.tab) return mb + j;
+  return k.tab[(mb / k.lane_S) * k.ppl + (j >> k.shift)] + (j & ((1 << k.shift) - 1));
+}
+// Key index of token t of this forward among the keys query (mb, main_len,
+// bbase, blen) sees, or -1: a main-cache token (blen 0) is key pos[t] of its
+// lane; a branch token is matched by slot (visible_key).
+__device__ __forceinline__ int visible_token_key(const FwdParams* P, int t, int mb, int main_len, int bbase, int blen) {
+  if (P->blen[t] == 0) return (P->mbase[t] == mb && P->pos[t] < main_len) ? P->pos[t] : -1;
+  return visible_key(P->slot[t], mb, main_len, bbase, blen);
+}
+
 // Batch lanes (run_protocol_harness with batch_size > 1, sim.cpp:502-601):
 // lane l's loop state is st[l], its history hist[l * hist_stride ..], its
 // main KV slots start at l * lane_slots of each model, and its pre-speculation
@@ -954,7 +976,7 @@ __global__ void __launch_bounds__(kSampleThreads) verify_decide_kernel(const flo
 // lanes: lane l fills rows [l*M, (l+1)*M) from st[l] and its history, its
 // main KV slots starting at l * lane_slots.
 __global__ void prep_chain_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int M,
-                                  int hist_stride, int lane_slots) {
+                                  int hist_stride, int lane_slots, KvMap km) {
   const int l = blockIdx.x, m = threadIdx.x;
   if (m >= M) return;
   st += l;
@@ -962,14 +984,15 @@ __global__ void prep_chain_kernel(const LoopState* __restrict__ st, const int* _
   const int n = st->n;
   const int tok = m == 0 ? hist[n - 1] : st->spec[m - 1];
   const int pos = n - 1 + m, r = l * M + m, mb = l * lane_slots;
-  P->tokens[r] = tok; P->pos[r] = pos; P->slot[r] = mb + pos;
+  P->tokens[r] = tok; P->pos[r] = pos; P->slot[r] = main_slot(km, mb, pos);
   P->main_len[r] = pos + 1; P->bbase[r] = 0; P->blen[r] = 0; P->mbase[r] = mb;
 }
 
 // Draft step i of specdec::draft: input hist[n-1] (i == 0) or spec[i-1].
 // Row m drafts for lane lanes[m] (lanes == nullptr: lane 0, one row).
 __global__ void prep_draft_step_kernel(const LoopState* __restrict__ st, const int* __restrict__ hist, FwdParams* P, int i,
-                                       const int* __restrict__ lanes, int nl, int hist_stride, int lane_slots) {
+                                       const int* __restrict__ lanes, int nl, int hist_stride, int lane_slots,
+                                       KvMap km) {
   const int m = threadIdx.x;
   if (m >= (lanes ? nl : 1)) return;
   const int l = lanes ? lanes[m] : 0;
@@ -978,17 +1001,17 @@ __global__ void prep_draft_step_kernel(const LoopState* __restrict__ st, const i
   const int n = st->n;
   const int pos = n - 1 + i, mb = l * lane_slots;
   P->tokens[m] = i == 0 ? hist[n - 1] : st->spec[i - 1];
-  P->pos[m] = pos; P->slot[m] = mb + pos; P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
+  P->pos[m] = pos; P->slot[m] = main_slot(km, mb, pos); P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0;
   P->mbase[m] = mb;
 }
 
 // Prefill of hist[lo, hi) (chunked by the caller, M <= kMaxM) into the main
 // KV slots starting at mb.
-__global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, int lo, int M, int mb) {
+__global__ void prep_prefill_kernel(const int* __restrict__ hist, FwdParams* P, int lo, int M, int mb, KvMap km) {
   const int m = threadIdx.x;
   if (m >= M) return;
   const int pos = lo + m;
-  P->tokens[m] = hist[pos]; P->pos[m] = pos; P->slot[m] = mb + pos;
+  P->tokens[m] = hist[pos]; P->pos[m] = pos; P->slot[m] = main_slot(km, mb, pos);
   P->main_len[m] = pos + 1; P->bbase[m] = 0; P->blen[m] = 0; P->mbase[m] = mb;
 }
 
