@@ -194,6 +194,10 @@ struct Engine {
   int V = 0;
   cudaStream_t sv = nullptr, ss = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_verified = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaEvent_t ev_extended = nullptr;
+  // colocated harness round: the verify forward waits for the speculator's
+  // extend forward (SSD_B200_VERIFY_AFTER_EXTEND)
+  int verify_after_extend = 0;
   LoopState* st = nullptr;
   int* hist = nullptr;
   FwdParams *P_t = nullptr, *P_x = nullptr, *P_b = nullptr, *P_s = nullptr, *P_pre = nullptr;
@@ -229,6 +233,7 @@ struct Engine {
   int attn_dec_wide_m = 20;
   long long cl_gemm_bytes = 72LL << 20;  // SSD_B200_CL_GEMM_MB: cluster split-K GEMM up to this size
   int cl_min_m = 17;                     // SSD_B200_CL_MIN_M: ... for forwards of at least this many tokens
+  int cl_fused = 0;                      // SSD_B200_CL_FUSED=1: ... also with atomic split-K (fused mode)
   // Deterministic forwards (fixed fp32 summation order: partials + ordered
   // last-arriver reduction, residual adds in the norm kernel). Forced for the
   // split roles, whose speculators must compute bit-identical key tables in
@@ -818,7 +823,13 @@ static void linear(Engine& E, Model& m, const WMat& W, const bf16* X, int M, flo
   // M <= 16 (profiles/r01_summary.md), so decode / verify steps keep stream-K.
   // (M <= 16 measured slower with the cluster kernel too: 1B step 1.29 vs
   // 1.13 ms, r02 profiles/r02_summary.md)
-  if (W.bytes <= E.cl_gemm_bytes && M >= E.cl_min_m && M > 16 && M <= 32 && m.gemm_ctas == 0) {
+  // (only with a fixed summation order: since split-K tiles accumulate with
+  // fp32 atomics, stream-K is faster at these widths — 1B branch step 1.63 ->
+  // 1.33 ms, colocated round 9.14 -> 8.49 ms, profiles/r02f_summary.md;
+  // SSD_B200_CL_FUSED=1 restores the cluster GEMM there)
+  const bool fused_mode = !E.deterministic && m.tp_size == 1;
+  if ((!fused_mode || E.cl_fused) && W.bytes <= E.cl_gemm_bytes && M >= E.cl_min_m && M > 16 && M <= 32 &&
+      m.gemm_ctas == 0) {
     gemm_cl_dispatch<EPI, 32>(m, W, X, M, Y, ldy, Yb, ldyb, s, pf, E.cl_small && W.bytes <= E.small_gemm_bytes);
     return;
   }
@@ -1322,11 +1333,13 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 // draws, so the branch half waits for the verifier. Kb: continuation length
 // of each entry (build_cache's next_lookahead; K in the loops).
 static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
-                         cudaStream_t s, int nl = 1, cudaEvent_t before_streams = nullptr, int Kb = -1) {
+                         cudaStream_t s, int nl = 1, cudaEvent_t before_streams = nullptr, int Kb = -1,
+                         cudaEvent_t after_extend = nullptr) {
   if (Kb < 0) Kb = K;
   prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S, E.D.km);
   KCHECK();
   forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
+  if (after_extend) CK(cudaEventRecord(after_extend, s));
   mark(E, 4, s);
   row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s, nl, B);
   if (before_streams) CK(cudaStreamWaitEvent(s, before_streams, 0));
@@ -1533,6 +1546,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* sg = std::getenv("SSD_B200_SMALL_GEMM_MB")) E.small_gemm_bytes = std::atoll(sg) << 20;
   if (const char* cg = std::getenv("SSD_B200_CL_GEMM_MB")) E.cl_gemm_bytes = std::atoll(cg) << 20;
   if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
+  if (const char* cf = std::getenv("SSD_B200_CL_FUSED")) E.cl_fused = std::atoi(cf) != 0;
   if (const char* sw = std::getenv("SSD_B200_SWIGLU_WHOLE")) g_swiglu_whole = std::atoi(sw) != 0;
   E.deterministic = role != SSD_ROLE_COLOCATED || tp_size > 1;
   if (const char* dt = std::getenv("SSD_B200_DETERMINISTIC")) E.deterministic = E.deterministic || std::atoi(dt) != 0;
@@ -1540,6 +1554,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
   if (const char* pkv = std::getenv("SSD_B200_PK")) E.use_pk = std::atoi(pkv);
+  if (const char* vae = std::getenv("SSD_B200_VERIFY_AFTER_EXTEND")) E.verify_after_extend = std::atoi(vae) != 0;
   if (const char* pkc = std::getenv("SSD_B200_PK_CTAS")) E.pk_ctas = std::max(0, std::atoi(pkc));
   if (const char* pkp = std::getenv("SSD_B200_PK_PF")) E.pk_pf_units = std::max(0, std::atoi(pkp));
   if (const char* pkn = std::getenv("SSD_B200_PK_NCH")) E.pk_nch = std::max(0, std::atoi(pkn));
@@ -1574,6 +1589,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_verified, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&E.ev_extended, cudaEventDisableTiming));
   CK(cudaEventCreate(&E.ev_t0));
   CK(cudaEventCreate(&E.ev_t1));
   CK(cudaEventCreateWithFlags(&E.ev_prespec, cudaEventDisableTiming));
@@ -1675,7 +1691,7 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   for (void* p : E.owned) cudaFree(p);
   for (cudaStream_t st : {E.sv, E.ss})
     if (st) cudaStreamDestroy(st);
-  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1, E.ev_prespec, E.ev_user})
+  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1, E.ev_prespec, E.ev_user, E.ev_extended})
     if (ev) cudaEventDestroy(ev);
   if (E.pin_rng) cudaFreeHost(E.pin_rng);
   for (cudaEvent_t ev : E.prof_ev)
@@ -1873,6 +1889,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
                 static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
   const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "") + " mode" + std::to_string(mode) +
+                          " vae" + std::to_string(E.verify_after_extend) +
                           (tr.i ? " tr" : "") + " n0 " + std::to_string(n0);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
@@ -1893,7 +1910,12 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
         CK(cudaEventRecord(E.ev_verified, sv));
         prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, E.ev_verified);
       } else {
-        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb);
+        // verify_after_extend: the verify forward starts when the extend
+        // forward has finished, so the speculator's first (critical-path)
+        // forward does not share HBM with the verifier's heaviest GEMMs
+        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, nullptr, -1,
+                     E.verify_after_extend ? E.ev_extended : nullptr);
+        if (E.verify_after_extend) CK(cudaStreamWaitEvent(sv, E.ev_extended, 0));
         verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
         CK(cudaEventRecord(E.ev_verified, sv));
         CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));

@@ -43,7 +43,8 @@ def summary(path, tail_from=None, top=25):
         a[1] += e.get("us", 0.0)
         a[2] += e.get("mb", 0.0)
     tot = sum(a[1] for a in agg.values())
-    print(f"{path}: {len(ids)} launches, {tot/1e3:.3f} ms total")
+    mb = sum(a[2] for a in agg.values())
+    print(f"{path}: {len(ids)} launches, {tot/1e3:.3f} ms total, {mb:.1f} MB DRAM read+write")
     for k, a in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
         gbs = a[2] / a[1] * 1e3 if a[1] else 0  # MB/us -> GB/s
         print(f"  {k[:44]:44s} n={a[0]:5d} {a[1]/1e3:8.3f} ms avg {a[1]/a[0]:8.2f} us  {100*a[1]/tot:5.1f}%  {gbs:8.0f} GB/s")
