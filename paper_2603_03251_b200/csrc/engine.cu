@@ -562,6 +562,9 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
 
 static int E_num_sms = 148;
 static int g_swiglu_whole = 1;  // SSD_B200_SWIGLU_WHOLE=0: always stream-K
+// ... when the tiles fill at least this many eighths of the SMs (1B gate/up:
+// 128 tiles on 148 SMs; SSD_B200_SWIGLU_WHOLE_FRAC8)
+static int g_swiglu_whole_frac8 = 6;
 
 static void free_model(Model& m) {
   for (void* p : m.owned) cudaFree(p);
@@ -594,7 +597,7 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
   // gate/up: 128 tiles on 148 SMs) one whole tile per CTA beats stream-K,
   // whose split tiles end in the partials + last-arriver reduction (~6 us
   // after the last MMA, scripts/ktl.py)
-  if (EPI == EPI_SWIGLU && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * 7) grid = tiles;
+  if (EPI == EPI_SWIGLU && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * g_swiglu_whole_frac8) grid = tiles;
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
   static int dbg_seq = 0;
   tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++, EPI == EPI_SWIGLU ? 0 : atomic};
@@ -868,7 +871,7 @@ struct PfCursor {
   int cap = 0;
   int parts(const WMat& w) const {
     const int tiles = (w.N + tc::kBM - 1) / tc::kBM;
-    if (w.swiglu && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * 7) return tiles;  // as gemm_tc_launch
+    if (w.swiglu && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * g_swiglu_whole_frac8) return tiles;  // as gemm_tc_launch
     return int(std::min<long long>(gemm_units(w), cap));
   }
   // Window up to `ahead` bytes past the start of GEMM `next` (index in seq).
@@ -1548,6 +1551,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
   if (const char* cf = std::getenv("SSD_B200_CL_FUSED")) E.cl_fused = std::atoi(cf) != 0;
   if (const char* sw = std::getenv("SSD_B200_SWIGLU_WHOLE")) g_swiglu_whole = std::atoi(sw) != 0;
+  if (const char* swf = std::getenv("SSD_B200_SWIGLU_WHOLE_FRAC8")) g_swiglu_whole_frac8 = std::max(1, std::atoi(swf));
   E.deterministic = role != SSD_ROLE_COLOCATED || tp_size > 1;
   if (const char* dt = std::getenv("SSD_B200_DETERMINISTIC")) E.deterministic = E.deterministic || std::atoi(dt) != 0;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
