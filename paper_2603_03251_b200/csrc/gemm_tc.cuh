@@ -255,13 +255,29 @@ struct Cfg {
   static constexpr int kBBlock = NP * kBK * 2;
   static constexpr int kBBytes = kBBlock * kKPS;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (kBudget / kStageBytes) < 2 ? 2
-                                 : ((kBudget / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
-                                                                                  : kBudget / kStageBytes);
+  // staging tile of the atomic split-K epilogue: [NP tokens][128 rows] fp32,
+  // added into Y with one TMA bulk reduce per token row (NP = 32: the M = 17..32
+  // branch steps; at M <= 16 a few atomics per thread are cheaper)
+  static constexpr int kCBytes = NP == 32 ? NP * kBM * 4 : 0;
+  // (the staging tile comes out of the 227 KB CTA limit, not the stage budget,
+  // while both fit: NP = 16 keeps its 6 stages)
+  static constexpr int kRing = kBudget < 227 * 1024 - 1280 - kCBytes ? kBudget : 227 * 1024 - 1280 - kCBytes;
+  static constexpr int kStages = (kRing / kStageBytes) < 2 ? 2
+                                 : ((kRing / kStageBytes) > SSD_GEMM_MAX_STAGES ? SSD_GEMM_MAX_STAGES
+                                                                                : kRing / kStageBytes);
   static constexpr int kAccCols = NP < 32 ? 32 : NP;
   static constexpr int kTmemCols = 2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512));
-  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + 256;
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + kCBytes + 256;
 };
+
+// Add `bytes` of fp32 from shared memory into global memory (TMA bulk
+// reduce-add at L2: one instruction per contiguous row instead of a red per
+// element).
+__device__ __forceinline__ void bulk_reduce_add_f32(float* dst, const float* src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
 
 template <int EPI, int NP, int BUDGET_KB = SSD_GEMM_SMEM_KB>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
@@ -271,7 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * C::kBBytes);
+  float* sC = reinterpret_cast<float*>(sB + S * C::kBBytes);  // [NP][128] (kCBytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * C::kBBytes + C::kCBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
@@ -405,6 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const int r = t * kBM + rl;
       // partial slot: first segment of this CTA -> 2*cta, later -> 2*cta+1
       float* part = g.ws + (size_t(2 * blockIdx.x + (u == u0 ? 0 : 1)) * g.M) * kBM;
+      // atomic mode: split segments (and whole residual tiles) are staged in
+      // shared memory and added with TMA bulk reduces (NP = 32)
+      const bool bulk = C::kCBytes > 0 && EPI != EPI_SWIGLU && g.atomic && (!whole || EPI == EPI_RESID);
 #pragma unroll 1
       for (int c = 0; c < NP; c += 8) {
         uint32_t v[8];
@@ -418,11 +438,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float f = __uint_as_float(v[j]);
-          if (whole) apply_epi<EPI>(g, r, c + j, f);
+          if (bulk) {
+            if (c + j < g.M) sC[(c + j) * kBM + rl] = f;
+          } else if (whole) apply_epi<EPI>(g, r, c + j, f);
           else if (EPI != EPI_SWIGLU && g.atomic) {
             if (r < g.N && c + j < g.M) atomicAdd(g.Y + size_t(c + j) * g.ldy + r, f);
           } else if (c + j < g.M) part[size_t(c + j) * kBM + rl] = f;
         }
+      }
+      if (C::kCBytes > 0 && bulk) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staged rows visible to the TMA unit
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          const int rows = min(kBM, g.N - t * kBM);
+          for (int m = 0; m < g.M; ++m)
+            bulk_reduce_add_f32(g.Y + size_t(m) * g.ldy + size_t(t) * kBM, sC + m * kBM, uint32_t(rows) * 4);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // sC free again
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        u = seg_end;
+        continue;
       }
 #if SSD_KTL
       if (threadIdx.x == 64 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][4] = ktl_now();
@@ -486,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       u = seg_end;
     }
   }
+  if (C::kCBytes > 0 && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
