@@ -2297,7 +2297,10 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
   E.seq_base += int(R) + 2;
   if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
   Inbox** vpeers = E.peers_dev;  // [0..T) verifier ranks, [T..T+G) speculators
-  const int send_blocks = 2 * E_num_sms;
+  // greedy draft and target: the verification reads tokens only, so the
+  // message carries no draft rows (2 MB per round at K = 4, V = 128256)
+  const int with_rows = (c->scheme.temperature > 0.0 || c->target_scheme.temperature > 0.0) ? 1 : 0;
+  const int send_blocks = with_rows ? 2 * E_num_sms : 1;
   // initial synchronous draft, clock starts at T_p (sim.cpp:524-526)
   draft_steps(E, K, c->scheme, 0, 0, s);
   {
@@ -2306,7 +2309,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(E.st) + offsetof(LoopState, clock), &tmp.clock, sizeof(double),
                        cudaMemcpyHostToDevice, s));
   }
-  send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter);
+  send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter, with_rows);
   KCHECK();
   const bool jit = c->backup_kind == 0;
   E.launches = 0;
@@ -2317,7 +2320,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
       recv_outcome_kernel<<<1, 32, 0, s>>>(E.st, E.inbox, E.hist);
       lookup_kernel<<<1, 32, 0, s>>>(E.st, 1, E.keys, max_f, E.offs, E.bt, E.brows[parity], lo, Bl, 0, E.V, E.cum, nullptr,
                                      d_hit, 0, TrLog{nullptr, nullptr, 0});
-      send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 0, E.send_counter);
+      send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 0, E.send_counter, with_rows);
       recv_peer_spec_kernel<<<1, 32, 0, s>>>(E.st, E.inbox);
       KCHECK();
       E.launches += 4;
@@ -2336,7 +2339,7 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
       if (!hit) {  // SamePrimaryJIT re-draft (sim.cpp:229-232), identical on every speculator; rank 0 sends
         const long long before = E.launches;
         draft_steps(E, K, c->scheme, 1, 2, s);
-        send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter);
+        send_spec_kernel<<<send_blocks, 256, 0, s>>>(E.st, vpeers, T, n_spec, rank, E.V, 1, E.send_counter, with_rows);
         KCHECK();
         jit_launches += E.launches - before + 1;
       }

@@ -150,12 +150,14 @@ __global__ void recv_outcome_kernel(LoopState* st, const Inbox* in, int* hist) {
 // Speculator: send the speculation for round st->round (after lookup /
 // backup) to the verifier. Sender: the owner of a hit, or speculator 0 for a
 // backup (every speculator computes the identical backup) or the initial /
-// JIT draft (force). Rows [K][V] are copied by all CTAs; the last CTA to
-// finish publishes the header (release) so the rows are visible first.
+// JIT draft (force). Rows [K][V] are copied by all CTAs (not at all when
+// with_rows is 0: greedy draft and target, whose verification never reads
+// them); the last CTA to finish publishes the header (release) so the rows
+// are visible first.
 // peers[0..T) = verifier inboxes (the ranks of a tensor-parallel verifier
 // all verify the same speculation), peers[T..T+G) = speculator inboxes.
 __global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* const* peers, int T, int G, int rank,
-                                                        int V, int force, int* counter) {
+                                                        int V, int force, int* counter, int with_rows) {
   __shared__ int s_send, s_last;
   const int K = st->K;
   const int rslot = (st->seq_base + st->round + 1) & 1;  // rows slot of this message
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* co
   }
   __syncthreads();
   if (!s_send) return;
-  if (!st->spec_uniform) {
+  if (!st->spec_uniform && with_rows) {
     const size_t n4 = size_t(V) / 4;  // V % 4 == 0 (checked on the host)
     for (int i = 0; i < K; ++i) {
       const float4* src = reinterpret_cast<const float4*>(st->spec_rows[i]);
