@@ -2297,10 +2297,10 @@ ssd_status ssd_run_ssd_speculator(ssd_engine* h, const int32_t* prompt, int32_t 
   E.seq_base += int(R) + 2;
   if (n0 > 1) prefill(E, E.D, n0 - 1, nullptr, s);
   Inbox** vpeers = E.peers_dev;  // [0..T) verifier ranks, [T..T+G) speculators
-  // greedy draft and target: the verification reads tokens only, so the
-  // message carries no draft rows (2 MB per round at K = 4, V = 128256)
-  const int with_rows = (c->scheme.temperature > 0.0 || c->target_scheme.temperature > 0.0) ? 1 : 0;
-  const int send_blocks = with_rows ? 2 * E_num_sms : 1;
+  // (the verification's sanity checks read the draft rows in every mode, so
+  // the message always carries them)
+  const int with_rows = 1;
+  const int send_blocks = 2 * E_num_sms;
   // initial synchronous draft, clock starts at T_p (sim.cpp:524-526)
   draft_steps(E, K, c->scheme, 0, 0, s);
   {

@@ -150,10 +150,9 @@ __global__ void recv_outcome_kernel(LoopState* st, const Inbox* in, int* hist) {
 // Speculator: send the speculation for round st->round (after lookup /
 // backup) to the verifier. Sender: the owner of a hit, or speculator 0 for a
 // backup (every speculator computes the identical backup) or the initial /
-// JIT draft (force). Rows [K][V] are copied by all CTAs (not at all when
-// with_rows is 0: greedy draft and target, whose verification never reads
-// them); the last CTA to finish publishes the header (release) so the rows
-// are visible first.
+// JIT draft (force). Rows [K][V] are copied by all CTAs (with_rows = 1: the
+// verification reads them in every mode); the last CTA to finish publishes
+// the header (release) so the rows are visible first.
 // peers[0..T) = verifier inboxes (the ranks of a tensor-parallel verifier
 // all verify the same speculation), peers[T..T+G) = speculator inboxes.
 __global__ void __launch_bounds__(256) send_spec_kernel(LoopState* st, Inbox* const* peers, int T, int G, int rank,
