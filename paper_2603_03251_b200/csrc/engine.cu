@@ -21,7 +21,6 @@
 #include "../../include/ssd_b200.h"
 #include "gemm_tc.cuh"
 #include "gemm_cl.cuh"
-#include "fwd_pk.cuh"
 #include "attn_cl.cuh"
 #include "attn_dec.cuh"
 #include "tp.cuh"
@@ -157,15 +156,6 @@ struct Model {
   float* ws = nullptr;   // split-K partials
   size_t ws_floats = 0;
   int* counters = nullptr;
-  // persistent forward kernel (fwd_pk.cuh): its op list (with the LM head
-  // last), completion / attention-chunk counters, gate-up accumulator
-  pk::PkOp* pk_ops = nullptr;
-  int pk_nops = 0;
-  int* pk_done = nullptr;
-  int* pk_attn_cnt = nullptr;
-  float* pk_gu = nullptr;
-  float* pk_rs = nullptr;
-  float* pk_attn_part = nullptr;
   std::vector<ActMap> amaps;
   std::vector<void*> owned;
   int gemm_ctas = 0;                        // cap on a GEMM's CTAs (0 = every SM)
@@ -258,17 +248,10 @@ struct Engine {
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
   int split_t = 0, split_d = 0;
-  // Persistent layer-block kernel (fwd_pk.cuh) for forwards of <= 32 tokens:
-  // SSD_B200_PK=0 off (default: measured slower), 1 the draft model, 2 both models.
-  int use_pk = 0;
-  int pk_ctas = 0;      // SSD_B200_PK_CTAS: its grid (0 = every SM)
-  int pk_pf_units = 4;  // SSD_B200_PK_PF: L2 look-ahead of its weight stream beyond the ring (32 KB units per CTA)
-  int pk_nch = 0;       // SSD_B200_PK_NCH: attention key chunks per (kv head, token) (0: about two items per CTA)
-  unsigned long long* pk_trace = nullptr;
   // paged main cache (ssd_engine_set_block_table): prompt tokens of each lane
   // whose KV is already in its pages (prefix-cache hits): prefill starts there
   std::vector<int> prefill_skip;
-  int page_tokens = 0;  // SSD_B200_PK_TRACE=1: [SMs][kTrSlots] stamps of the last forward
+  int page_tokens = 0;
   // split processes (split.cuh)
   int role = 0;                      // 0 colocated, 1 verifier, 2 speculator
   Inbox* inbox = nullptr;            // this process's mailbox (+ draft rows)
@@ -503,61 +486,6 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
     m.attn_part = static_cast<float*>(own(dalloc<float>(size_t(maxM) * s.n_kv_heads * chunks * G * (hd + 2))));
     m.attn_cnt = static_cast<int*>(own(dalloc<int>(size_t(maxM) * s.n_kv_heads)));
   }
-  // persistent forward kernel (fwd_pk.cuh): op indices EMBED 0; layer l
-  // (base 9l): QKV 1, APPEND 2, ATTN 3, O 4, NORM 5, GU 6, SWIGLU 7, DN 8,
-  // NORM 9; HEAD 1 + 9L. Zero-fill duties (split-K accumulation targets):
-  // QKV(0)'s at EMBED, QKV(l+1)'s at O(l) once ATTN(l) has read it, GU(l)'s
-  // at ATTN(l) once SWIGLU(l-1) has read it, the logits at O(L-1).
-  if (tp_size == 1 && maxM >= pk::kMaxTok) {
-    const int L = s.n_layers, F = s.ffn, nqkv = m.qd + 2 * m.kvd;
-    m.pk_gu = static_cast<float*>(own(dalloc<float>(size_t(pk::kMaxTok) * 2 * F)));
-    m.pk_rs = static_cast<float*>(own(dalloc<float>(pk::kMaxTok)));
-    std::vector<pk::PkOp> ops;
-    auto base = [](int kind) { pk::PkOp o{}; o.kind = kind; o.zero_after = -1; return o; };
-    auto gemm = [&](const WMat& W, int in, const float* gain, const bf16* src, int ld_src, float* out, int ld_out) {
-      pk::PkOp o = base(pk::OP_GEMM);
-      o.W = W.w; o.N = W.N; o.KU = W.K / (tc::kBK * tc::kKPS);
-      o.in = in; o.gain = gain; o.src = src; o.ld_src = ld_src; o.out = out; o.ld_out = ld_out;
-      return o;
-    };
-    pk::PkOp e = base(pk::OP_EMBED);
-    e.zero = m.qkv; e.zero_ld = nqkv; e.zero_cols = nqkv;
-    ops.push_back(e);
-    for (int l = 0; l < L; ++l) {
-      const DevLayer& Ly = m.layers[size_t(l)];
-      const int b0 = 9 * l;
-      ops.push_back(gemm(Ly.qkv, pk::IN_NORM, nullptr, nullptr, 0, m.qkv, nqkv));
-      pk::PkOp ap = base(pk::OP_APPEND);
-      ap.kc = m.kc + size_t(l) * m.kv_layer_elems();
-      ap.vc = m.vc + size_t(l) * m.kv_layer_elems();
-      ap.qkv = m.qkv;
-      ops.push_back(ap);
-      pk::PkOp at = ap;
-      at.kind = pk::OP_ATTN;
-      at.attn = m.attn;
-      at.zero = m.pk_gu; at.zero_ld = 2 * F; at.zero_cols = 2 * F; at.zero_after = l > 0 ? b0 - 2 : -1;
-      ops.push_back(at);
-      pk::PkOp o = gemm(Ly.o, pk::IN_BF16, nullptr, m.attn, m.qd, m.x, d);
-      if (l + 1 < L) { o.zero = m.qkv; o.zero_ld = nqkv; o.zero_cols = nqkv; o.zero_after = b0 + 3; }
-      else { o.zero = reinterpret_cast<float*>(1); o.zero_ld = s.vocab; o.zero_cols = s.vocab; }
-      ops.push_back(o);
-      ops.push_back(base(pk::OP_NORM));
-      ops.push_back(gemm(Ly.gu, pk::IN_NORM, l == 0 ? m.ffn_gain0 : nullptr, nullptr, 0, m.pk_gu, 2 * F));
-      pk::PkOp sw = base(pk::OP_SWIGLU);
-      sw.gu = m.pk_gu; sw.act = m.act; sw.ffn = F;
-      ops.push_back(sw);
-      ops.push_back(gemm(Ly.dn, pk::IN_BF16, nullptr, m.act, F, m.x, d));
-      ops.push_back(base(pk::OP_NORM));
-    }
-    ops.push_back(gemm(m.head, pk::IN_NORM, m.final_gain, nullptr, 0, nullptr, 0));
-    m.pk_nops = int(ops.size());
-    m.pk_ops = static_cast<pk::PkOp*>(own(dalloc<pk::PkOp>(ops.size())));
-    CK(cudaMemcpy(m.pk_ops, ops.data(), ops.size() * sizeof(pk::PkOp), cudaMemcpyHostToDevice));
-    m.pk_done = static_cast<int*>(own(dalloc<int>((ops.size() * pk::kStripes + 1) * pk::kLine)));
-    m.pk_attn_cnt = static_cast<int*>(own(dalloc<int>(size_t(s.n_kv_heads) * pk::kMaxTok * pk::kLine)));
-    m.pk_attn_part = static_cast<float*>(own(dalloc<float>(size_t(s.n_kv_heads) * pk::kMaxTok * pk::kMaxChunks *
-                                                           (pk::kRows * hd + 2 * pk::kRows))));
-  }
 }
 
 static int E_num_sms = 148;
@@ -687,13 +615,6 @@ static void carveout_max(F* f) {
                           int(cudaSharedmemCarveoutMaxShared)));
 }
 
-template <int NP, int HD, int G>
-static void pk_configure_t() {
-  CK(cudaFuncSetAttribute(pk::pk_kernel<NP, HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(pk::Cfg<NP, HD, G>::kSmem)));
-  carveout_max(pk::pk_kernel<NP, HD, G>);
-}
-
 // Kernel attributes are set once, outside any stream capture.
 static void configure_kernels() {
   carveout_max(embed_kernel);
@@ -739,9 +660,6 @@ static void configure_kernels() {
   carveout_max(gen_layer_kernel);
   carveout_max(gen_table_kernel);
   carveout_max(rope_append_kernel);
-  pk_configure_t<16, 64, 1>(); pk_configure_t<32, 64, 1>();
-  pk_configure_t<16, 64, 4>(); pk_configure_t<32, 64, 4>();
-  pk_configure_t<16, 128, 4>(); pk_configure_t<32, 128, 4>();
   configure_gemm<EPI_STORE, 16>(); configure_gemm<EPI_SWIGLU, 16>();
   configure_gemm<EPI_STORE, 32>(); configure_gemm<EPI_SWIGLU, 32>();
   configure_gemm<EPI_STORE, 48>(); configure_gemm<EPI_SWIGLU, 48>();
@@ -1048,72 +966,11 @@ static void attend(Engine& E, Model& m, const FwdParams* P, int M, int l, cudaSt
   }
 }
 
-// Persistent forward (fwd_pk.cuh): the whole step in one launch.
-static bool use_pk(const Engine& E, const Model& m, int M) {
-  if (M > pk::kMaxTok || !m.pk_ops || E.skip_mask || m.km.tab) return false;
-  const int hd = m.s.head_dim, G = m.s.n_heads / m.s.n_kv_heads;
-  if (!((hd == 64 && (G == 1 || G == 4)) || (hd == 128 && G == 4))) return false;
-  if (E.use_pk == 2) return true;
-  return E.use_pk == 1 && m.role == 1;
-}
-
-template <int NP, int HD, int G>
-static void pk_launch_t(const pk::PkArgs& a, int grid, cudaStream_t s) {
-  launch_pdl(pk::pk_kernel<NP, HD, G>, dim3(grid), dim3(pk::kThreads), pk::Cfg<NP, HD, G>::kSmem, s, a);
-}
-
-static void forward_pk(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
-  const ssd_model_shape& sh = m.s;
-  const int grid = E.pk_ctas > 0 ? std::min(E.pk_ctas, E_num_sms) : E_num_sms;
-  const int hd = sh.head_dim, G = sh.n_heads / sh.n_kv_heads;
-  pk::PkArgs a{};
-  a.ops = m.pk_ops;
-  a.n_ops = logits ? m.pk_nops : m.pk_nops - 1;
-  a.M = M;
-  a.P = P;
-  a.embed = m.embed;
-  a.embed_tiled = m.embed_tiled;
-  a.d = sh.d_model;
-  a.H = sh.n_heads;
-  a.KVH = sh.n_kv_heads;
-  a.S = m.S;
-  a.eps = sh.norm_eps;
-  a.scale = 1.0f / std::sqrt(float(hd));
-  a.rope_cos = m.rope_cos;
-  a.rope_sin = m.rope_sin;
-  a.x = m.x;
-  a.rs = m.pk_rs;
-  a.logits = logits;
-  // attention: items (kv head, key chunk, query block) about one per CTA
-  const int nk = std::min(m.ctx_bound, sh.max_ctx + m.branch_len + 1);
-  const int nqb = (M + pk::kRows / G - 1) / (pk::kRows / G);
-  int nch = std::max(1, grid / (sh.n_kv_heads * nqb));
-  if (E.pk_nch > 0) nch = E.pk_nch;
-  nch = std::min(nch, pk::kMaxChunks);
-  const int passes = std::max(1, (nk + pk::kKeysPass - 1) / pk::kKeysPass);
-  a.chunk = std::max(1, (passes + nch - 1) / nch) * pk::kKeysPass;
-  a.done = m.pk_done;
-  a.attn_cnt = m.pk_attn_cnt;
-  a.attn_part = m.pk_attn_part;
-  a.pf_units = E.pk_pf_units;
-  a.trace = E.pk_trace;
-  a.trace_ops = pk::kTrOps;
-  const bool np16 = M <= 16;
-  if (hd == 64 && G == 1) np16 ? pk_launch_t<16, 64, 1>(a, grid, s) : pk_launch_t<32, 64, 1>(a, grid, s);
-  else if (hd == 64) np16 ? pk_launch_t<16, 64, 4>(a, grid, s) : pk_launch_t<32, 64, 4>(a, grid, s);
-  else np16 ? pk_launch_t<16, 128, 4>(a, grid, s) : pk_launch_t<32, 128, 4>(a, grid, s);
-  ++E.launches;
-}
-
 // One forward step of `m` over the M tokens described by P. Logits of all M
 // rows go to `logits` ([M][V]) when non-null. Every kernel is launched with
 // PDL so each GEMM streams its weights while its predecessor finishes.
 static void forward(Engine& E, Model& m, const FwdParams* P, int M, float* logits, cudaStream_t s) {
   if (M > m.maxM) throw Fail(SSD_CONFIG, "forward: M exceeds capacity");
-  if (use_pk(E, m, M)) {
-    forward_pk(E, m, P, M, logits, s);
-    return;
-  }
   const ssd_model_shape& sh = m.s;
   const int d = sh.d_model, F = sh.ffn;
   const int nqkv = m.qd + 2 * m.kvd;
@@ -1557,11 +1414,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;
   if (const char* cls = std::getenv("SSD_B200_CL_SMALL")) E.cl_small = std::atoi(cls) != 0;
   if (const char* ca = std::getenv("SSD_B200_CORUN_ATTN_KB")) E.corun_attn_kb = std::max(8, std::min(227, std::atoi(ca)));
-  if (const char* pkv = std::getenv("SSD_B200_PK")) E.use_pk = std::atoi(pkv);
   if (const char* vae = std::getenv("SSD_B200_VERIFY_AFTER_EXTEND")) E.verify_after_extend = std::atoi(vae) != 0;
-  if (const char* pkc = std::getenv("SSD_B200_PK_CTAS")) E.pk_ctas = std::max(0, std::atoi(pkc));
-  if (const char* pkp = std::getenv("SSD_B200_PK_PF")) E.pk_pf_units = std::max(0, std::atoi(pkp));
-  if (const char* pkn = std::getenv("SSD_B200_PK_NCH")) E.pk_nch = std::max(0, std::atoi(pkn));
   if (const char* sp = std::getenv("SSD_B200_SPLIT_SMS")) std::sscanf(sp, "%d,%d", &E.split_t, &E.split_d);
   {
     int sms = 0;
@@ -1605,9 +1458,6 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   E.hist_stride = std::max(target->max_ctx, draft->max_ctx) + K + 2;
   E.hist = static_cast<int*>(own(dalloc<int>(size_t(nb) * E.hist_stride)));
   E.d_lanes = static_cast<int*>(own(dalloc<int>(size_t(nb))));
-  if (std::getenv("SSD_B200_PK_TRACE"))
-    E.pk_trace = static_cast<unsigned long long*>(
-        own(dalloc<unsigned long long>(size_t(E_num_sms) * pk::kTrSlots)));
   E.P_t = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_x = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
   E.P_b = static_cast<FwdParams*>(own(dalloc<FwdParams>(1)));
@@ -2903,18 +2753,6 @@ ssd_status ssd_engine_clear_block_tables(ssd_engine* h) {
   E.prefill_skip.clear();
   E.ssd_graph_key.clear();
   API_END
-}
-
-// Persistent-kernel timeline of the last traced forward (SSD_B200_PK_TRACE=1):
-// [SMs][pk::kTrSlots] globaltimer stamps; returns the element count.
-extern "C" int ssd_debug_pk_trace(ssd_engine* h, unsigned long long* out, int n) {
-  if (!h || !h->e.pk_trace) return -1;
-  const int total = ssd::E_num_sms * ssd::pk::kTrSlots;
-  if (n < total) return -2;
-  cudaDeviceSynchronize();
-  cudaMemcpy(out, h->e.pk_trace, size_t(total) * 8, cudaMemcpyDeviceToHost);
-  cudaMemset(h->e.pk_trace, 0, size_t(total) * 8);
-  return total;
 }
 
 #if SSD_GEMM_TRACE
