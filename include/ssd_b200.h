@@ -467,6 +467,17 @@ ssd_status ssd_engine_set_block_table(ssd_engine* e, int32_t lane, const int32_t
                                       int32_t page_tokens, int32_t cached_tokens);
 ssd_status ssd_engine_clear_block_tables(ssd_engine* e);
 
+/* B200 execution knob, no reference counterpart: the colocated SSD round
+ * runs its verifier branch and its speculator branch on disjoint SM sets
+ * (two CUDA green contexts). verifier_sms > 0 sets the verifier's share
+ * (rounded by the driver to its partition granularity; the speculator gets
+ * the rest), 0 shares all SMs between the two streams, < 0 leaves the
+ * partition unchanged. *out_verifier / *out_speculator (nullable) receive
+ * the SM counts in effect (0, 0 when shared). Colocated single-GPU engines
+ * only (SSD_CONFIG otherwise); the default is 3/8 of the SMs. */
+ssd_status ssd_engine_sm_partition(ssd_engine* e, int32_t verifier_sms, int32_t* out_verifier,
+                                   int32_t* out_speculator);
+
 #ifdef __cplusplus
 }
 #endif

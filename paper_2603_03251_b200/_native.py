@@ -153,6 +153,7 @@ SIGNATURES = {
     "ssd_kv_pool_stats": (C.c_int, [C.c_void_p, P(KvStats)]),
     "ssd_kv_page_refs": (C.c_int, [C.c_void_p, i32p, C.c_int32]),
     "ssd_engine_kv_pages": (C.c_int, [EngineP, C.c_int32, i32p]),
+    "ssd_engine_sm_partition": (C.c_int, [EngineP, C.c_int32, i32p, i32p]),
     "ssd_engine_set_block_table": (C.c_int, [EngineP, C.c_int32, i32p, C.c_int32, C.c_int32, C.c_int32]),
     "ssd_engine_clear_block_tables": (C.c_int, [EngineP]),
 }

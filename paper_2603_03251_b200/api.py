@@ -668,6 +668,15 @@ class Engine:
     def clear_block_tables(self) -> None:
         _check(self.lib.ssd_engine_clear_block_tables(self.h))
 
+    # ---- B200 knob: disjoint SM sets for the colocated round's two streams
+    def sm_partition(self, verifier_sms: int | None = None) -> tuple[int, int]:
+        """(verifier SMs, speculator SMs) of the colocated SSD round; with
+        verifier_sms set first (0 = both streams share every SM)."""
+        v, s = C.c_int32(), C.c_int32()
+        _check(self.lib.ssd_engine_sm_partition(self.h, -1 if verifier_sms is None else int(verifier_sms),
+                                                C.byref(v), C.byref(s)))
+        return v.value, s.value
+
     def profile_forward(self, which: int, M: int, pos: int, iters: int) -> dict:
         f, g = C.c_double(), C.c_double()
         b, n = C.c_int64(), C.c_int32()

@@ -67,6 +67,45 @@ static void init_encode() {
   g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
+template <class Fn>
+static Fn driver_fn(const char* name) {
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  CK(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) throw Fail(SSD_CUDA, std::string(name) + " unavailable");
+  return reinterpret_cast<Fn>(fn);
+}
+
+#define DRV(call) do { const CUresult r_ = (call); \
+  if (r_ != CUDA_SUCCESS) throw Fail(SSD_CUDA, std::string(#call) + " failed: " + std::to_string(int(r_))); } while (0)
+
+// Two green contexts on `device`: want_v SMs (rounded by the driver to its
+// partition granularity) and the remaining SMs, one non-blocking stream in
+// each. The streams take runtime launches and stream capture; the captured
+// kernels keep their partition when the graph is launched on any stream
+// (scripts/green_probe.cu, profiles/r02g_summary.md).
+static void make_green_streams(int device, int want_v, CUgreenCtx ctx[2], cudaStream_t st[2], int sms[2]) {
+  auto get_res = driver_fn<PFN_cuDeviceGetDevResource_v12040>("cuDeviceGetDevResource");
+  auto split = driver_fn<PFN_cuDevSmResourceSplitByCount_v12040>("cuDevSmResourceSplitByCount");
+  auto gen = driver_fn<PFN_cuDevResourceGenerateDesc_v12040>("cuDevResourceGenerateDesc");
+  auto create = driver_fn<PFN_cuGreenCtxCreate_v12040>("cuGreenCtxCreate");
+  auto mkstream = driver_fn<PFN_cuGreenCtxStreamCreate_v12050>("cuGreenCtxStreamCreate");
+  CUdevResource all, part[2];
+  DRV(get_res(CUdevice(device), &all, CU_DEV_RESOURCE_TYPE_SM));
+  unsigned n = 1;
+  DRV(split(&part[0], &n, &all, &part[1], 0, unsigned(want_v)));
+  if (n != 1 || part[1].sm.smCount == 0) throw Fail(SSD_CONFIG, "green: SM split left no speculator SMs");
+  for (int i = 0; i < 2; ++i) {
+    CUdevResourceDesc d;
+    DRV(gen(&d, &part[i], 1));
+    DRV(create(&ctx[i], d, CUdevice(device), CU_GREEN_CTX_DEFAULT_STREAM));
+    CUstream s;
+    DRV(mkstream(&s, ctx[i], CU_STREAM_NON_BLOCKING, 0));
+    st[i] = reinterpret_cast<cudaStream_t>(s);
+    sms[i] = int(part[i].sm.smCount);
+  }
+}
+
 // 2-D bf16 [rows][cols] row-major, box = 64 (K) x box_rows, 128B swizzle.
 static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   init_encode();
@@ -248,6 +287,16 @@ struct Engine {
   // both streams' GEMMs run at once (SSD_B200_SPLIT_SMS=<target>,<draft>;
   // 0 = all SMs, the default: no partition measured faster, profiles/)
   int split_t = 0, split_d = 0;
+  // colocated SSD: true SM partition through two CUDA green contexts
+  // (SSD_B200_GREEN=<verifier SMs>): the round graph's verifier branch runs
+  // on green_v SMs, the speculator branch on the rest; 0 = shared SMs
+  int green_v = 0, green_s = 0;
+  CUgreenCtx green_ctx[2] = {nullptr, nullptr};
+  cudaStream_t gsv = nullptr, gss = nullptr;
+  // branch steps from green_tail on run on the whole device after the
+  // verifier finished (SSD_B200_GREEN_TAIL; -1 = every step on the partition)
+  int green_tail = -1;
+  cudaEvent_t ev_tail = nullptr;
   // paged main cache (ssd_engine_set_block_table): prompt tokens of each lane
   // whose KV is already in its pages (prefix-cache hits): prefill starts there
   std::vector<int> prefill_skip;
@@ -260,11 +309,13 @@ struct Engine {
   Inbox** peers_dev = nullptr;       // device copy of `peers`
   int* send_counter = nullptr;
   int seq_base = 0;                  // advances by rounds + 2 per split run
-  // In-graph round profile (ssd_profile_ssd_round): timing events recorded by
-  // event-record nodes of the captured round graph (cudaEventRecordExternal)
-  // at the segment boundaries of both streams; kProfMarks per round.
+  // In-graph round profile (ssd_profile_ssd_round): one-thread stamp kernels
+  // of the captured round graph write %globaltimer at the segment boundaries
+  // of both streams (event-record nodes cannot time streams of green
+  // contexts: cudaEventElapsedTime rejects them, scripts/green_probe.cu).
   int prof_on = 0;
-  cudaEvent_t prof_ev[32] = {};
+  unsigned long long* prof_ts = nullptr;  // [32] device
+  unsigned long long prof_h[32] = {};
   // asynchronous pre-speculation session (ssd_prespec_begin / ssd_cache_*)
   cudaEvent_t ev_prespec = nullptr, ev_user = nullptr;
   int pre_active = 0, pre_count = 0, pre_kb = 0, pre_keys_valid = 0;
@@ -301,8 +352,16 @@ static void d2h(Engine& E, void* dst, const void* src, size_t bytes) {
 // 5 keys + branch streams done, 6 + 2j branch step j forward done, 7 + 2j
 // its token pick done (j < 8), 31 lookup done.
 constexpr int kMarkRoundEnd = 31;
+__global__ void stamp_kernel(unsigned long long* ts, int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  ts[i] = t;
+}
+
 static void mark(Engine& E, int i, cudaStream_t s) {
-  if (E.prof_on) CK(cudaEventRecordWithFlags(E.prof_ev[i], s, cudaEventRecordExternal));
+  if (!E.prof_on) return;
+  stamp_kernel<<<1, 1, 0, s>>>(E.prof_ts, i);
+  KCHECK();
 }
 
 static void rope_tables(const ssd_model_shape& s, std::vector<float>& cs, std::vector<float>& sn) {
@@ -1163,6 +1222,39 @@ static void draft_lanes(Engine& E, int K, const ssd_scheme& sc, int origin, int 
   ++E.launches;
 }
 
+// Colocated SSD round on disjoint SM sets (green contexts): the verifier
+// branch on `want_v` SMs, the speculator branch on the rest. The round graph
+// is re-captured at the next run.
+static void drop_green(Engine& E) {
+  for (cudaStream_t st : {E.gsv, E.gss})
+    if (st) cudaStreamDestroy(st);
+  if (E.green_ctx[0] || E.green_ctx[1]) {
+    auto destroy = driver_fn<PFN_cuGreenCtxDestroy_v12040>("cuGreenCtxDestroy");
+    for (CUgreenCtx& g : E.green_ctx) {
+      if (g) destroy(g);
+      g = nullptr;
+    }
+  }
+  E.gsv = E.gss = nullptr;
+  E.green_v = E.green_s = 0;
+  E.ssd_graph_key.clear();
+}
+
+static void set_green(Engine& E, int want_v) {
+  drop_green(E);
+  if (want_v <= 0) return;
+  if (E.role != SSD_ROLE_COLOCATED || E.T.tp_size > 1)
+    throw Fail(SSD_CONFIG, "sm_partition: colocated single-GPU engines only");
+  if (want_v >= E_num_sms) throw Fail(SSD_CONFIG, "sm_partition: verifier SMs must leave SMs for the speculator");
+  cudaStream_t st[2];
+  int sms[2];
+  make_green_streams(E.dev, want_v, E.green_ctx, st, sms);
+  E.gsv = st[0];
+  E.gss = st[1];
+  E.green_v = sms[0];
+  E.green_s = sms[1];
+}
+
 // Verification of st->spec against the target (verify forward M = K+1,
 // then the decision kernels).
 static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_scheme& ds, double scale, int use_draft_stream,
@@ -1194,8 +1286,32 @@ static void verify_round(Engine& E, int K, const ssd_scheme& ts, const ssd_schem
 // of each entry (build_cache's next_lookahead; K in the loops).
 static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, const ssd_scheme& sc, int parity,
                          cudaStream_t s, int nl = 1, cudaEvent_t before_streams = nullptr, int Kb = -1,
-                         cudaEvent_t after_extend = nullptr) {
+                         cudaEvent_t after_extend = nullptr, int jb = -1, int je = -1) {
   if (Kb < 0) Kb = K;
+  if (je < 0) je = Kb;
+  if (nl > 1) Bl = nl * B;
+  const DScheme ds = dscheme(sc);
+  float* rows = E.brows[parity];
+  const bool sampled = sc.temperature > 0.0;
+  // jb >= 0: branch steps [jb, je) only (the green tail: the last steps run
+  // on the whole device once the verifier is done); else everything up to je
+  auto steps = [&](int j0, int j1) {
+    for (int j = j0; j < j1 && Bl > 0; ++j) {
+      prep_branch_kernel<<<(Bl + 127) / 128, 128, 0, s>>>(E.st, E.bk + lo, E.btok + lo, E.bt, E.P_b, Bl, j,
+                                                           E.D.s.max_ctx, nl > 1 ? B : 0, E.D.lane_S);
+      float* out = rows + size_t(j) * Bl * E.V;
+      forward(E, E.D, E.P_b, Bl, out, s);
+      if (j < 8) mark(E, 6 + 2 * j, s);
+      row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * Kb + j : nullptr, Kb, E.bt + j, Kb, s);
+      KCHECK();
+      if (j < 8) mark(E, 7 + 2 * j, s);
+      E.launches += 1;
+    }
+  };
+  if (jb >= 0) {
+    steps(jb, je);
+    return;
+  }
   prep_chain_kernel<<<nl, 32, 0, s>>>(E.st, E.hist, E.P_x, K + 1, E.hist_stride, E.D.lane_S, E.D.km);
   KCHECK();
   forward(E, E.D, E.P_x, nl * (K + 1), E.xrows, s);
@@ -1203,26 +1319,11 @@ static void prespeculate(Engine& E, int K, int B, int lo, int Bl, int max_f, con
   mark(E, 4, s);
   row_keys(E, E.xrows, K + 1, E.V, max_f, E.st, nullptr, K, s, nl, B);
   if (before_streams) CK(cudaStreamWaitEvent(s, before_streams, 0));
-  const bool sampled = sc.temperature > 0.0;
   branch_streams_kernel<<<nl, 128, 0, s>>>(E.st, B, E.bu, sampled ? 1 : 0);
   KCHECK();
   mark(E, 5, s);
   E.launches += 2;
-  if (nl > 1) Bl = nl * B;
-  if (Bl <= 0) return;
-  const DScheme ds = dscheme(sc);
-  float* rows = E.brows[parity];
-  for (int j = 0; j < Kb; ++j) {
-    prep_branch_kernel<<<(Bl + 127) / 128, 128, 0, s>>>(E.st, E.bk + lo, E.btok + lo, E.bt, E.P_b, Bl, j,
-                                                         E.D.s.max_ctx, nl > 1 ? B : 0, E.D.lane_S);
-    float* out = rows + size_t(j) * Bl * E.V;
-    forward(E, E.D, E.P_b, Bl, out, s);
-    if (j < 8) mark(E, 6 + 2 * j, s);
-    row_pick(E, out, size_t(E.V), Bl, E.V, ds, sampled ? E.bu + size_t(lo) * Kb + j : nullptr, Kb, E.bt + j, Kb, s);
-    KCHECK();
-    if (j < 8) mark(E, 7 + 2 * j, s);
-    E.launches += 1;
-  }
+  steps(0, je);
 }
 
 static void upload_plans(Engine& E, const ssd_plan& p, const ssd_plan& b, int K, int& B, int& max_f) {
@@ -1443,6 +1544,15 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
     CK(cudaStreamCreateWithPriority(&E.sv, cudaStreamNonBlocking, lo));
     CK(cudaStreamCreateWithPriority(&E.ss, cudaStreamNonBlocking, prio ? hi : lo));
   }
+  if (role == SSD_ROLE_COLOCATED && tp_size == 1) {
+    // default: 3/8 of the SMs for the verifier (bench workload sweep,
+    // profiles/r02g_summary.md); SSD_B200_GREEN=<SMs> overrides, 0 = shared
+    int want = E_num_sms * 3 / 8;
+    if (const char* gv = std::getenv("SSD_B200_GREEN")) want = std::atoi(gv);
+    if (const char* gt = std::getenv("SSD_B200_GREEN_TAIL")) E.green_tail = std::atoi(gt);
+    CK(cudaEventCreateWithFlags(&E.ev_tail, cudaEventDisableTiming));
+    set_green(E, want);
+  }
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_verified, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_join, cudaEventDisableTiming));
@@ -1545,11 +1655,11 @@ ssd_status ssd_engine_destroy(ssd_engine* h) {
   for (void* p : E.owned) cudaFree(p);
   for (cudaStream_t st : {E.sv, E.ss})
     if (st) cudaStreamDestroy(st);
-  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1, E.ev_prespec, E.ev_user, E.ev_extended})
+  drop_green(E);
+  for (cudaEvent_t ev : {E.ev_fork, E.ev_verified, E.ev_join, E.ev_t0, E.ev_t1, E.ev_prespec, E.ev_user, E.ev_extended, E.ev_tail})
     if (ev) cudaEventDestroy(ev);
   if (E.pin_rng) cudaFreeHost(E.pin_rng);
-  for (cudaEvent_t ev : E.prof_ev)
-    if (ev) cudaEventDestroy(ev);
+  if (E.prof_ts) cudaFree(E.prof_ts);
   cudaGetLastError();  // teardown errors must not surface in a later call
   delete h;
   API_END
@@ -1725,10 +1835,12 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   // branch-row buffers (the next round's verifier reads this round's rows).
   E.launches = 0;
   // verifier and speculator GEMMs on disjoint SM sets so both streams run at once
-  E.T.gemm_ctas = E.split_t;
-  E.D.gemm_ctas = E.split_d;
+  E.T.gemm_ctas = E.green_v ? E.green_v : E.split_t;
+  E.D.gemm_ctas = E.green_v ? E.green_s : E.split_d;
   const long long small_saved = E.small_gemm_bytes;
-  E.small_gemm_bytes = std::max(E.small_gemm_bytes, E.corun_small_gemm_bytes);  // co-running streams
+  // co-running streams on shared SMs: the co-resident (small-budget) GEMM
+  // configuration; on disjoint partitions each stream keeps the full one
+  if (!E.gsv) E.small_gemm_bytes = std::max(E.small_gemm_bytes, E.corun_small_gemm_bytes);
   g_attn_smem_cap_kb = E.corun_attn_kb;
   struct Uncap {
     Engine& e;
@@ -1740,10 +1852,10 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   std::snprintf(keybuf, sizeof keybuf, "%d %d %d %d | %d %d %.17g %.17g | %d %d %.17g %.17g | %.17g | %d %d | %d %d | %p %lld %d",
                 K, B, max_f, nb, c->scheme.kind, c->scheme.fan_out, c->scheme.temperature, c->scheme.downweight,
                 c->target_scheme.kind, c->target_scheme.fan_out, c->target_scheme.temperature,
-                c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.split_t, E.split_d,
+                c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.T.gemm_ctas, E.D.gemm_ctas,
                 static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
   const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "") + " mode" + std::to_string(mode) +
-                          " vae" + std::to_string(E.verify_after_extend) +
+                          " vae" + std::to_string(E.verify_after_extend) + " tail" + std::to_string(E.green_tail) +
                           (tr.i ? " tr" : "") + " n0 " + std::to_string(n0);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
@@ -1751,36 +1863,54 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
     E.ssd_graphs.clear();
     E.ssd_graph_key.clear();
     GraphSet gs;
+    // green partition: the round's two branches are captured on the green streams
+    cudaStream_t cv = E.gsv ? E.gsv : sv, cs = E.gss ? E.gss : ss;
   for (int parity = 0; parity < 2; ++parity) {
-    gs.g.push_back(capture_graph(sv, [&] {
-      mark(E, 0, sv);
-      CK(cudaEventRecord(E.ev_fork, sv));
-      CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
-      mark(E, 3, ss);
+    gs.g.push_back(capture_graph(cv, [&] {
+      mark(E, 0, cv);
+      CK(cudaEventRecord(E.ev_fork, cv));
+      CK(cudaStreamWaitEvent(cs, E.ev_fork, 0));
+      mark(E, 3, cs);
+      cudaStream_t cend = cs;  // the speculator's last stream (lookup, join)
       if (mode == 1) {
         // verify first on the sequence stream; extend + keys overlap it, the
         // branch streams / steps follow it (their base is drawn after verify)
-        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 1, sv, nb);
-        CK(cudaEventRecord(E.ev_verified, sv));
-        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, E.ev_verified);
+        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 1, cv, nb);
+        CK(cudaEventRecord(E.ev_verified, cv));
+        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, cs, nb, E.ev_verified);
       } else {
         // verify_after_extend: the verify forward starts when the extend
         // forward has finished, so the speculator's first (critical-path)
         // forward does not share HBM with the verifier's heaviest GEMMs
-        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, nullptr, -1,
-                     E.verify_after_extend ? E.ev_extended : nullptr);
-        if (E.verify_after_extend) CK(cudaStreamWaitEvent(sv, E.ev_extended, 0));
-        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, sv, nb);
-        CK(cudaEventRecord(E.ev_verified, sv));
-        CK(cudaStreamWaitEvent(ss, E.ev_verified, 0));
+        const int tail = E.gsv && E.green_tail >= 0 && E.green_tail < K ? E.green_tail : -1;
+        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, cs, nb, nullptr, -1,
+                     E.verify_after_extend ? E.ev_extended : nullptr, -1, tail);
+        if (E.verify_after_extend) CK(cudaStreamWaitEvent(cv, E.ev_extended, 0));
+        verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, cv, nb);
+        CK(cudaEventRecord(E.ev_verified, cv));
+        CK(cudaStreamWaitEvent(cs, E.ev_verified, 0));
+        if (tail >= 0) {
+          // the verifier is done: the remaining branch steps on every SM
+          // (ordinary stream, uncapped GEMM grids, the full-budget configs)
+          CK(cudaEventRecord(E.ev_tail, cs));
+          CK(cudaStreamWaitEvent(ss, E.ev_tail, 0));
+          const int dcap = E.D.gemm_ctas;
+          const long long small = E.small_gemm_bytes;
+          E.D.gemm_ctas = 0;
+          E.small_gemm_bytes = small_saved;
+          prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, nullptr, -1, nullptr, tail, K);
+          E.D.gemm_ctas = dcap;
+          E.small_gemm_bytes = small;
+          cend = ss;
+        }
       }
-      lookup_kernel<<<1, 32, 0, ss>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V, E.cum,
-                                      d_out, d_hit, mode, tr);
+      lookup_kernel<<<1, 32, 0, cend>>>(E.st, nb, E.keys, max_f, E.offs, E.bt, E.brows[parity], 0, nb * B, B, E.V,
+                                        E.cum, d_out, d_hit, mode, tr);
       KCHECK();
-      mark(E, kMarkRoundEnd, ss);
+      mark(E, kMarkRoundEnd, cend);
       ++E.launches;
-      CK(cudaEventRecord(E.ev_join, ss));
-      CK(cudaStreamWaitEvent(sv, E.ev_join, 0));
+      CK(cudaEventRecord(E.ev_join, cend));
+      CK(cudaStreamWaitEvent(cv, E.ev_join, 0));
     }));
   }
     E.ssd_graphs = gs.g;
@@ -1798,12 +1928,9 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
   for (int64_t r = 0; r < R; ++r) {
     CK(cudaGraphLaunch(E.ssd_graphs[size_t(r & 1)], sv));
     if (E.prof_on && prof) {  // in-graph segment times of this round (one host sync per round)
+      CK(cudaMemcpyAsync(E.prof_h, E.prof_ts, sizeof E.prof_h, cudaMemcpyDeviceToHost, sv));
       CK(cudaStreamSynchronize(sv));
-      auto el = [&](int a, int b) {
-        float v = 0.f;
-        CK(cudaEventElapsedTime(&v, E.prof_ev[a], E.prof_ev[b]));
-        return double(v);
-      };
+      auto el = [&](int a, int b) { return 1e-6 * double(static_cast<long long>(E.prof_h[b] - E.prof_h[a])); };
       prof[0] += el(0, kMarkRoundEnd);
       prof[1] += el(0, 1);
       prof[2] += el(1, 2);
@@ -1952,8 +2079,7 @@ ssd_status ssd_profile_ssd_round(ssd_engine* h, const int32_t* prompt, int32_t n
   Engine& E = h->e;
   CK(cudaSetDevice(E.dev));
   if (!out_ms) throw Fail(SSD_CONFIG, "profile_ssd_round: null output");
-  for (int i = 0; i < 32; ++i)
-    if (!E.prof_ev[i]) CK(cudaEventCreate(&E.prof_ev[i]));
+  if (!E.prof_ts) E.prof_ts = dalloc<unsigned long long>(32);
   double acc[10] = {0};
   E.prof_on = 1;
   struct Off {
@@ -2752,6 +2878,19 @@ ssd_status ssd_engine_clear_block_tables(ssd_engine* h) {
   E.page_tokens = 0;
   E.prefill_skip.clear();
   E.ssd_graph_key.clear();
+  API_END
+}
+
+ssd_status ssd_engine_sm_partition(ssd_engine* h, int32_t verifier_sms, int32_t* out_v, int32_t* out_s) {
+  API_BEGIN
+  Engine& E = h->e;
+  CK(cudaSetDevice(E.dev));
+  if (verifier_sms >= 0) {
+    CK(cudaDeviceSynchronize());  // no round graph of this engine in flight
+    set_green(E, verifier_sms);
+  }
+  if (out_v) *out_v = E.green_v;
+  if (out_s) *out_s = E.green_s;
   API_END
 }
 
