@@ -2739,7 +2739,28 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   Model& m = which == 0 ? E.T : E.D;
   need(m, "profile_forward");
   if (M < 1 || M > m.maxM || pos + M > m.s.max_ctx || iters < 1) throw Fail(SSD_TOO_LARGE, "profile: bad shape");
+  // SSD_B200_PROFILE_PART=v|s: on the verifier / speculator partition of
+  // the colocated round (its green stream and GEMM grid cap); the timing
+  // events stay on the ordinary stream (joined through events)
   cudaStream_t s = E.sv;
+  if (const char* pp = std::getenv("SSD_B200_PROFILE_PART"); pp && E.gsv && (pp[0] == 'v' || pp[0] == 's')) {
+    s = pp[0] == 'v' ? E.gsv : E.gss;
+    m.gemm_ctas = pp[0] == 'v' ? E.green_v : E.green_s;
+  }
+  struct Uncap {
+    Model& m;
+    ~Uncap() { m.gemm_ctas = 0; }
+  } uncap{m};
+  auto t_begin = [&] {
+    CK(cudaEventRecord(E.ev_t0, E.sv));
+    CK(cudaStreamWaitEvent(s, E.ev_t0, 0));
+  };
+  auto t_end = [&] {
+    CK(cudaEventRecord(E.ev_join, s));
+    CK(cudaStreamWaitEvent(E.sv, E.ev_join, 0));
+    CK(cudaEventRecord(E.ev_t1, E.sv));
+    CK(cudaEventSynchronize(E.ev_t1));
+  };
   m.ctx_bound = pos + M + 1;
   prep_prefill_kernel<<<1, kMaxM, 0, s>>>(E.hist, E.P_pre, pos, M, 0, m.km);
   KCHECK();
@@ -2761,16 +2782,14 @@ ssd_status ssd_profile_forward(ssd_engine* h, int32_t which, int32_t M, int32_t 
   };
   forward(E, m, E.P_pre, M, m.logits, s);  // warm
   gemms();
-  CK(cudaEventRecord(E.ev_t0, s));
+  t_begin();
   for (int i = 0; i < iters; ++i) forward(E, m, E.P_pre, M, m.logits, s);
-  CK(cudaEventRecord(E.ev_t1, s));
-  CK(cudaEventSynchronize(E.ev_t1));
+  t_end();
   float f_ms = 0.f;
   CK(cudaEventElapsedTime(&f_ms, E.ev_t0, E.ev_t1));
-  CK(cudaEventRecord(E.ev_t0, s));
+  t_begin();
   for (int i = 0; i < iters; ++i) gemms();
-  CK(cudaEventRecord(E.ev_t1, s));
-  CK(cudaEventSynchronize(E.ev_t1));
+  t_end();
   float g_ms = 0.f;
   CK(cudaEventElapsedTime(&g_ms, E.ev_t0, E.ev_t1));
   *ms_forward = f_ms / iters;

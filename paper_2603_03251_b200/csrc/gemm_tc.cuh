@@ -154,6 +154,28 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Converged-warp producer steps (one elected lane issues; warp-uniform
+// operands stay in uniform registers, see the MMA issuer).
+__device__ __forceinline__ void expect_bulk_elect(uint64_t* bar, uint32_t tx, void* dst, const void* src, uint32_t bytes,
+                                                  uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %4, [%0], %5;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(tx), "r"(smem_u32(dst)), "l"(src), "r"(bytes), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // PDL (programmatic dependent launch)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -181,6 +203,43 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// Issued by a converged warp: one elected lane issues (operands warp-uniform).
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// The four K = 16 MMAs of one 64-wide k-block (one swizzle atom: the
+// descriptors advance by 32 bytes = 2 in the >> 4 address field), in one asm
+// block so the descriptor adds stay next to the MMAs (fewer uniform-register
+// moves per MMA). acc: accumulate into D on the first MMA.
+__device__ __forceinline__ void mma4_bf16_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %4, %4;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -317,52 +376,57 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   pdl_launch();  // let the next kernel start its own prologue / weight prefetch
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- producer
+  if (warp == 0) {
+    // ---------------- producer (converged warp, elected issue)
     uint64_t pol_w;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
     const int n = u1 - u0;
     const int pre = n < S ? n : S;
     if (threadIdx.x == 0) TRACE(4, 0);
     for (int i = 0; i < pre; ++i) {  // weights only: independent of the previous kernel
-      mbar_expect_tx(&full[i], C::kStageBytes);
-      bulk_load(sA + i * kABytes, g.W + size_t(u0 + i) * (kABytes / 2), kABytes, &full[i], pol_w);
-      TRACE(0, i);
+      expect_bulk_elect(&full[i], C::kStageBytes, sA + i * kABytes, g.W + size_t(u0 + i) * (kABytes / 2), kABytes,
+                        pol_w);
+      if (lane == 0) TRACE(0, i);
     }
     pdl_wait();  // activations are produced by the previous kernel
     KTL_READY();
 #if SSD_KTL
-    if (blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][0] = ktl_now();
+    if (lane == 0 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][0] = ktl_now();
 #endif
     for (int i = 0; i < pre; ++i) {
       const int kb = ((u0 + i) % g.KU) * kKPS;
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
-        tma_load_2d(sB + i * C::kBBytes + h * C::kBBlock, &mapX, &full[i], (kb + h) * kBK, 0);
+        tma_load_2d_elect(sB + i * C::kBBytes + h * C::kBBlock, &mapX, &full[i], (kb + h) * kBK, 0);
     }
     for (int i = pre; i < n; ++i) {
       const int s = i % S;
       mbar_spin(&empty[s], ((i / S) - 1) & 1);
-      TRACE(3, i);
+      if (lane == 0) TRACE(3, i);
       const int u = u0 + i;
 #if SSD_GEMM_NO_B_RELOAD  // bandwidth experiment only: stale activations
-      mbar_expect_tx(&full[s], kABytes);
-      bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
+      expect_bulk_elect(&full[s], kABytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, pol_w);
 #else
-      mbar_expect_tx(&full[s], C::kStageBytes);
-      bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
+      expect_bulk_elect(&full[s], C::kStageBytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, pol_w);
       const int kb = (u % g.KU) * kKPS;
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
-        tma_load_2d(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kb + h) * kBK, 0);
+        tma_load_2d_elect(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kb + h) * kBK, 0);
 #endif
-      TRACE(0, i);
+      if (lane == 0) TRACE(0, i);
     }
-    prefetch_window(g.pf, kABytes);
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+    if (lane == 0) prefetch_window(g.pf, kABytes);
+  } else if (warp == 1) {
+    // ---------------- MMA issuer. The whole warp runs the loop, so the
+    // descriptors are warp-uniform values the compiler keeps in uniform
+    // registers, and one elected lane issues each tcgen05.mma / commit. (A
+    // lone lane-0 branch made every MMA a divergent ELECT / R2UR.BROADCAST
+    // loop of ~20 instructions: ~150 cycles per MMA, the issue rate, not the
+    // tensor core or HBM, bounded a CTA at ~55 GB/s — scripts/gemm_trace.py,
+    // profiles/r02g_summary.md.)
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
+    const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
     int seg = -1, cur_tile = -1;
     for (int i = 0; i < u1 - u0; ++i) {
       const int u = u0 + i, t = u / g.KU, s = i % S;
@@ -373,28 +437,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if (seg >= 2) mbar_spin(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
       }
       mbar_spin(&full[s], (i / S) & 1);
-      TRACE(1, i);
+      if (lane == 0) TRACE(1, i);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
+      static_assert(kBK == 64, "mma4: four K = 16 MMAs per k-block");
 #pragma unroll
       for (int h = 0; h < kKPS; ++h) {
-        const uint32_t a0 = smem_u32(sA + s * kABytes + h * kABlock);
-        const uint32_t b0 = smem_u32(sB + s * C::kBBytes + h * C::kBBlock);
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)
-          mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (!first || h || k) ? 1u : 0u);
+        // descriptor start address field = smem address >> 4 (< 2^14: no carry)
+        const uint64_t ad = adesc0 + uint64_t((s * kABytes + h * kABlock) >> 4);
+        const uint64_t bd = bdesc0 + uint64_t((s * C::kBBytes + h * C::kBBlock) >> 4);
+        mma4_bf16_elect(d, ad, bd, idesc, (!first || h) ? 1u : 0u);
       }
-      mma_commit(&empty[s]);
-      TRACE(2, i);
+      mma_commit_elect(&empty[s]);
+      if (lane == 0) TRACE(2, i);
 #if SSD_KTL
-      if (i + 1 == u1 - u0 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][1] = ktl_now();
+      if (lane == 0 && i + 1 == u1 - u0 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][1] = ktl_now();
 #endif
       const bool last = (u + 1 == u1) || ((u + 1) / g.KU != t);
-      if (last) mma_commit(&tfull[seg & 1]);
+      if (last) mma_commit_elect(&tfull[seg & 1]);
 #if SSD_KTL
       if (last && u + 1 == u1 && blockIdx.x < 160) {  // profiling: when the accumulator is complete
         mbar_wait(&tfull[seg & 1], (seg >> 1) & 1);
-        g_ktl_cta[g.dbg_seq & 63][blockIdx.x][7] = ktl_now();
+        if (lane == 0) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][7] = ktl_now();
       }
 #endif
     }
@@ -484,11 +548,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if (s_last) {
           // only the first contributing CTA can start before the tile
           const int first_slot = 2 * cf + (unit_begin(cf, U, P) >= t * g.KU ? 0 : 1);
-          // All partial loads of a (16 contributors x 4 tokens) block are in
-          // flight together (one L2 round trip instead of one per
-          // contributor), then summed in CTA order: the same order, hence the
-          // same bits, as a sequential reduction.
-          constexpr int kC = 16, kT = 4;
+          // All partial loads of a (kC contributors x kT tokens) block are in
+          // flight together, then summed in CTA order: the same order, hence
+          // the same bits, as a sequential reduction. kT covers every token
+          // up to NP = 32 (one L2 round trip for the usual <= 3 contributors
+          // of a stream-K tile; 4 tokens per round trip took ~9 us at M = 20,
+          // scripts/ktl.py)
+          constexpr int kT = NP <= 32 ? NP : 16, kC = NP <= 16 ? 4 : 3;
           for (int t0 = 0; t0 < g.M; t0 += kT) {
             float acc[kT];
 #pragma unroll

@@ -126,12 +126,37 @@ def test_batch_capacity_errors(tiny_batch):
         eng.run_ssd(_prompt(8), _cfg(P, 4, 4, 1, 0.0, [4] * 5, [4] * 5, "fast_random", 0, 0.0))
 
 
-def test_round_graph_cache_invalidation(tiny_batch):
+@pytest.fixture(scope="module")
+def tiny_batch_det(oracle_lib):
+    """The tiny pair on an engine with a fixed summation order
+    (SSD_B200_DETERMINISTIC=1 at creation): bit-identical reruns, also of
+    sampled configurations (the colocated default sums split GEMM tiles with
+    fp32 atomics, whose order varies from run to run, and sampled tiny-pair
+    streams flip at near-ties)."""
+    import os
+
+    import paper_2603_03251_b200 as P
+    from paper_2603_03251_b200.configs import shapes
+    ts, ds = shapes("tiny", max_ctx=1024)
+    old = os.environ.get("SSD_B200_DETERMINISTIC")
+    os.environ["SSD_B200_DETERMINISTIC"] = "1"
+    try:
+        eng = P.Engine(ts, ds, P.Pair(), max_branches=32, max_lookahead=8, max_batch=4)
+    finally:
+        if old is None:
+            os.environ.pop("SSD_B200_DETERMINISTIC", None)
+        else:
+            os.environ["SSD_B200_DETERMINISTIC"] = old
+    yield P, eng, None
+    eng.close()
+
+
+def test_round_graph_cache_invalidation(tiny_batch_det):
     """run_ssd reuses its captured round graphs while every baked-in parameter
     matches; interleaving configurations (lookahead, plans, batch, scheme,
     rounds) on one engine must give exactly the results of the first run of
     each configuration."""
-    P, eng, orc = tiny_batch
+    P, eng, orc = tiny_batch_det
     prompt = _prompt(12, seed=31)
     a = _cfg(P, 4, 6, 3, 0.0, [4] * 5, [4] * 5, "fast_random", 1, 0.0)
     b = _cfg(P, 3, 9, 3, 0.0, [2, 2, 2, 2], [2, 2, 2, 2], "fast_random", 2, 0.5)
