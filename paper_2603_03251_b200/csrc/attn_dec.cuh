@@ -29,6 +29,7 @@ namespace ssd {
 
 constexpr int kDecThreads = 256;
 constexpr int kDecBatch = 4;  // K-row passes whose loads are in flight together
+constexpr size_t kDecStaticSmem = 2 * kMaxM * sizeof(int);  // s_tj + s_tp
 
 // RoPE'd key element d of a K row x (fp32, head_dim hd) at cos / sin row
 // (c, s): the writer and the in-kernel recomputation use this one function
@@ -150,52 +151,71 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + size_t(bbase) * HD), "r"(bbytes & ~15u) : "memory");
     }
   }
+  // Everything that depends only on P and the RoPE tables happens before the
+  // PDL wait (P and the tables predate this forward): the key -> token map of
+  // this forward's tokens, the staged-key patch list, the query's and the
+  // appended key's cos / sin. After the wait only the QKV row is read.
+  __shared__ int s_tj[kMaxM], s_tp[kMaxM];  // token t -> visible key j (or -1), RoPE position (kDecStaticSmem)
+  for (int j = tid; j < nk; j += kDecThreads) ovr[j] = -1;
+  const int pos_m = P->pos[m];
+  constexpr int NQE = (G * HD + kDecThreads - 1) / kDecThreads;
+  float qcv[NQE], qsv[NQE];
+#pragma unroll
+  for (int r = 0; r < NQE; ++r) {
+    const int e = tid + r * kDecThreads, dd = (e % HD) % HALF;
+    qcv[r] = e < G * HD ? cos_t[size_t(pos_m) * HALF + dd] : 0.f;
+    qsv[r] = e < G * HD ? sin_t[size_t(pos_m) * HALF + dd] : 0.f;
+  }
+  __syncthreads();  // ovr initialised before the sets below
+  for (int t = tid; t < M; t += kDecThreads) {
+    const int j = visible_token_key(P, t, mb, main_len, bbase, blen);
+    s_tj[t] = j;
+    s_tp[t] = P->pos[t];
+    // appended: rope_append_kernel wrote this forward's rows before this
+    // launch (wide forwards), so every key is read from the cache
+    if (j >= 0 && !appended) ovr[j] = t;
+  }
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   KTL_READY();
 
   const size_t row_len = size_t(H + 2 * KVH) * HD;
-  // 1) keys of this forward's tokens visible to this query; rotated queries;
-  //    append of token m's K / V (this kv head) to the cache
-  for (int j = tid; j < nk; j += kDecThreads) ovr[j] = -1;
+  // 1) rotated queries; append of token m's K / V (this kv head) to the cache;
+  //    keys of this forward in the staged range patched
   if (nst > 0) tc::mbar_wait(bar, 0);  // staged rows landed before they are patched below
   __syncthreads();
-  // appended: rope_append_kernel wrote this forward's rows before this
-  // launch (wide forwards), so every key is read from the cache
-  for (int t = tid; t < M && !appended; t += kDecThreads) {
-    const int j = visible_token_key(P, t, mb, main_len, bbase, blen);
-    if (j >= 0) ovr[j] = t;
-  }
   // keys of this forward that fall in the staged range: patch the stale
   // staged rows with the recomputed ones (the writer's rounding), so scores
   // and P.V read every staged key from shared memory
   for (int e = tid; e < M * HD && ns > 0; e += kDecThreads) {
     const int t = e / HD, d = e % HD;
-    const int j = visible_token_key(P, t, mb, main_len, bbase, blen);
+    const int j = s_tj[t];
     if (j < 0 || j >= ns) continue;
-    const int pos = P->pos[t];
+    const int pos = s_tp[t];
     const float* x = qkv + size_t(t) * row_len + size_t(H + kvh) * HD;
     Ks[size_t(j) * HD + d] =
         __float2bfloat16_rn(rope_elem(x, d, HALF, cos_t + size_t(pos) * HALF, sin_t + size_t(pos) * HALF));
     Vs[size_t(j) * HD + d] = __float2bfloat16_rn(__ldcg(x + KVH * HD + d));
   }
   {
-    const int pos = P->pos[m];
-    const float* c = cos_t + size_t(pos) * HALF;
-    const float* s = sin_t + size_t(pos) * HALF;
-    for (int e = tid; e < G * HD; e += kDecThreads) {
+#pragma unroll
+    for (int r = 0; r < NQE; ++r) {
+      const int e = tid + r * kDecThreads;
+      if (e >= G * HD) break;
       const int gg = e / HD, d = e % HD;
       const float* x = qkv + size_t(m) * row_len + size_t(kvh * G + gg) * HD;
       const float a = __ldcg(x + d), b = __ldcg(x + (d < HALF ? d + HALF : d - HALF));
-      const float r = d < HALF ? __fsub_rn(__fmul_rn(a, c[d]), __fmul_rn(b, s[d]))
-                               : __fadd_rn(__fmul_rn(a, c[d - HALF]), __fmul_rn(b, s[d - HALF]));
-      qs[e] = r * scale;
+      const float rr = d < HALF ? __fsub_rn(__fmul_rn(a, qcv[r]), __fmul_rn(b, qsv[r]))
+                                : __fadd_rn(__fmul_rn(a, qcv[r]), __fmul_rn(b, qsv[r]));
+      qs[e] = rr * scale;
     }
+    const float* c = cos_t + size_t(pos_m) * HALF;
+    const float* sn = sin_t + size_t(pos_m) * HALF;
     const float* xk = qkv + size_t(m) * row_len + size_t(H + kvh) * HD;
     const float* xv = qkv + size_t(m) * row_len + size_t(H + KVH + kvh) * HD;
     const int slot = P->slot[m];
     for (int d = tid; d < HD && !appended; d += kDecThreads) {
-      kc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(rope_elem(xk, d, HALF, c, s));
+      kc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(rope_elem(xk, d, HALF, c, sn));
       vc[(size_t(kvh) * S + slot) * HD + d] = __float2bfloat16_rn(__ldcg(xv + d));
     }
   }

@@ -549,9 +549,22 @@ static void build_model(Model& m, const ssd_model_shape& sfull, const ssd_model_
 
 static int E_num_sms = 148;
 static int g_swiglu_whole = 1;  // SSD_B200_SWIGLU_WHOLE=0: always stream-K
-// ... when the tiles fill at least this many eighths of the SMs (1B gate/up:
-// 128 tiles on 148 SMs; SSD_B200_SWIGLU_WHOLE_FRAC8)
-static int g_swiglu_whole_frac8 = 6;
+// SwiGLU needs complete sums: a tile split between CTAs ends in partials +
+// a last-arriver reduction (~8 us after the last MMA at M = 20,
+// scripts/ktl.py), worth about this many 32 KB units of streaming
+// (SSD_B200_SWIGLU_REDUCE_UNITS)
+static int g_swiglu_reduce_units = 10;
+
+// Grid of a SwiGLU GEMM: w whole tiles per CTA (no partials) when that costs
+// no more units per CTA than stream-K plus its reduction (1B gate/up, 128
+// tiles: 1 tile per CTA on 148 SMs, 2 per CTA on a 92-SM partition), else
+// stream-K over `cap` CTAs (0).
+static int swiglu_whole_grid(int tiles, int KU, int cap) {
+  if (!g_swiglu_whole || cap < 1) return 0;
+  const int w = (tiles + cap - 1) / cap;
+  const long long sk = ((long long)tiles * KU + cap - 1) / cap;
+  return (long long)w * KU <= sk + g_swiglu_reduce_units ? (tiles + w - 1) / w : 0;
+}
 
 static void free_model(Model& m) {
   for (void* p : m.owned) cudaFree(p);
@@ -580,11 +593,10 @@ static void gemm_tc_launch(Model& m, const WMat& W, const bf16* X, int M, float*
 #endif
   const int cap = m.gemm_ctas > 0 ? std::min(m.gemm_ctas, E_num_sms) : E_num_sms * SSD_GEMM_CTAS_PER_SM;
   int grid = std::min(units, cap);
-  // SwiGLU needs complete sums: when the tiles nearly fill the SMs (1B
-  // gate/up: 128 tiles on 148 SMs) one whole tile per CTA beats stream-K,
-  // whose split tiles end in the partials + last-arriver reduction (~6 us
-  // after the last MMA, scripts/ktl.py)
-  if (EPI == EPI_SWIGLU && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * g_swiglu_whole_frac8) grid = tiles;
+  if (EPI == EPI_SWIGLU) {
+    const int gw = swiglu_whole_grid(tiles, KU, cap);
+    if (gw > 0) grid = gw;
+  }
   if (size_t(2) * grid * M * tc::kBM > m.ws_floats) throw Fail(SSD_TOO_LARGE, "gemm: split-K workspace");
   static int dbg_seq = 0;
   tc::GemmArgs g{W.w, W.N, KU, M, Y, ldy, Yb, ldyb, m.ws, m.counters, pf, dbg_seq++, EPI == EPI_SWIGLU ? 0 : atomic};
@@ -748,7 +760,7 @@ static void configure_kernels() {
   CK(cudaFuncSetAttribute(attention_cl_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(4, 128))));
   CK(cudaFuncSetAttribute(attention_cl_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_cl_smem(8, 128))));
   {
-    constexpr int kDecSmemMax = 227 * 1024;
+    constexpr int kDecSmemMax = 227 * 1024 - int(kDecStaticSmem);
     auto dec = [&](const void* f) {
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemMax));
       CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
@@ -848,7 +860,10 @@ struct PfCursor {
   int cap = 0;
   int parts(const WMat& w) const {
     const int tiles = (w.N + tc::kBM - 1) / tc::kBM;
-    if (w.swiglu && g_swiglu_whole && tiles <= cap && tiles * 8 >= cap * g_swiglu_whole_frac8) return tiles;  // as gemm_tc_launch
+    if (w.swiglu) {  // as gemm_tc_launch
+      const int gw = swiglu_whole_grid(tiles, int(gemm_units(w) / tiles), cap);
+      if (gw > 0) return gw;
+    }
     return int(std::min<long long>(gemm_units(w), cap));
   }
   // Window up to `ahead` bytes past the start of GEMM `next` (index in seq).
@@ -951,7 +966,7 @@ static int g_attn_smem_cap_kb = 227;
 template <int G, int HD>
 static void attn_dec_pick(Model& m, int M, const FwdParams* P, bf16* kc, bf16* vc, float scale, int kcap,
                           cudaStream_t s, Prefetch pf) {
-  constexpr size_t kSmemMax = 227 * 1024;
+  constexpr size_t kSmemMax = 227 * 1024 - kDecStaticSmem;  // the kernel's static token tables
   if (size_t(M) * m.s.n_kv_heads > size_t(2 * E_num_sms)) {
     // wide forward (prefill chunk): append every row first, then attend from the cache
     launch_pdl(rope_append_kernel, dim3(M, m.s.n_kv_heads), dim3(128), 0, s, (const float*)m.qkv, P,
@@ -1509,7 +1524,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
   if (const char* cm = std::getenv("SSD_B200_CL_MIN_M")) E.cl_min_m = std::max(1, std::atoi(cm));
   if (const char* cf = std::getenv("SSD_B200_CL_FUSED")) E.cl_fused = std::atoi(cf) != 0;
   if (const char* sw = std::getenv("SSD_B200_SWIGLU_WHOLE")) g_swiglu_whole = std::atoi(sw) != 0;
-  if (const char* swf = std::getenv("SSD_B200_SWIGLU_WHOLE_FRAC8")) g_swiglu_whole_frac8 = std::max(1, std::atoi(swf));
+  if (const char* swr = std::getenv("SSD_B200_SWIGLU_REDUCE_UNITS")) g_swiglu_reduce_units = std::max(0, std::atoi(swr));
   E.deterministic = role != SSD_ROLE_COLOCATED || tp_size > 1;
   if (const char* dt = std::getenv("SSD_B200_DETERMINISTIC")) E.deterministic = E.deterministic || std::atoi(dt) != 0;
   if (const char* cs = std::getenv("SSD_B200_CORUN_SMALL_GEMM_MB")) E.corun_small_gemm_bytes = std::atoll(cs) << 20;

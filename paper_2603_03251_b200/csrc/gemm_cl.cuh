@@ -118,17 +118,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   pdl_launch();
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
     // ---------------- producer: the rank's k-slice of every tile of the cluster
+    // (converged warp, elected issue: gemm_tc.cuh)
     uint64_t pol_w;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
     const int n = (t1 - t0) * nk;
     const int pre = n < S ? n : S;
     for (int i = 0; i < pre; ++i) {  // weights only: independent of the previous kernel
       const int u = (t0 + i / nk) * g.KU + k0 + i % nk;
-      mbar_expect_tx(&full[i], C::kStageBytes);
-      bulk_load(sA + i * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[i], pol_w);
+      expect_bulk_elect(&full[i], C::kStageBytes, sA + i * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, pol_w);
     }
     pdl_wait();  // activations are produced by the previous kernel
     KTL_READY();
@@ -137,17 +137,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
       if (i >= pre) {
         mbar_wait(&empty[s], ((i / S) - 1) & 1);
         const int u = (t0 + i / nk) * g.KU + kk;
-        mbar_expect_tx(&full[s], C::kStageBytes);
-        bulk_load(sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, &full[s], pol_w);
+        expect_bulk_elect(&full[s], C::kStageBytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes,
+                          pol_w);
       }
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
-        tma_load_2d(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kk * kKPS + h) * kBK, 0);
+        tma_load_2d_elect(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kk * kKPS + h) * kBK, 0);
     }
-    prefetch_window(g.pf, kABytes);
-  } else if (warp == 1 && lane == 0 && nk > 0) {
+    if (lane == 0) prefetch_window(g.pf, kABytes);
+  } else if (warp == 1 && nk > 0) {
     // ---------------- MMA issuer: one accumulation segment per tile
+    // (converged warp, elected issue: gemm_tc.cuh)
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
+    const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
     int i = 0;
     for (int t = t0; t < t1; ++t) {
       const int seg = t - t0;
@@ -159,15 +161,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int h = 0; h < kKPS; ++h) {
-          const uint32_t a0 = smem_u32(sA + s * kABytes + h * kABlock);
-          const uint32_t b0 = smem_u32(sB + s * C::kBBytes + h * C::kBBlock);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (j || h || k) ? 1u : 0u);
+          const uint64_t ad = adesc0 + uint64_t((s * kABytes + h * kABlock) >> 4);
+          const uint64_t bd = bdesc0 + uint64_t((s * C::kBBytes + h * C::kBBlock) >> 4);
+          mma4_bf16_elect(d, ad, bd, idesc, (j || h) ? 1u : 0u);
         }
-        mma_commit(&empty[s]);
+        mma_commit_elect(&empty[s]);
       }
-      mma_commit(&tfull[seg & 1]);
+      mma_commit_elect(&tfull[seg & 1]);
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: drain -> own smem partial -> signal -> reduce a row slice over DSMEM

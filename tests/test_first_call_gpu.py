@@ -16,6 +16,8 @@ import sys
 import numpy as np
 import pytest
 
+from parity import check_greedy_stream
+
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -81,13 +83,17 @@ def test_first_call_of_fresh_processes_is_exact(oracle_lib):
             for i, status, lg, st in res:
                 assert status == "ok", (i, status)
                 err = float(np.max(np.abs(lg - orc.logits(i % 2, _prompt(i)))))
-                o = orc.call({"op": "simulate", "mode": "harness", "lookahead": 4, "rounds": 4, "seed": 3,
-                              "prompt": _prompt(i), "scheme": {"temperature": 0.0}, "primary_plan": {"fan": [4] * 5},
-                              "backup_plan": {"fan": [4] * 5}, "timing": {"primary_time": 0.4}})
                 # corruption (a stale history / plan) moves logits by O(1-10);
-                # fp32 summation-order noise of the tiny pair is ~1e-2
-                if err >= CORRUPT_TOL or list(st) != o["streams"][0]:
-                    bad.append((i, err, list(st)[:6], o["streams"][0][:6]))
+                # fp32 summation-order noise of the tiny pair is ~1e-2. The
+                # greedy stream is checked teacher-forced against the oracle
+                # (a divergence only at a documented near-tie: parity.py)
+                try:
+                    check_greedy_stream(orc, 0, _prompt(i), list(st))
+                    stream_ok = True
+                except AssertionError as e:
+                    stream_ok = str(e)
+                if err >= CORRUPT_TOL or stream_ok is not True:
+                    bad.append((i, err, list(st)[:6], stream_ok))
     finally:
         stop.set()
         loader.join(timeout=120)

@@ -69,3 +69,19 @@ def test_staged_and_l2_attention_paths_agree():
     b = _logits({"SSD_B200_ATTN_STAGE": "1"}, n=9, steps=6)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert a[2] == b[2]
+
+
+@pytest.mark.parametrize("n", [1, 7])
+def test_swiglu_whole_tile_matches_stream_k(n):
+    """The SwiGLU GEMM with whole tiles per CTA (one TMEM accumulator over
+    all of K, the default when it costs no more than stream-K plus its
+    reduction) against forced stream-K (partials + ordered last-arriver
+    reduction): the same sums in another fp32 order, so logits agree within
+    one activation rounding flip (parity.FLIP_MAX) and the greedy SSD streams
+    are identical."""
+    from parity import FLIP_MAX
+    a = _logits({"SSD_B200_SWIGLU_WHOLE": "0"}, n=n, steps=6)
+    b = _logits({"SSD_B200_SWIGLU_WHOLE": "1"}, n=n, steps=6)
+    for x, y in zip(a[:2], b[:2]):
+        assert float(np.max(np.abs(x - y))) < FLIP_MAX
+    assert a[2] == b[2]
