@@ -29,6 +29,9 @@ namespace ssd {
 
 constexpr int kDecThreads = 256;
 constexpr int kDecBatch = 4;  // K-row passes whose loads are in flight together
+#ifndef SSD_DEC_BATCH_MINB2
+#define SSD_DEC_BATCH_MINB2 2  // two CTAs per SM (128 registers): 4 spilled (d20 1.27 -> 1.23 ms)
+#endif
 constexpr size_t kDecStaticSmem = 2 * kMaxM * sizeof(int);  // s_tj + s_tp
 
 // RoPE'd key element d of a K row x (fp32, head_dim hd) at cos / sin row
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
   constexpr int KPW = 32 / LPK;  // keys per warp pass
   constexpr int HALF = HD / 2;
   constexpr int NDC = HD / 8;    // 8-dim chunks of a row
+  constexpr int NBT = MINB == 2 ? SSD_DEC_BATCH_MINB2 : kDecBatch;
   constexpr int NKG = dec_nkg(HD);
   extern __shared__ __align__(16) float dsm[];
   float* qs = dsm;                       // [G][HD] rotated, scaled queries
@@ -231,11 +235,11 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
     for (int gg = 0; gg < G; ++gg)
 #pragma unroll
       for (int i = 0; i < 16; ++i) qr[gg][i] = qs[gg * HD + sub * 16 + i];
-    for (int jb = warp * KPW; jb < nk; jb += NW * KPW * kDecBatch) {
-      uint4 kr[kDecBatch][2];
-      int tk[kDecBatch];
+    for (int jb = warp * KPW; jb < nk; jb += NW * KPW * NBT) {
+      uint4 kr[NBT][2];
+      int tk[NBT];
 #pragma unroll
-      for (int u = 0; u < kDecBatch; ++u) {  // issue every load of the batch first
+      for (int u = 0; u < NBT; ++u) {  // issue every load of the batch first
         const int j = jb + u * NW * KPW + grp;
         tk[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tk[u] == -1) {
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
         }
       }
 #pragma unroll
-      for (int u = 0; u < kDecBatch; ++u) {
+      for (int u = 0; u < NBT; ++u) {
         const int j = jb + u * NW * KPW + grp;
         float kf[16];
         if (tk[u] == -1) {
@@ -313,11 +317,11 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
     for (int gg = 0; gg < G; ++gg)
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[gg][i] = 0.f;
-    for (int jb = kg; jb < nk; jb += NKG * kDecBatch) {
-      uint4 vr[kDecBatch];
-      int tv[kDecBatch];
+    for (int jb = kg; jb < nk; jb += NKG * NBT) {
+      uint4 vr[NBT];
+      int tv[NBT];
 #pragma unroll
-      for (int u = 0; u < kDecBatch; ++u) {
+      for (int u = 0; u < NBT; ++u) {
         const int j = jb + u * NKG;
         tv[u] = j < nk ? (j < ns ? -1 : ovr[j]) : -2;
         if (tv[u] == -1) {
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(kDecThreads, MINB) attention_dec_kernel(
         }
       }
 #pragma unroll
-      for (int u = 0; u < kDecBatch; ++u) {
+      for (int u = 0; u < NBT; ++u) {
         const int j = jb + u * NKG;
         if (tv[u] == -2) continue;
         float f[8];
