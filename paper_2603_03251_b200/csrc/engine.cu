@@ -296,6 +296,11 @@ struct Engine {
   // branch steps from green_tail on run on the whole device after the
   // verifier finished (SSD_B200_GREEN_TAIL; -1 = every step on the partition)
   int green_tail = -1;
+  // partitioned round: the extend forward (+ keys, branch streams) first on
+  // every SM, then verifier and branch steps on their partitions
+  // (SSD_B200_EXTEND_FULL=0: the extend on the speculator partition beside
+  // the verifier; measured 6.06 -> 5.95 ms per round, profiles/r02g_summary.md)
+  int extend_full = 1;
   cudaEvent_t ev_tail = nullptr;
   // paged main cache (ssd_engine_set_block_table): prompt tokens of each lane
   // whose KV is already in its pages (prefix-cache hits): prefill starts there
@@ -1565,6 +1570,7 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
     int want = E_num_sms * 3 / 8;
     if (const char* gv = std::getenv("SSD_B200_GREEN")) want = std::atoi(gv);
     if (const char* gt = std::getenv("SSD_B200_GREEN_TAIL")) E.green_tail = std::atoi(gt);
+    if (const char* ef = std::getenv("SSD_B200_EXTEND_FULL")) E.extend_full = std::atoi(ef) != 0;
     CK(cudaEventCreateWithFlags(&E.ev_tail, cudaEventDisableTiming));
     set_green(E, want);
   }
@@ -1870,7 +1876,7 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
                 c->target_scheme.downweight, c->accept_scale, E.T.ctx_bound, E.D.ctx_bound, E.T.gemm_ctas, E.D.gemm_ctas,
                 static_cast<void*>(E.ssd_log), E.small_gemm_bytes, g_attn_smem_cap_kb);
   const std::string key = std::string(keybuf) + (E.prof_on ? " prof" : "") + " mode" + std::to_string(mode) +
-                          " vae" + std::to_string(E.verify_after_extend) + " tail" + std::to_string(E.green_tail) +
+                          " vae" + std::to_string(E.verify_after_extend) + " tail" + std::to_string(E.green_tail) + " xf" + std::to_string(E.extend_full) +
                           (tr.i ? " tr" : "") + " n0 " + std::to_string(n0);
   if (key != E.ssd_graph_key || E.ssd_graphs.size() != 2) {
     for (auto g : E.ssd_graphs)
@@ -1898,9 +1904,23 @@ static void run_ssd_impl(Engine& E, const int32_t* prompt, int32_t n0, const ssd
         // forward has finished, so the speculator's first (critical-path)
         // forward does not share HBM with the verifier's heaviest GEMMs
         const int tail = E.gsv && E.green_tail >= 0 && E.green_tail < K ? E.green_tail : -1;
-        prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, cs, nb, nullptr, -1,
-                     E.verify_after_extend ? E.ev_extended : nullptr, -1, tail);
-        if (E.verify_after_extend) CK(cudaStreamWaitEvent(cv, E.ev_extended, 0));
+        if (E.gsv && E.extend_full) {
+          // the extend forward (+ keys, branch streams) first, on every SM;
+          // then the verifier and the branch steps on their partitions
+          CK(cudaStreamWaitEvent(ss, E.ev_fork, 0));
+          const int dcap = E.D.gemm_ctas;
+          E.D.gemm_ctas = 0;
+          prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, ss, nb, nullptr, -1, nullptr, -1, 0);
+          E.D.gemm_ctas = dcap;
+          CK(cudaEventRecord(E.ev_extended, ss));
+          CK(cudaStreamWaitEvent(cs, E.ev_extended, 0));
+          CK(cudaStreamWaitEvent(cv, E.ev_extended, 0));
+          prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, cs, nb, nullptr, -1, nullptr, 0, tail >= 0 ? tail : K);
+        } else {
+          prespeculate(E, K, B, 0, B, max_f, c->scheme, parity, cs, nb, nullptr, -1,
+                       E.verify_after_extend ? E.ev_extended : nullptr, -1, tail);
+          if (E.verify_after_extend) CK(cudaStreamWaitEvent(cv, E.ev_extended, 0));
+        }
         verify_round(E, K, c->target_scheme, c->scheme, c->accept_scale, 0, cv, nb);
         CK(cudaEventRecord(E.ev_verified, cv));
         CK(cudaStreamWaitEvent(cs, E.ev_verified, 0));
