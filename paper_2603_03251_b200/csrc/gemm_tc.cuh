@@ -400,21 +400,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       for (int h = 0; h < kKPS; ++h)
         tma_load_2d_elect(sB + i * C::kBBytes + h * C::kBBlock, &mapX, &full[i], (kb + h) * kBK, 0);
     }
+    int ku = (u0 + pre) % g.KU, s = pre % S;  // kept incrementally (no divisions in the loop)
+    uint32_t ph = pre / S - 1;                // parity of the empty phase awaited for unit i >= S
     for (int i = pre; i < n; ++i) {
-      const int s = i % S;
-      mbar_spin(&empty[s], ((i / S) - 1) & 1);
+      mbar_spin(&empty[s], ph & 1);
       if (lane == 0) TRACE(3, i);
       const int u = u0 + i;
 #if SSD_GEMM_NO_B_RELOAD  // bandwidth experiment only: stale activations
       expect_bulk_elect(&full[s], kABytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, pol_w);
 #else
       expect_bulk_elect(&full[s], C::kStageBytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes, pol_w);
-      const int kb = (u % g.KU) * kKPS;
+      const int kb = ku * kKPS;
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
         tma_load_2d_elect(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kb + h) * kBK, 0);
 #endif
       if (lane == 0) TRACE(0, i);
+      if (++ku == g.KU) ku = 0;
+      if (++s == S) { s = 0; ++ph; }
     }
     if (lane == 0) prefetch_window(g.pf, kABytes);
   } else if (warp == 1) {
@@ -427,16 +430,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // profiles/r02g_summary.md.)
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
     const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
-    int seg = -1, cur_tile = -1;
+    int seg = -1;
+    // tile position of unit u0 + i, kept incrementally (no divisions in the loop)
+    int ku = u0 % g.KU, s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < u1 - u0; ++i) {
-      const int u = u0 + i, t = u / g.KU, s = i % S;
-      const bool first = t != cur_tile;
+      const int u = u0 + i;
+      const bool first = i == 0 || ku == 0;
       if (first) {
         ++seg;
-        cur_tile = t;
         if (seg >= 2) mbar_spin(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
       }
-      mbar_spin(&full[s], (i / S) & 1);
+      mbar_spin(&full[s], ph);
       if (lane == 0) TRACE(1, i);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #if SSD_KTL
       if (lane == 0 && i + 1 == u1 - u0 && blockIdx.x < 160) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][1] = ktl_now();
 #endif
-      const bool last = (u + 1 == u1) || ((u + 1) / g.KU != t);
+      const bool last = (u + 1 == u1) || (ku + 1 == g.KU);
       if (last) mma_commit_elect(&tfull[seg & 1]);
 #if SSD_KTL
       if (last && u + 1 == u1 && blockIdx.x < 160) {  // profiling: when the accumulator is complete
@@ -461,6 +466,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if (lane == 0) g_ktl_cta[g.dbg_seq & 63][blockIdx.x][7] = ktl_now();
       }
 #endif
+      if (++ku == g.KU) ku = 0;
+      if (++s == S) { s = 0; ph ^= 1u; }
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: TMEM lanes (warp % 4) * 32 + lane
