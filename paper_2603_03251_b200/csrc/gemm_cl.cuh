@@ -132,17 +132,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
     }
     pdl_wait();  // activations are produced by the previous kernel
     KTL_READY();
+    // (tile, k-slice, stage, parity) kept incrementally: no divisions in the loop
+    int tt = t0, j = 0, s = 0;
+    uint32_t ph = 0xffffffffu;  // (i / S) - 1: the empty phase awaited for i >= S
     for (int i = 0; i < n; ++i) {
-      const int s = i % S, kk = k0 + i % nk;
+      const int kk = k0 + j;
       if (i >= pre) {
-        mbar_wait(&empty[s], ((i / S) - 1) & 1);
-        const int u = (t0 + i / nk) * g.KU + kk;
+        mbar_wait(&empty[s], ph & 1);
+        const int u = tt * g.KU + kk;
         expect_bulk_elect(&full[s], C::kStageBytes, sA + s * kABytes, g.W + size_t(u) * (kABytes / 2), kABytes,
                           pol_w);
       }
 #pragma unroll
       for (int h = 0; h < kKPS; ++h)
         tma_load_2d_elect(sB + s * C::kBBytes + h * C::kBBlock, &mapX, &full[s], (kk * kKPS + h) * kBK, 0);
+      if (++j == nk) { j = 0; ++tt; }
+      if (++s == S) { s = 0; ++ph; }
     }
     if (lane == 0) prefetch_window(g.pf, kABytes);
   } else if (warp == 1 && nk > 0) {
@@ -150,14 +155,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
     // (converged warp, elected issue: gemm_tc.cuh)
     constexpr uint32_t idesc = idesc_bf16(kBM, NP);
     const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_desc(smem_u32(sB));
-    int i = 0;
+    int s = 0;
+    uint32_t ph = 0;  // ring stage and parity, kept incrementally
     for (int t = t0; t < t1; ++t) {
       const int seg = t - t0;
       if (seg >= 2) mbar_wait(&tempty[seg & 1], ((seg >> 1) - 1) & 1);
       const uint32_t d = tmem + uint32_t((seg & 1) * C::kAccCols);
-      for (int j = 0; j < nk; ++j, ++i) {
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
+      for (int j = 0; j < nk; ++j) {
+        mbar_wait(&full[s], ph & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int h = 0; h < kKPS; ++h) {
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cl_kernel(const __grid_const
           mma4_bf16_elect(d, ad, bd, idesc, (j || h) ? 1u : 0u);
         }
         mma_commit_elect(&empty[s]);
+        if (++s == S) { s = 0; ph ^= 1u; }
       }
       mma_commit_elect(&tfull[seg & 1]);
     }
