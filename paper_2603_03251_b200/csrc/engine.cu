@@ -1572,7 +1572,14 @@ static ssd_status engine_create(const ssd_model_shape* target, const ssd_model_s
     if (const char* gt = std::getenv("SSD_B200_GREEN_TAIL")) E.green_tail = std::atoi(gt);
     if (const char* ef = std::getenv("SSD_B200_EXTEND_FULL")) E.extend_full = std::atoi(ef) != 0;
     CK(cudaEventCreateWithFlags(&E.ev_tail, cudaEventDisableTiming));
-    set_green(E, want);
+    try {
+      set_green(E, want);
+    } catch (const Fail&) {
+      // no green-context support (driver, MIG, MPS limits): the round runs
+      // on shared SMs; ssd_engine_sm_partition reports the error explicitly
+      drop_green(E);
+      cudaGetLastError();
+    }
   }
   CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&E.ev_verified, cudaEventDisableTiming));
